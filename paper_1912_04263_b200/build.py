@@ -1,0 +1,64 @@
+"""Build the engine's shared libraries in-tree (they travel with the gpurun snapshot).
+
+    python -m paper_1912_04263_b200.build [--force]
+
+* libqpcg_b200.so : CUDA engine + C-ABI, sm_100a only, --fmad=false (see
+                    csrc/common.cuh for why), -lineinfo for ncu source pages.
+* libqpcg_gen.so  : host C++ instance generators (counter RNG, parallel).
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+ROOT = os.path.dirname(HERE)
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+ENGINE_SO = os.path.join(HERE, "libqpcg_b200.so")
+GEN_SO = os.path.join(HERE, "libqpcg_gen.so")
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
+              "--extended-lambda", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+              f"-I{os.path.join(ROOT, 'include')}"]
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_engine(force: bool = False) -> str:
+    deps = glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        [os.path.join(ROOT, "include", "qpcg_b200.h")]
+    if force or _stale(ENGINE_SO, deps):
+        cmd = [NVCC, *NVCC_FLAGS, "-o", ENGINE_SO, os.path.join(CSRC, "engine.cu")]
+        print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    return ENGINE_SO
+
+
+def build_gen(force: bool = False) -> str:
+    src = os.path.join(CSRC, "gen.cpp")
+    if not os.path.exists(src):
+        return ""
+    if force or _stale(GEN_SO, [src]):
+        cmd = ["g++", "-std=c++17", "-O3", "-ffp-contract=off", "-fPIC", "-shared", "-pthread",
+               "-o", GEN_SO, src]
+        print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    return GEN_SO
+
+
+def build(force: bool = False) -> None:
+    build_engine(force)
+    build_gen(force)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

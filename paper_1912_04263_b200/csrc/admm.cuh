@@ -1,0 +1,831 @@
+// admm.cuh — device control block, deterministic grid reductions and the
+// fused ADMM/PCG vector + SpMV-epilogue kernels.
+//
+// Every scalar decision of the reference loop (solver.hpp:444-514 and
+// pcg_solve linsys.hpp:233-269) is taken on the device by the last block of a
+// reduction kernel, so the loops run without host synchronisation: in graph
+// mode the same kernels also drive CUDA-graph conditional nodes.
+#pragma once
+
+#include "spmv.cuh"
+
+namespace qpcg_b200 {
+
+enum PcgExit : uint32_t { kPcgConverged = 0, kPcgCap = 1, kPcgZeroRhs = 2 };
+enum ErrCode : uint32_t { kErrNone = 0, kErrInvalid = 1, kErrNotPD = 2 };
+
+// Device-resident control block (one per workspace).
+template <typename T>
+struct Ctl {
+  // settings (settings.hpp:25-42, in T)
+  T alpha, sigma, eps_abs, eps_rel, eps_pinf, eps_dinf, lambda, eps_min;
+  uint32_t max_iter, check_interval, rho_interval, pcg_cap;
+  // scaling scalars (scaling.hpp:43-56)
+  T c, c_inv, q_inf_orig, q_inf_scaled;
+  // ADMM state (SolverState, solver.hpp:103-134)
+  T rho, pcg_eps, last_rp, last_rd;
+  uint32_t iter, done, status, error;
+  uint32_t rho_update_count, residuals_current, is_check, admm_continue;
+  unsigned long long pcg_total;
+  // PCG (linsys.hpp:207-275)
+  T b_norm, thr, r_norm, best_norm, rm, alpha_cg, beta, curv;
+  uint32_t k, pcg_active, pcg_exit, improved;
+  // residual norms: scaled and unscaled (solver.hpp:460-475)
+  T rp_s, rd_s, ax_s, z_s, px_s, aty_s;
+  T rp_o, rd_o, ax_o, z_o, px_o, aty_o;
+  // certificates (solver.hpp:236-297, 318-325)
+  T dx_norm, dy_norm, support, qv;
+  uint32_t need_pinf, need_dinf, pinf_bad, dinf_bad;
+  unsigned long long atv_inf_bits, pv_inf_bits;
+  // objective (solver.hpp:525-532)
+  T objective;
+  // reductions / diagnostics
+  uint32_t red_counter, n_calls, n_checks, n_rho;
+  uint32_t inf_branch, rho_branch, diag_cap, pad_;
+};
+
+// diagnostics records (device side, converted to qpcg_pcg_call on the host)
+template <typename T>
+struct DiagRec {
+  uint32_t admm_iter, iterations;
+  T eps, rp, rd;
+  uint32_t converged, pad;
+};
+template <typename T>
+struct RhoRec {
+  uint32_t admm_iter, pad;
+  T before, after;
+};
+
+// Handles of the CUDA-graph conditional nodes (0 in eager mode).
+struct Handles {
+  unsigned long long admm = 0, pcg = 0, chk = 0, inf = 0, rho = 0;
+};
+
+__device__ __forceinline__ void set_cond(unsigned long long h, unsigned int v) {
+  if (h != 0ull) cudaGraphSetConditional((cudaGraphConditionalHandle)h, v);
+}
+
+// Device view of every workspace buffer.
+template <typename T>
+struct Dev {
+  uint32_t n, m;
+  Ctl<T>* ctl;
+  T* red;  // [kRedBlocks * kMaxQ] reduction partials
+  // scaled problem (ScaledProblem, scaling.hpp:57-68)
+  DevCsr<T> P, A, AT;
+  SpmvPlan<T> pP, pA, pAT;
+  T *q, *l, *u, *d, *e, *d_inv, *e_inv;
+  // original problem (for infeasibility tests and the objective)
+  DevCsr<T> Po, Ao, ATo;
+  SpmvPlan<T> pPo, pAo, pATo;
+  T *q_o, *l_o, *u_o;
+  // iterates
+  T *x, *z, *y, *xt, *zt, *dx, *dy;
+  // PCG workspace
+  T *b, *r, *p, *kp, *best, *dinv, *t, *diag_p, *diag_ata;
+  // residual workspace (ResidualData, solver.hpp:181-188)
+  T *ax, *px, *aty, *rdual;
+  // outputs (unscaled)
+  T *xo, *zo, *yo, *cert, *pxo;
+  // diagnostics
+  DiagRec<T>* calls;
+  uint32_t* checks;
+  RhoRec<T>* rhos;
+};
+
+constexpr int kMaxQ = 16;
+
+template <typename T>
+__host__ __device__ inline uint32_t red_grid(uint32_t len) {
+  uint32_t g = (len + kThreads - 1) / kThreads;
+  if (g > (uint32_t)kRedBlocks) g = kRedBlocks;
+  return g == 0 ? 1u : g;
+}
+
+// Block all-reduce (result in every thread), fixed tree.
+template <typename T, bool MAX>
+__device__ __forceinline__ T block_allreduce(T v, T* sm) {
+  v = MAX ? warp_max(v) : warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    T r = (l < kWarpsPerBlock) ? sm[l] : T(0);
+    r = MAX ? warp_max(r) : warp_sum(r);
+    if (l == 0) sm[32] = r;
+  }
+  __syncthreads();
+  return sm[32];
+}
+
+// Deterministic grid reduction of NQ quantities (mask bit q set = max, else
+// sum).  Returns true in every thread of the last block to arrive, with the
+// totals in tot[].  Partials are combined in block-index order.
+template <typename T, int NQ>
+__device__ bool grid_reduce(const T (&vals)[NQ], uint32_t max_mask, T* part, uint32_t* counter,
+                            T (&tot)[NQ]) {
+  __shared__ T sm[33];
+  __shared__ bool is_last;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const bool mx = (max_mask >> q) & 1u;
+    const T b = mx ? block_allreduce<T, true>(vals[q], sm) : block_allreduce<T, false>(vals[q], sm);
+    if (threadIdx.x == 0) part[q * gridDim.x + blockIdx.x] = b;
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t prev = atomicAdd(counter, 1u);
+    is_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return false;
+  __threadfence();
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const bool mx = (max_mask >> q) & 1u;
+    T a = T(0);
+    for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+      const T v = __ldcg(part + q * gridDim.x + i);
+      a = mx ? smax(a, v) : a + v;
+    }
+    tot[q] = mx ? block_allreduce<T, true>(a, sm) : block_allreduce<T, false>(a, sm);
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+  return true;
+}
+
+template <typename T>
+__device__ __forceinline__ T tabs(T v) {
+  return v < T(0) ? -v : v;
+}
+
+// atomicMax over non-negative floating values through their bit patterns
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* a, double v) {
+  atomicMax(a, (unsigned long long)__double_as_longlong(v));
+}
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* a, float v) {
+  atomicMax(a, (unsigned long long)__float_as_uint(v));
+}
+__host__ __device__ inline double bits_to_value(unsigned long long b, double) {
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)b);
+#else
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+#endif
+}
+__host__ __device__ inline float bits_to_value(unsigned long long b, float) {
+  const uint32_t u = (uint32_t)b;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(u);
+#else
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+#endif
+}
+
+// Sequential dot of P row r with gathered vector x (spmv of P, one row, in
+// stored order: bit-identical to sparse.hpp:289-295 for that row).
+template <typename T>
+__device__ __forceinline__ T prow_dot(const DevCsr<T>& P, uint32_t r, const T* x) {
+  T s = T(0);
+  const uint32_t b = P.rp[r], e = P.rp[r + 1];
+  for (uint32_t k = b; k < e; ++k) s += P.val[k] * x[P.ci[k]];
+  return s;
+}
+
+// =====================================================================
+// SpMV gathers and epilogues of the loop
+// =====================================================================
+
+// rhs pass over A^T (admm_step, solver.hpp:351-355) fused with the PCG r0
+// operator apply (linsys.hpp:218-219, 80-90): col0 = rho z - y, col1 = rho z~
+// (A x~_prev == z~ from the previous step, reused bit-exactly).
+template <typename T>
+struct GatherRhs {
+  const T *z, *y, *zt;
+  const Ctl<T>* ctl;
+  T rho;
+  __device__ __forceinline__ void init() { rho = ctl->rho; }
+  __device__ __forceinline__ void operator()(uint32_t c, T (&g)[2]) const {
+    g[0] = rho * __ldg(z + c) - __ldg(y + c);
+    g[1] = rho * __ldg(zt + c);
+  }
+};
+template <typename T>
+struct EpiRhs {
+  Dev<T> D;
+  T sigma;
+  __device__ __forceinline__ bool init() {
+    sigma = D.ctl->sigma;
+    return D.ctl->error == 0;
+  }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[2]) const {
+    const T rhs = s[0] + (sigma * D.x[r] - D.q[r]);
+    const T xt = D.xt[r];
+    const T kx = (prow_dot(D.P, r, D.xt) + sigma * xt) + s[1];
+    D.b[r] = rhs;
+    D.r[r] = kx - rhs;
+  }
+};
+
+// t = rho (A p)   (linsys.hpp:84-85)
+template <typename T>
+struct EpiAp {
+  T* t;
+  const Ctl<T>* ctl;
+  T rho;
+  __device__ __forceinline__ bool init() {
+    rho = ctl->rho;
+    return ctl->pcg_active != 0 && ctl->error == 0;
+  }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const { t[r] = s[0] * rho; }
+};
+
+// Kp = (P p + sigma p) + A^T t   (linsys.hpp:86-89)
+template <typename T>
+struct EpiKp {
+  Dev<T> D;
+  T sigma;
+  __device__ __forceinline__ bool init() {
+    sigma = D.ctl->sigma;
+    return D.ctl->pcg_active != 0 && D.ctl->error == 0;
+  }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const {
+    D.kp[r] = (prow_dot(D.P, r, D.p) + sigma * D.p[r]) + s[0];
+  }
+};
+
+// z~ = A x~ with the whole m-side ADMM update fused (solver.hpp:360-378);
+// col1 (check iterations only) = A x_new with x_new formed on the fly exactly
+// as solver.hpp:366-367 forms it, feeding compute_residuals' A x (:196).
+template <typename T>
+struct GatherAdmm {
+  const T *xt, *x;
+  const Ctl<T>* ctl;
+  T alpha, one_m_alpha;
+  bool two;
+  __device__ __forceinline__ void init() {
+    alpha = ctl->alpha;
+    one_m_alpha = T(1) - alpha;
+    two = ((ctl->iter + 1) % ctl->check_interval) == 0;
+  }
+  __device__ __forceinline__ void operator()(uint32_t c, T (&g)[2]) const {
+    const T a = __ldg(xt + c);
+    g[0] = a;
+    g[1] = two ? alpha * a + one_m_alpha * __ldg(x + c) : T(0);
+  }
+};
+template <typename T>
+struct EpiAdmm {
+  Dev<T> D;
+  T alpha, one_m_alpha, rho;
+  bool two;
+  __device__ __forceinline__ bool init() {
+    alpha = D.ctl->alpha;
+    one_m_alpha = T(1) - alpha;
+    rho = D.ctl->rho;
+    two = ((D.ctl->iter + 1) % D.ctl->check_interval) == 0;
+    return D.ctl->error == 0;
+  }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[2]) const {
+    const T zt = s[0];
+    const T zp = D.z[r], yp = D.y[r];
+    const T w = alpha * zt + one_m_alpha * zp + yp / rho;
+    const T zn = smin(smax(w, D.l[r]), D.u[r]);
+    const T yn = rho * (w - zn);
+    D.zt[r] = zt;
+    D.z[r] = zn;
+    D.y[r] = yn;
+    D.dy[r] = yn - yp;
+    if (two) D.ax[r] = s[1];
+  }
+};
+
+// plain store (A x for the initial / final residuals)
+template <typename T>
+struct EpiStore {
+  T* out;
+  __device__ __forceinline__ bool init() { return true; }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const { out[r] = s[0]; }
+};
+
+// A^T y with P x and r_dual fused (compute_residuals, solver.hpp:197-204)
+template <typename T>
+struct EpiDual {
+  Dev<T> D;
+  __device__ __forceinline__ bool init() { return D.ctl->error == 0; }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const {
+    const T px = prow_dot(D.P, r, D.x);
+    D.aty[r] = s[0];
+    D.px[r] = px;
+    D.rdual[r] = px + D.q[r] + s[0];
+  }
+};
+
+// certificate vectors formed on the fly (certificate_vectors, solver.hpp:318-325,
+// then normalised: check_primal/dual_infeasible :240-243, :275-278)
+template <typename T>
+struct GatherCertY {  // v_i = ((e_i dy_i) c_inv) * (1/|dy|)
+  const T *e, *dy;
+  const Ctl<T>* ctl;
+  T c_inv, s;
+  __device__ __forceinline__ void init() {
+    c_inv = ctl->c_inv;
+    s = T(1) / ctl->dy_norm;
+  }
+  __device__ __forceinline__ void operator()(uint32_t c, T (&g)[1]) const {
+    g[0] = ((__ldg(e + c) * __ldg(dy + c)) * c_inv) * s;
+  }
+};
+template <typename T>
+struct GatherCertX {  // v_i = (d_i dx_i) * (1/|dx|)
+  const T *d, *dx;
+  const Ctl<T>* ctl;
+  T s;
+  __device__ __forceinline__ void init() { s = T(1) / ctl->dx_norm; }
+  __device__ __forceinline__ void operator()(uint32_t c, T (&g)[1]) const {
+    g[0] = (__ldg(d + c) * __ldg(dx + c)) * s;
+  }
+};
+template <typename T>
+struct EpiNormMax {  // max |row result| into a bits slot (order-free => exact)
+  unsigned long long* slot;
+  const uint32_t* enable;
+  __device__ __forceinline__ bool init() { return *enable != 0; }
+  __device__ __forceinline__ void operator()(uint32_t, const T (&s)[1]) const {
+    atomic_max_nonneg(slot, tabs(s[0]));
+  }
+};
+template <typename T>
+struct EpiDualRows {  // per-row sign tests of check_dual_infeasible (:283-295)
+  const T *l, *u;
+  uint32_t* bad;
+  const uint32_t* enable;
+  T eps;
+  const Ctl<T>* ctl;
+  __device__ __forceinline__ bool init() {
+    eps = ctl->eps_dinf;
+    return *enable != 0;
+  }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const {
+    const T li = l[r], ui = u[r], av = s[0];
+    const bool lf = li != -(T)INFINITY, uf = ui != (T)INFINITY;
+    bool b = false;
+    if (lf && uf)
+      b = tabs(av) > eps;
+    else if (!uf && lf)
+      b = av < -eps;
+    else if (!lf && uf)
+      b = av > eps;
+    if (b) atomicOr(bad, 1u);
+  }
+};
+
+// =====================================================================
+// vector kernels
+// =====================================================================
+
+// PCG initialisation (linsys.hpp:203-233) after the fused rhs/r0 pass.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_pcg_init(Dev<T> D, Handles H) {
+  Ctl<T>* C = D.ctl;
+  if (C->error) return;
+  const uint32_t n = D.n;
+  T v[4] = {T(0), T(0), T(0), T(0)};  // max|b|, max|r|, r.y, #nonfinite(x~)
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const T ri = D.r[i];
+    const T yi = D.dinv[i] * ri;
+    D.p[i] = -yi;
+    const T xi = D.xt[i];
+    D.best[i] = xi;
+    v[0] = smax(v[0], tabs(D.b[i]));
+    v[1] = smax(v[1], tabs(ri));
+    v[2] += ri * yi;
+    if (!isfinite(xi)) v[3] += T(1);
+  }
+  T tot[4];
+  if (!grid_reduce<T, 4>(v, 0x3u, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  C->k = 0;
+  C->improved = 0;
+  C->pcg_exit = kPcgConverged;
+  uint32_t active = 0;
+  if (tot[3] != T(0)) {
+    C->error = kErrInvalid;  // pcg: warm start must be finite (linsys.hpp:203-205)
+    C->done = 1;
+  } else if (tot[0] == T(0)) {
+    C->pcg_exit = kPcgZeroRhs;  // linsys.hpp:208-213
+    C->b_norm = T(0);
+  } else {
+    C->b_norm = tot[0];
+    C->thr = C->pcg_eps * tot[0];
+    C->r_norm = tot[1];
+    C->best_norm = tot[1];
+    C->rm = tot[2];
+    active = (C->r_norm > C->thr) && !(C->rm == T(0));
+  }
+  C->pcg_active = active;
+  set_cond(H.pcg, active);
+}
+
+// curvature p.Kp and step length (linsys.hpp:246-253)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_pcg_dot(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (!C->pcg_active || C->error) return;
+  T v[1] = {T(0)};
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
+    v[0] += D.p[i] * D.kp[i];
+  T tot[1];
+  if (!grid_reduce<T, 1>(v, 0x0u, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  C->curv = tot[0];
+  if (tot[0] <= T(0)) {
+    C->error = kErrNotPD;  // NotPositiveDefiniteError (linsys.hpp:247-250)
+    C->done = 1;
+    C->pcg_active = 0;
+  } else {
+    C->alpha_cg = C->rm / tot[0];
+  }
+}
+
+// x += a p; r += a Kp; y = M^-1 r; r.y; |r|  (linsys.hpp:254-263)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_pcg_update(Dev<T> D, Handles H) {
+  Ctl<T>* C = D.ctl;
+  if (!C->pcg_active || C->error) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.pcg, 0);
+    return;
+  }
+  const T a = C->alpha_cg;
+  T v[2] = {T(0), T(0)};  // r.y, max|r|
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+    D.xt[i] += a * D.p[i];
+    const T ri = D.r[i] + a * D.kp[i];
+    D.r[i] = ri;
+    const T yi = D.dinv[i] * ri;
+    v[0] += ri * yi;
+    v[1] = smax(v[1], tabs(ri));
+  }
+  T tot[2];
+  if (!grid_reduce<T, 2>(v, 0x2u, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  const T rm_next = tot[0];
+  C->beta = rm_next / C->rm;
+  C->rm = rm_next;
+  C->k += 1;
+  C->r_norm = tot[1];
+  C->improved = tot[1] < C->best_norm;
+  if (C->improved) C->best_norm = tot[1];
+  uint32_t active = C->r_norm > C->thr;
+  if (active) {
+    if (C->k >= C->pcg_cap) {
+      C->pcg_exit = kPcgCap;  // linsys.hpp:235-241: return best iterate
+      active = 0;
+    } else if (C->rm == T(0)) {
+      active = 0;  // linsys.hpp:243
+    }
+  }
+  C->pcg_active = active;
+  set_cond(H.pcg, active);
+}
+
+// p = -y + beta p; best-iterate copy (linsys.hpp:259, 264-267)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_pcg_pupdate(Dev<T> D) {
+  const Ctl<T>* C = D.ctl;
+  if (C->error) return;
+  if (C->k == 0) return;  // nothing to do before the first update
+  const T beta = C->beta;
+  const bool imp = C->improved;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+    const T yi = D.dinv[i] * D.r[i];
+    D.p[i] = -yi + beta * D.p[i];
+    if (imp) D.best[i] = D.xt[i];
+  }
+}
+
+// PCG exit: x~ = 0 (b == 0) or best iterate (cap); PcgCall record.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_pcg_fin(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (C->error) return;
+  const uint32_t ex = C->pcg_exit;
+  if (ex != kPcgConverged) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
+      D.xt[i] = ex == kPcgZeroRhs ? T(0) : D.best[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    C->pcg_total += C->k;
+    if (C->n_calls < C->diag_cap) {
+      DiagRec<T> rec;
+      rec.admm_iter = C->iter + 1;
+      rec.iterations = C->k;
+      rec.eps = C->pcg_eps;
+      rec.rp = C->last_rp;
+      rec.rd = C->last_rd;
+      rec.converged = ex != kPcgCap;
+      rec.pad = 0;
+      D.calls[C->n_calls] = rec;
+    }
+    C->n_calls += 1;
+  }
+}
+
+// n-side relaxation (solver.hpp:366-368, 377) and the iteration counter.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_xupdate(Dev<T> D, Handles H) {
+  Ctl<T>* C = D.ctl;
+  if (C->error) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.chk, 0);
+    return;
+  }
+  const T alpha = C->alpha, oma = T(1) - alpha;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+    const T xp = D.x[i];
+    const T xn = alpha * D.xt[i] + oma * xp;
+    D.x[i] = xn;
+    D.dx[i] = xn - xp;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint32_t it = C->iter + 1;
+    C->iter = it;
+    C->residuals_current = 0;
+    const uint32_t chk = (it % C->check_interval) == 0;
+    C->is_check = chk;
+    set_cond(H.chk, chk);
+  }
+}
+
+// Residual norms (solver.hpp:205-206, 468-475) + termination (:476-495 start).
+// mode 0: loop check; mode 1: initial residuals (eps only); mode 2: final.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Handles H) {
+  Ctl<T>* C = D.ctl;
+  if (C->error) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.inf, 0);
+    return;
+  }
+  const uint32_t n = D.n, m = D.m;
+  const T c_inv = C->c_inv;
+  // 0 rp_s 1 ax_s 2 z_s 3 rp_o 4 ax_o 5 z_o 6 dy_norm | 7 rd_s 8 px_s 9 aty_s
+  // 10 rd_o' 11 px_o' 12 aty_o' 13 dx_norm
+  T v[14];
+#pragma unroll
+  for (int q = 0; q < 14; ++q) v[q] = T(0);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const T ax = D.ax[i], z = D.z[i], ei = D.e_inv[i];
+    const T rp = ax - z;
+    v[0] = smax(v[0], tabs(rp));
+    v[1] = smax(v[1], tabs(ax));
+    v[2] = smax(v[2], tabs(z));
+    v[3] = smax(v[3], tabs(rp * ei));
+    v[4] = smax(v[4], tabs(ax * ei));
+    v[5] = smax(v[5], tabs(z * ei));
+    v[6] = smax(v[6], tabs((D.e[i] * D.dy[i]) * c_inv));
+  }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const T rd = D.rdual[i], px = D.px[i], aty = D.aty[i], di = D.d_inv[i];
+    v[7] = smax(v[7], tabs(rd));
+    v[8] = smax(v[8], tabs(px));
+    v[9] = smax(v[9], tabs(aty));
+    v[10] = smax(v[10], tabs(rd * di));
+    v[11] = smax(v[11], tabs(px * di));
+    v[12] = smax(v[12], tabs(aty * di));
+    v[13] = smax(v[13], tabs(D.d[i] * D.dx[i]));
+  }
+  T tot[14];
+  if (!grid_reduce<T, 14>(v, 0x3fffu, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  C->rp_s = tot[0];
+  C->ax_s = tot[1];
+  C->z_s = tot[2];
+  C->rd_s = tot[7];
+  C->px_s = tot[8];
+  C->aty_s = tot[9];
+  C->rp_o = tot[3];
+  C->ax_o = tot[4];
+  C->z_o = tot[5];
+  C->rd_o = c_inv * tot[10];
+  C->px_o = c_inv * tot[11];
+  C->aty_o = c_inv * tot[12];
+  C->dy_norm = tot[6];
+  C->dx_norm = tot[13];
+  C->residuals_current = 1;
+  uint32_t inf = 0;
+  if (mode != 2) {
+    // adaptive_eps (linsys.hpp:170-179)
+    const T e = smax(C->lambda * t_sqrt(C->rp_s * C->rd_s), C->eps_min);
+    C->pcg_eps = e;
+    C->last_rp = C->rp_s;
+    C->last_rd = C->rd_s;
+  }
+  if (mode == 0) {
+    if (C->n_checks < C->diag_cap) D.checks[C->n_checks] = C->iter;
+    C->n_checks += 1;
+    // check_optimal (solver.hpp:222-230) on unscaled norms
+    const T eps_prim = C->eps_abs + C->eps_rel * smax(C->ax_o, C->z_o);
+    const T eps_dual = C->eps_abs + C->eps_rel * smax(smax(C->px_o, C->aty_o), C->q_inf_orig);
+    if (C->rp_o <= eps_prim && C->rd_o <= eps_dual) {
+      C->status = 0;  // solved
+      C->done = 1;
+    } else {
+      C->need_pinf = C->dy_norm != T(0);
+      C->need_dinf = C->dx_norm != T(0);
+      C->pinf_bad = 0;
+      C->dinf_bad = 0;
+      C->atv_inf_bits = 0ull;
+      C->pv_inf_bits = 0ull;
+      inf = C->need_pinf | C->need_dinf;
+    }
+  }
+  C->inf_branch = inf;
+  set_cond(H.inf, inf);
+}
+
+// Infeasibility tests' vector parts (support sum :248-262, q'v :281) and the
+// decision (solver.hpp:483-494).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_infeas(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (C->error || !C->inf_branch) return;
+  const uint32_t n = D.n, m = D.m;
+  const T c_inv = C->c_inv, eps_p = C->eps_pinf;
+  const T sy = C->need_pinf ? T(1) / C->dy_norm : T(0);
+  const T sx = C->need_dinf ? T(1) / C->dx_norm : T(0);
+  T v[3] = {T(0), T(0), T(0)};  // support, bad (max), q'v
+  const uint32_t stride = gridDim.x * blockDim.x;
+  if (C->need_pinf) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+      const T vi = ((D.e[i] * D.dy[i]) * c_inv) * sy;
+      const T neg = smin(vi, T(0)), pos = smax(vi, T(0));
+      const T li = D.l_o[i], ui = D.u_o[i];
+      if (li == -(T)INFINITY) {
+        if (neg < -eps_p) v[1] = T(1);
+      } else {
+        v[0] += li * neg;
+      }
+      if (ui == (T)INFINITY) {
+        if (pos > eps_p) v[1] = T(1);
+      } else {
+        v[0] += ui * pos;
+      }
+    }
+  }
+  if (C->need_dinf) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+      v[2] += D.q_o[i] * ((D.d[i] * D.dx[i]) * sx);
+  }
+  T tot[3];
+  if (!grid_reduce<T, 3>(v, 0x2u, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  C->support = tot[0];
+  C->qv = tot[2];
+  const T atv = bits_to_value(C->atv_inf_bits, T(0));
+  const T pv = bits_to_value(C->pv_inf_bits, T(0));
+  const bool primal = C->need_pinf && !(atv > eps_p) && tot[1] == T(0) && tot[0] < eps_p;
+  const bool dual = C->need_dinf && !(pv > C->eps_dinf) && (tot[2] < C->eps_dinf) &&
+                    C->dinf_bad == 0;
+  if (primal) {
+    C->status = 1;
+    C->done = 1;
+  } else if (dual) {
+    C->status = 2;
+    C->done = 1;
+  }
+}
+
+// decides the rho branch (solver.hpp:498)
+template <typename T>
+__global__ void k_rho_flag(Dev<T> D, Handles H) {
+  Ctl<T>* C = D.ctl;
+  const uint32_t f = !C->error && !C->done && (C->iter % C->rho_interval) == 0;
+  C->rho_branch = f;
+  set_cond(H.rho, f);
+}
+
+// adapt_rho (solver.hpp:302-314) from the last residuals and the current |z|
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_rho(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (!C->rho_branch) return;
+  T v[1] = {T(0)};
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.m; i += gridDim.x * blockDim.x)
+    v[0] = smax(v[0], tabs(D.z[i]));
+  T tot[1];
+  if (!grid_reduce<T, 1>(v, 0x1u, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  const T fl = T(1e-10);
+  const T rel_prim = C->last_rp / smax(smax(C->ax_s, tot[0]), fl);
+  const T rel_dual = C->last_rd / smax(smax(smax(C->px_s, C->aty_s), C->q_inf_scaled), fl);
+  const T rho = C->rho;
+  T next;
+  if (rel_prim == T(0) && rel_dual == T(0))
+    next = rho;
+  else if (rel_dual == T(0))
+    next = T(1e6);
+  else {
+    next = rho * t_sqrt(rel_prim / rel_dual);
+    if (next < T(1e-6)) next = T(1e-6);
+    else if (T(1e6) < next) next = T(1e6);
+  }
+  if (C->n_rho < C->diag_cap) {
+    RhoRec<T> rr;
+    rr.admm_iter = C->iter;
+    rr.pad = 0;
+    rr.before = rho;
+    rr.after = next;
+    D.rhos[C->n_rho] = rr;
+  }
+  C->n_rho += 1;
+  if (!(next > T(0))) {
+    C->error = kErrInvalid;  // kkt operator: rho must be positive
+    C->done = 1;
+    return;
+  }
+  C->rho = next;
+  C->rho_update_count += 1;
+}
+
+// Jacobi diagonal (linsys.hpp:142-146): (diag_p + sigma) + rho diag_ata
+template <typename T>
+__global__ void k_precond(Dev<T> D, int force) {
+  const Ctl<T>* C = D.ctl;
+  if (!force && !C->rho_branch) return;
+  if (C->error) return;
+  const T sigma = C->sigma, rho = C->rho;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+    const T dm = D.diag_p[i] + sigma + rho * D.diag_ata[i];
+    D.dinv[i] = T(1) / dm;
+  }
+}
+
+// loop condition (solver.hpp:444)
+template <typename T>
+__global__ void k_admm_cond(Dev<T> D, Handles H) {
+  Ctl<T>* C = D.ctl;
+  const uint32_t go = !C->done && !C->error && C->iter < C->max_iter;
+  C->admm_continue = go;
+  set_cond(H.admm, go);
+}
+
+// unscale_solution (scaling.hpp:209-222) and the certificate (solver.hpp:485, 491)
+template <typename T>
+__global__ void k_unscale(Dev<T> D) {
+  const Ctl<T>* C = D.ctl;
+  const T c_inv = C->c_inv;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint32_t i = t0; i < D.n; i += stride) D.xo[i] = D.d[i] * D.x[i];
+  for (uint32_t i = t0; i < D.m; i += stride) {
+    D.zo[i] = D.e_inv[i] * D.z[i];
+    D.yo[i] = (D.e[i] * D.y[i]) * c_inv;
+  }
+  if (C->status == 1) {
+    const T s = T(1) / C->dy_norm;
+    for (uint32_t i = t0; i < D.m; i += stride) D.cert[i] = ((D.e[i] * D.dy[i]) * c_inv) * s;
+  } else if (C->status == 2) {
+    const T s = T(1) / C->dx_norm;
+    for (uint32_t i = t0; i < D.n; i += stride) D.cert[i] = (D.d[i] * D.dx[i]) * s;
+  }
+}
+
+// objective = 0.5 x'(P x) + q'x on the original data (solver.hpp:530-531)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_objective(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  T v[2] = {T(0), T(0)};
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+    v[0] += D.xo[i] * D.pxo[i];
+    v[1] += D.q_o[i] * D.xo[i];
+  }
+  T tot[2];
+  if (!grid_reduce<T, 2>(v, 0x0u, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  if (C->status == 1)
+    C->objective = (T)INFINITY;
+  else if (C->status == 2)
+    C->objective = -(T)INFINITY;
+  else
+    C->objective = T(0.5) * tot[0] + tot[1];
+}
+
+// max-norm helper (q_inf etc.)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_infnorm(const T* v, uint32_t n, T* part,
+                                                     uint32_t* counter, T* out) {
+  T a[1] = {T(0)};
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    a[0] = smax(a[0], tabs(v[i]));
+  T tot[1];
+  if (!grid_reduce<T, 1>(a, 0x1u, part, counter, tot)) return;
+  if (threadIdx.x == 0) *out = tot[0];
+}
+
+}  // namespace qpcg_b200

@@ -1,0 +1,150 @@
+// common.cuh — shared device/host plumbing for the B200 ADMM/PCG engine.
+//
+// Build note: the whole engine is compiled with --fmad=false so that every
+// `a * b + c` rounds twice, exactly like the reference built with
+// -ffp-contract=off; setup kernels (Ruiz, symmetrize,
+// transpose, diag caches) are therefore bit-exact with the reference and the
+// iteration kernels differ only by summation order.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace qpcg_b200 {
+
+// ---------------------------------------------------------------- errors
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct NotPositiveDefinite : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct OutOfMemory : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  std::string msg = std::string(what) + " failed: " + cudaGetErrorString(e) + " (" + file + ":" +
+                    std::to_string(line) + ")";
+  if (e == cudaErrorMemoryAllocation) throw OutOfMemory(msg);
+  throw CudaError(msg);
+}
+#define CK(x) ::qpcg_b200::cuda_check((x), #x, __FILE__, __LINE__)
+#define CK_LAUNCH() ::qpcg_b200::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// ------------------------------------------------------------ constants
+constexpr int kNumSMs = 148;           // B200
+constexpr int kThreads = 256;          // default block size
+constexpr int kWarpsPerBlock = kThreads / 32;
+constexpr uint32_t kShortRowMax = 8;   // rows with <= 8 nnz: one thread per row
+constexpr uint32_t kChunk = 2048;      // nnz per warp work item (long rows split)
+constexpr int kRedBlocks = 2 * kNumSMs;  // fixed grid of reduction kernels (deterministic)
+
+__host__ __device__ inline uint32_t ceil_div(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------ CSR views
+template <typename T>
+struct DevCsr {
+  uint32_t rows = 0, cols = 0, nnz = 0;
+  T* val = nullptr;           // [nnz]
+  uint32_t* rp = nullptr;     // [rows + 1]
+  uint32_t* ci = nullptr;     // [nnz]
+};
+
+// ---------------------------------------------------------- warp helpers
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = v < w ? w : v;
+  }
+  return v;
+}
+
+// Deterministic block reductions (fixed tree); result valid in thread 0.
+template <typename T, int NT>
+__device__ __forceinline__ T block_sum(T v, T* sm) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  T r = T(0);
+  if (w == 0) {
+    r = (l < NT / 32) ? sm[l] : T(0);
+    r = warp_sum(r);
+  }
+  __syncthreads();
+  return r;
+}
+template <typename T, int NT>
+__device__ __forceinline__ T block_max(T v, T* sm) {
+  v = warp_max(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  T r = T(0);
+  if (w == 0) {
+    r = (l < NT / 32) ? sm[l] : T(0);
+    r = warp_max(r);
+  }
+  __syncthreads();
+  return r;
+}
+
+// std::max / std::min semantics (first argument wins ties / NaN ordering)
+template <typename T>
+__host__ __device__ __forceinline__ T smax(T a, T b) { return (a < b) ? b : a; }
+template <typename T>
+__host__ __device__ __forceinline__ T smin(T a, T b) { return (b < a) ? b : a; }
+
+// streaming loads: bypass L1 allocation for the matrix streams
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T t_sqrt(T x);
+template <>
+__device__ __forceinline__ double t_sqrt<double>(double x) { return __dsqrt_rn(x); }
+template <>
+__device__ __forceinline__ float t_sqrt<float>(float x) { return __fsqrt_rn(x); }
+
+template <typename T>
+__device__ __forceinline__ T t_div(T a, T b);
+template <>
+__device__ __forceinline__ double t_div<double>(double a, double b) { return __ddiv_rn(a, b); }
+template <>
+__device__ __forceinline__ float t_div<float>(float a, float b) { return __fdiv_rn(a, b); }
+
+template <typename T>
+__host__ __device__ __forceinline__ T t_inf() {
+  return T(1.0) / T(0.0);
+}
+
+}  // namespace qpcg_b200

@@ -1,0 +1,1040 @@
+// engine.cu — the B200 ADMM/PCG workspace and the C-ABI (include/qpcg_b200.h).
+//
+// Drop-in for qpcg::solve (solver.hpp:386-541).  One workspace = one device,
+// one stream, all buffers; calls on distinct workspaces are re-entrant.
+//
+// Per ADMM step (SURVEY.md §7 hard part 4b):
+//   A^T pass  [rhs = A^T(rho z - y) + (sigma x - q) ; r0 = K x~ - rhs]   2 cols
+//   k_pcg_init
+//   while PCG: A pass [t = rho A p] ; A^T pass [Kp = P p + sigma p + A^T t] ;
+//              k_pcg_dot ; k_pcg_update ; k_pcg_pupdate
+//   k_pcg_fin
+//   A pass    [z~ = A x~, m-side relax/project/dual update ; A x_new]    2 cols
+//   k_xupdate
+//   if check: A^T pass [A^T y, P x, r_dual] ; k_residuals
+//             if not optimal: A_o^T, P_o, A_o passes ; k_infeas
+//   if rho:   k_rho ; k_precond
+// The matrix streams are A and A^T once per PCG iteration plus once each per
+// ADMM step (the reference streams 4 A-sized matrices + P per step).
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/qpcg_b200.h"
+#include "admm.cuh"
+#include "setup.cuh"
+
+namespace qpcg_b200 {
+
+template <typename T>
+struct HostCsr {
+  uint32_t rows, cols, nnz;
+  const T* values;
+  const uint32_t* row_ptr;
+  const uint32_t* col_indices;
+};
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------ setup kernels
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_ruiz_delta(const T* pn, const T* atn, uint32_t n,
+                                                        const T* an, uint32_t m, T* dx, T* dz,
+                                                        T* d, T* e, T* q, T* part,
+                                                        uint32_t* counter, T* dev_out) {
+  // scaling.hpp:125-138: delta = 1/sqrt(col norm) (1 for empty), D *= dx, E *= dz,
+  // q *= dx; deviation = |1 - delta|_inf (:163-165)
+  T v[1] = {T(0)};
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const T cn = smax(pn[i], atn[i]);
+    const T di = cn > T(0) ? T(1) / t_sqrt(cn) : T(1);
+    dx[i] = di;
+    d[i] *= di;
+    q[i] *= di;
+    v[0] = smax(v[0], tabs(T(1) - di));
+  }
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
+    const T a = an[j];
+    const T dj = a > T(0) ? T(1) / t_sqrt(a) : T(1);
+    dz[j] = dj;
+    e[j] *= dj;
+    v[0] = smax(v[0], tabs(T(1) - dj));
+  }
+  T tot[1];
+  if (!grid_reduce<T, 1>(v, 0x1u, part, counter, tot)) return;
+  if (threadIdx.x == 0) *dev_out = tot[0];
+}
+
+// gamma = 1/max(mean, |q|_inf) (1 if 0); c *= gamma  (scaling.hpp:159-162)
+template <typename T>
+__global__ void k_ruiz_gamma(const T* mean, const T* qinf, T* gamma, T* c) {
+  const T denom = smax(*mean, *qinf);
+  const T g = denom > T(0) ? T(1) / denom : T(1);
+  *gamma = g;
+  *c *= g;
+}
+
+template <typename T>
+__global__ void k_scale_by(T* v, uint32_t n, const T* g) {
+  const T s = *g;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    v[i] *= s;
+}
+
+// =====================================================================
+template <typename T>
+class Workspace {
+ public:
+  int device = 0;
+  cudaStream_t s = nullptr;
+  CubTemp tmp;
+  Dev<T> D{};
+  Ctl<T> hc{};
+  qpcg_settings set{};
+  qpcg_options opt{};
+  std::vector<void*> allocs;
+  uint32_t* permA = nullptr;  // transpose permutation of A
+  T* ruiz_scal = nullptr;      // [mean, qinf, gamma, c, dev]
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double setup_seconds = 0, h2d_seconds = 0, setup_wall = 0;
+  uint64_t h2d_bytes = 0;
+  std::string err;
+  bool have_solved = false;
+
+  ~Workspace() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (void* p : allocs) cudaFree(p);
+    for (SpmvPlan<T>* p : {&D.pP, &D.pA, &D.pAT}) plan_free(*p);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (s) cudaStreamDestroy(s);
+  }
+
+  template <typename U>
+  U* alloc(size_t count) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, sizeof(U) * (count ? count : 1)));
+    allocs.push_back(p);
+    return static_cast<U*>(p);
+  }
+  T* vec(size_t count, bool zero = true) {
+    T* p = alloc<T>(count);
+    if (zero) CK(cudaMemsetAsync(p, 0, sizeof(T) * (count ? count : 1), s));
+    return p;
+  }
+  void upload(void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return;
+    const bool host = opt.input_memory == QPCG_MEM_HOST;
+    CK(cudaMemcpyAsync(dst, src, bytes, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    if (host) h2d_bytes += bytes;
+  }
+  void download(void* dst, const void* src, size_t bytes) {
+    if (bytes == 0 || dst == nullptr) return;
+    const bool host = opt.input_memory == QPCG_MEM_HOST;
+    CK(cudaMemcpyAsync(dst, src, bytes, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+  }
+  void fill(T* p, uint32_t n, T v) {
+    for_n(n, [=] __device__(uint32_t i) { p[i] = v; }, s);
+  }
+  T read_scalar(const T* p) {
+    T v;
+    CK(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return v;
+  }
+  void pull_ctl() {
+    CK(cudaMemcpyAsync(&hc, D.ctl, sizeof(Ctl<T>), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  void push_ctl() { CK(cudaMemcpyAsync(D.ctl, &hc, sizeof(Ctl<T>), cudaMemcpyHostToDevice, s)); }
+
+  // ------------------------------------------------------------- setup
+  void setup(const HostCsr<T>& Pu, const T* q, const HostCsr<T>& A, const T* l, const T* u,
+             const qpcg_settings& st, const qpcg_options& op) {
+    const double w0 = now_s();
+    set = st;
+    opt = op;
+    validate_settings(st);
+    device = op.device;
+    if (device < 0) CK(cudaGetDevice(&device));
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    const uint32_t n = Pu.rows, m = A.rows;
+    // host-side shape checks that do not need the data (problem.hpp:47-58 order
+    // is preserved below by deferring these messages until after the CSR loops)
+    const bool p_square = Pu.rows == Pu.cols;
+    const bool a_cols_ok = A.cols == Pu.cols;
+    CK(cudaEventRecord(ev0, s));
+    D.n = n;
+    D.m = m;
+    // ---- upload (the only host->device traffic of a solve)
+    const double th = now_s();
+    uint32_t* pu_rp = alloc<uint32_t>(n + 1);
+    uint32_t* pu_ci = alloc<uint32_t>(Pu.nnz);
+    T* pu_v = alloc<T>(Pu.nnz);
+    uint32_t* a_rp = alloc<uint32_t>(m + 1);
+    uint32_t* a_ci = alloc<uint32_t>(A.nnz);
+    T* a_v = alloc<T>(A.nnz);
+    D.q_o = alloc<T>(n);
+    D.l_o = alloc<T>(m);
+    D.u_o = alloc<T>(m);
+    upload(pu_rp, Pu.row_ptr, sizeof(uint32_t) * (n + 1));
+    upload(pu_ci, Pu.col_indices, sizeof(uint32_t) * Pu.nnz);
+    upload(pu_v, Pu.values, sizeof(T) * Pu.nnz);
+    upload(a_rp, A.row_ptr, sizeof(uint32_t) * (m + 1));
+    upload(a_ci, A.col_indices, sizeof(uint32_t) * A.nnz);
+    upload(a_v, A.values, sizeof(T) * A.nnz);
+    upload(D.q_o, q, sizeof(T) * n);
+    upload(D.l_o, l, sizeof(T) * m);
+    upload(D.u_o, u, sizeof(T) * m);
+    if (opt.input_memory == QPCG_MEM_HOST) {
+      CK(cudaStreamSynchronize(s));
+      h2d_seconds = now_s() - th;
+    }
+    // ---- validation (problem.hpp:46-92, sparse.hpp:98-124)
+    validate_problem(Pu, A, pu_rp, pu_ci, pu_v, a_rp, a_ci, a_v, p_square, a_cols_ok);
+    DevCsr<T> Pup{n, n, Pu.nnz, pu_v, pu_rp, pu_ci};
+    D.A = DevCsr<T>{m, n, A.nnz, a_v, a_rp, a_ci};  // values replaced by scaled copy below
+    // ---- plans and structures
+    SpmvPlan<T> pPu = plan_build<T>(pu_rp, n, tmp, s);
+    D.pA = plan_build<T>(a_rp, m, tmp, s);
+    uint32_t* row_of = alloc<uint32_t>(std::max(Pu.nnz, A.nnz));
+    plan_visit(Pup, pPu, RowOfFn{row_of}, s);
+    // symmetrize_upper (solver.hpp:397)
+    DevCsr<T> Pfull;
+    symmetrize_upper_dev(Pup, row_of, Pfull, tmp, s);
+    allocs.push_back(Pfull.rp);
+    allocs.push_back(Pfull.ci);
+    allocs.push_back(Pfull.val);
+    plan_free(pPu);
+    D.pP = plan_build<T>(Pfull.rp, n, tmp, s);
+    D.Po = Pfull;
+    // transpose_csr (solver.hpp:398)
+    plan_visit(D.A, D.pA, RowOfFn{row_of}, s);
+    uint32_t* at_rp = alloc<uint32_t>(n + 1);
+    uint32_t* at_ci = alloc<uint32_t>(A.nnz);
+    permA = alloc<uint32_t>(A.nnz);
+    transpose_structure(a_ci, row_of, n, A.nnz, at_rp, at_ci, permA, tmp, s);
+    T* ato_v = alloc<T>(A.nnz);
+    gather_values(a_v, permA, A.nnz, ato_v, s);
+    D.Ao = DevCsr<T>{m, n, A.nnz, a_v, a_rp, a_ci};
+    D.ATo = DevCsr<T>{n, m, A.nnz, ato_v, at_rp, at_ci};
+    D.pAT = plan_build<T>(at_rp, n, tmp, s);
+    D.pPo = D.pP;
+    D.pAo = D.pA;
+    D.pATo = D.pAT;
+    // ---- control block + reductions
+    D.ctl = alloc<Ctl<T>>(1);
+    D.red = alloc<T>(kRedBlocks * kMaxQ);
+    CK(cudaMemsetAsync(D.ctl, 0, sizeof(Ctl<T>), s));
+    ruiz_scal = vec(8);
+    // q_inf_orig (solver.hpp:399)
+    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q_o, n, D.red, &D.ctl->red_counter,
+                                                      ruiz_scal + 5);
+    CK_LAUNCH();
+    // ---- scaled copies
+    D.P = DevCsr<T>{n, n, Pfull.nnz, alloc<T>(Pfull.nnz), Pfull.rp, Pfull.ci};
+    D.A = DevCsr<T>{m, n, A.nnz, alloc<T>(A.nnz), a_rp, a_ci};
+    D.AT = DevCsr<T>{n, m, A.nnz, alloc<T>(A.nnz), at_rp, at_ci};
+    CK(cudaMemcpyAsync(D.P.val, Pfull.val, sizeof(T) * Pfull.nnz, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(D.A.val, a_v, sizeof(T) * A.nnz, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(D.AT.val, ato_v, sizeof(T) * A.nnz, cudaMemcpyDeviceToDevice, s));
+    D.q = vec(n, false);
+    CK(cudaMemcpyAsync(D.q, D.q_o, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+    D.d = vec(n, false);
+    D.e = vec(m, false);
+    D.d_inv = vec(n, false);
+    D.e_inv = vec(m, false);
+    D.l = vec(m, false);
+    D.u = vec(m, false);
+    fill(D.d, n, T(1));
+    fill(D.e, m, T(1));
+    uint32_t passes = 0;
+    T deviation = T(0);
+    T c = T(1);
+    CK(cudaMemcpyAsync(ruiz_scal + 3, &c, sizeof(T), cudaMemcpyHostToDevice, s));
+    if (st.scaling_enabled) {
+      ruiz(st, passes, deviation);
+      c = read_scalar(ruiz_scal + 3);
+    }
+    // scaling.hpp:166-176: a_t re-derived from the scaled a; reciprocals; l, u
+    if (st.scaling_enabled) gather_values(D.A.val, permA, A.nnz, D.AT.val, s);
+    {
+      T *d = D.d, *e = D.e, *di = D.d_inv, *ei = D.e_inv, *lo = D.l_o, *uo = D.u_o, *ls = D.l,
+        *us = D.u;
+      for_n(n, [=] __device__(uint32_t i) { di[i] = T(1) / d[i]; }, s);
+      for_n(m, [=] __device__(uint32_t j) {
+        ei[j] = T(1) / e[j];
+        ls[j] = e[j] * lo[j];
+        us[j] = e[j] * uo[j];
+      }, s);
+    }
+    if (!st.scaling_enabled) {  // identity_scaled_problem (scaling.hpp:190-205): l, u copied
+      CK(cudaMemcpyAsync(D.l, D.l_o, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(D.u, D.u_o, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
+    }
+    // q_inf_scaled (solver.hpp:407)
+    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q, n, D.red, &D.ctl->red_counter,
+                                                      ruiz_scal + 6);
+    CK_LAUNCH();
+    // ---- operator caches + Jacobi (linsys.hpp:59-60, 137-148)
+    D.diag_p = vec(n, false);
+    D.diag_ata = vec(n, false);
+    D.dinv = vec(n, false);
+    extract_diag_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.P, D.diag_p);
+    CK_LAUNCH();
+    diag_ata_kernel<T><<<grid_for(uint64_t(n) * 32), kThreads, 0, s>>>(D.AT, D.diag_ata);
+    CK_LAUNCH();
+    // ---- state and workspace vectors
+    D.x = vec(n); D.xt = vec(n); D.dx = vec(n); D.b = vec(n); D.r = vec(n); D.p = vec(n);
+    D.kp = vec(n); D.best = vec(n); D.px = vec(n); D.aty = vec(n); D.rdual = vec(n);
+    D.xo = vec(n); D.pxo = vec(n);
+    D.z = vec(m); D.y = vec(m); D.zt = vec(m); D.dy = vec(m); D.t = vec(m); D.ax = vec(m);
+    D.zo = vec(m); D.yo = vec(m);
+    D.cert = vec(std::max(n, m));
+    const uint32_t cap = op.record_diagnostics ? st.max_admm_iter : 0u;
+    D.calls = alloc<DiagRec<T>>(cap);
+    D.checks = alloc<uint32_t>(cap);
+    D.rhos = alloc<RhoRec<T>>(cap);
+    // ---- control block
+    T hs[8];
+    CK(cudaMemcpyAsync(hs, ruiz_scal, sizeof(T) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::memset(&hc, 0, sizeof(hc));
+    hc.alpha = T(st.alpha);
+    hc.sigma = T(st.sigma);
+    hc.eps_abs = T(st.eps_abs);
+    hc.eps_rel = T(st.eps_rel);
+    hc.eps_pinf = T(st.eps_pinf);
+    hc.eps_dinf = T(st.eps_dinf);
+    hc.lambda = T(st.lambda_pcg);
+    hc.eps_min = T(st.eps_pcg_min);
+    hc.max_iter = st.max_admm_iter;
+    hc.check_interval = st.check_interval;
+    hc.rho_interval = st.rho_update_interval;
+    hc.pcg_cap = pcg_cap(n);
+    hc.c = c;
+    hc.c_inv = T(1) / c;
+    hc.q_inf_orig = hs[5];
+    hc.q_inf_scaled = hs[6];
+    hc.rho = T(st.rho_bar_init);
+    hc.status = QPCG_STATUS_MAX_ITER_REACHED;
+    hc.diag_cap = cap;
+    equil_passes = passes;
+    equil_residual = deviation;
+    push_ctl();
+    k_precond<T><<<grid_for(n), kThreads, 0, s>>>(D, 1);
+    CK_LAUNCH();
+    CK(cudaEventRecord(ev1, s));
+    CK(cudaEventSynchronize(ev1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    setup_seconds = ms * 1e-3;
+    setup_wall = now_s() - w0;
+  }
+
+  uint32_t equil_passes = 0;
+  T equil_residual = T(0);
+
+  static uint32_t pcg_cap(uint32_t n) {  // solver.hpp:330-334, evaluated in T
+    const uint32_t by_dim = (uint32_t)std::ceil(T(20) * std::sqrt(static_cast<T>(n)));
+    return std::max<uint32_t>(20, std::min<uint32_t>(by_dim, n));
+  }
+
+  static void validate_settings(const qpcg_settings& s) {  // settings.hpp:44-75 in T
+    auto bad = [](const char* m) { throw InvalidArgument(m); };
+    const T alpha = T(s.alpha);
+    if (!(alpha > T(0)) || !(alpha < T(2))) bad("settings: alpha must be in (0, 2)");
+    if (!(T(s.sigma) > T(0))) bad("settings: sigma must be positive");
+    if (!(T(s.rho_bar_init) > T(0))) bad("settings: rho_bar_init must be positive");
+    if (T(s.eps_abs) < T(0) || T(s.eps_rel) < T(0)) bad("settings: tolerances must be >= 0");
+    if (!(T(s.eps_pinf) > T(0)) || !(T(s.eps_dinf) > T(0)))
+      bad("settings: infeasibility tolerances must be positive");
+    if (s.max_admm_iter < 1 || s.check_interval < 1 || s.rho_update_interval < 1)
+      bad("settings: iteration counts must be >= 1");
+    if (!(T(s.lambda_pcg) > T(0)) || !(T(s.lambda_pcg) < T(1)))
+      bad("settings: lambda_pcg must be in (0, 1)");
+    if (!(T(s.eps_pcg_min) > T(0))) bad("settings: eps_pcg_min must be positive");
+    if (!(T(s.eps_equil) > T(0)) || s.equil_max_passes < 1)
+      bad("settings: bad equilibration parameters");
+  }
+
+  void validate_problem(const HostCsr<T>& Pu, const HostCsr<T>& A, const uint32_t* pu_rp,
+                        const uint32_t* pu_ci, const T* pu_v, const uint32_t* a_rp,
+                        const uint32_t* a_ci, const T* a_v, bool p_square, bool a_cols_ok) {
+    const uint32_t n = Pu.rows, m = A.rows;
+    uint32_t ends[4];
+    CK(cudaMemcpyAsync(ends + 0, pu_rp, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ends + 1, pu_rp + n, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ends + 2, a_rp, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ends + 3, a_rp + m, 4, cudaMemcpyDeviceToHost, s));
+    unsigned long long* key = alloc<unsigned long long>(1);
+    CK(cudaMemsetAsync(key, 0xff, 8, s));
+    CK(cudaStreamSynchronize(s));
+    if (ends[0] != 0 || ends[1] != Pu.nnz)
+      throw InvalidArgument("csr: row_ptr must start at 0 and end at nnz");
+    validate_csr_rows_kernel<<<grid_for(n), kThreads, 0, s>>>(pu_rp, pu_ci, n, Pu.cols, kValPRowPtr,
+                                                             p_square ? 1 : 0, key);
+    CK_LAUNCH();
+    unsigned long long k = 0;
+    CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if ((k >> 56) == kValPRowPtr) throw InvalidArgument(validation_message(k));
+    if (ends[2] != 0 || ends[3] != A.nnz)
+      throw InvalidArgument("csr: row_ptr must start at 0 and end at nnz");
+    validate_csr_rows_kernel<<<grid_for(m), kThreads, 0, s>>>(a_rp, a_ci, m, A.cols, kValARowPtr, 0,
+                                                             key);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if ((k >> 56) == kValARowPtr) throw InvalidArgument(validation_message(k));
+    if (!p_square) throw InvalidArgument("problem: P must be square");
+    if (n == 0) throw InvalidArgument("problem: at least one variable required");
+    if ((k >> 56) == kValPBelow) throw InvalidArgument(validation_message(k));
+    if (!a_cols_ok) throw InvalidArgument("problem: A column count must equal n");
+    validate_values_kernel<T><<<grid_for(Pu.nnz), kThreads, 0, s>>>(pu_v, Pu.nnz, kValPFinite, key);
+    validate_values_kernel<T><<<grid_for(A.nnz), kThreads, 0, s>>>(a_v, A.nnz, kValAFinite, key);
+    validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.q_o, n, kValQFinite, key);
+    validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(D.l_o, D.u_o, m, key);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (k != ~0ull) throw InvalidArgument(validation_message(k));
+  }
+
+  // modified Ruiz equilibration (scaling.hpp:92-187), bit-exact
+  void ruiz(const qpcg_settings& st, uint32_t& passes, T& deviation) {
+    const uint32_t n = D.n, m = D.m;
+    T* dx = vec(n, false);
+    T* dz = vec(m, false);
+    T* pn = vec(n, false);
+    T* atn = vec(n, false);
+    T* an = vec(m, false);
+    deviation = T(1);
+    passes = 0;
+    const T eps = T(st.eps_equil);
+    T* mean = ruiz_scal + 0;
+    T* qinf = ruiz_scal + 1;
+    T* gamma = ruiz_scal + 2;
+    T* cc = ruiz_scal + 3;
+    T* dev = ruiz_scal + 4;
+    while (passes < st.equil_max_passes && deviation > eps) {
+      ++passes;
+      row_inf_norms(D.P, D.pP, pn, s);
+      row_inf_norms(D.AT, D.pAT, atn, s);
+      row_inf_norms(D.A, D.pA, an, s);
+      k_ruiz_delta<T><<<red_grid<T>(std::max(n, m)), kThreads, 0, s>>>(
+          pn, atn, n, an, m, dx, dz, D.d, D.e, D.q, D.red, &D.ctl->red_counter, dev);
+      CK_LAUNCH();
+      plan_visit(D.P, D.pP, ScaleRowColFn<T>{D.P.val, D.P.ci, dx, dx}, s);
+      plan_visit(D.A, D.pA, ScaleRowColFn<T>{D.A.val, D.A.ci, dz, dx}, s);
+      plan_visit(D.AT, D.pAT, ScaleRowColFn<T>{D.AT.val, D.AT.ci, dx, dz}, s);
+      // cost scaling
+      row_inf_norms(D.P, D.pP, pn, s);
+      ordered_mean_kernel<T><<<1, 32, 0, s>>>(pn, n, mean);
+      CK_LAUNCH();
+      k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q, n, D.red, &D.ctl->red_counter, qinf);
+      CK_LAUNCH();
+      k_ruiz_gamma<T><<<1, 1, 0, s>>>(mean, qinf, gamma, cc);
+      CK_LAUNCH();
+      k_scale_by<T><<<grid_for(D.P.nnz), kThreads, 0, s>>>(D.P.val, D.P.nnz, gamma);
+      k_scale_by<T><<<grid_for(n), kThreads, 0, s>>>(D.q, n, gamma);
+      CK_LAUNCH();
+      deviation = read_scalar(dev);
+    }
+  }
+
+  // ------------------------------------------------------ enqueue helpers
+  void enq_rhs(const Handles&) {
+    launch_spmv<T, 2, SumOp>(D.AT, D.pAT, GatherRhs<T>{D.z, D.y, D.zt, D.ctl, T(0)},
+                             EpiRhs<T>{D, T(0)}, s);
+  }
+  void enq_pcg_init(const Handles& H) {
+    k_pcg_init<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D, H);
+    CK_LAUNCH();
+  }
+  void enq_pcg_iter(const Handles& H) {
+    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
+    launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
+    k_pcg_dot<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D);
+    CK_LAUNCH();
+    k_pcg_update<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D, H);
+    CK_LAUNCH();
+    k_pcg_pupdate<T><<<grid_for(D.n), kThreads, 0, s>>>(D);
+    CK_LAUNCH();
+  }
+  void enq_post_pcg(const Handles& H) {
+    k_pcg_fin<T><<<grid_for(D.n), kThreads, 0, s>>>(D);
+    CK_LAUNCH();
+    launch_spmv<T, 2, SumOp>(D.A, D.pA, GatherAdmm<T>{D.xt, D.x, D.ctl, T(0), T(0), false},
+                             EpiAdmm<T>{D, T(0), T(0), T(0), false}, s);
+    k_xupdate<T><<<grid_for(D.n), kThreads, 0, s>>>(D, H);
+    CK_LAUNCH();
+  }
+  void enq_check(const Handles& H, int mode) {
+    launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.y}, EpiDual<T>{D}, s);
+    k_residuals<T><<<red_grid<T>(std::max(D.n, D.m)), kThreads, 0, s>>>(D, mode, H);
+    CK_LAUNCH();
+  }
+  void enq_infeas(const Handles&) {
+    launch_spmv<T, 1, SumOp>(
+        D.ATo, D.pATo, GatherCertY<T>{D.e, D.dy, D.ctl, T(0), T(0)},
+        EpiNormMax<T>{&D.ctl->atv_inf_bits, &D.ctl->need_pinf}, s);
+    launch_spmv<T, 1, SumOp>(D.Po, D.pPo, GatherCertX<T>{D.d, D.dx, D.ctl, T(0)},
+                             EpiNormMax<T>{&D.ctl->pv_inf_bits, &D.ctl->need_dinf}, s);
+    launch_spmv<T, 1, SumOp>(
+        D.Ao, D.pAo, GatherCertX<T>{D.d, D.dx, D.ctl, T(0)},
+        EpiDualRows<T>{D.l_o, D.u_o, &D.ctl->dinf_bad, &D.ctl->need_dinf, T(0), D.ctl}, s);
+    k_infeas<T><<<red_grid<T>(std::max(D.n, D.m)), kThreads, 0, s>>>(D);
+    CK_LAUNCH();
+  }
+  void enq_rho_flag(const Handles& H) {
+    k_rho_flag<T><<<1, 1, 0, s>>>(D, H);
+    CK_LAUNCH();
+  }
+  void enq_rho(const Handles&) {
+    k_rho<T><<<red_grid<T>(D.m), kThreads, 0, s>>>(D);
+    CK_LAUNCH();
+    k_precond<T><<<grid_for(D.n), kThreads, 0, s>>>(D, 0);
+    CK_LAUNCH();
+  }
+  void enq_admm_cond(const Handles& H) {
+    k_admm_cond<T><<<1, 1, 0, s>>>(D, H);
+    CK_LAUNCH();
+  }
+  // residuals at the current iterates (solver.hpp:436, :517)
+  void enq_residuals_fresh(int mode) {
+    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.x}, EpiStore<T>{D.ax}, s);
+    enq_check(Handles{}, mode);
+  }
+
+  // ------------------------------------------------------- graph build
+  cudaGraph_t add_cond_in_capture(cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = type;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, deps, nd, &cp));
+    CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    return cp.conditional.phGraph_out[0];
+  }
+
+  void build_graph() {
+    CK(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h_admm, h_pcg, h_chk, h_inf, h_rho;
+    CK(cudaGraphConditionalHandleCreate(&h_admm, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h_admm;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t n_admm;
+    CK(cudaGraphAddNode(&n_admm, graph, nullptr, 0, &cp));
+    cudaGraph_t b_admm = cp.conditional.phGraph_out[0];
+    CK(cudaGraphConditionalHandleCreate(&h_pcg, b_admm, 0, cudaGraphCondAssignDefault));
+    CK(cudaGraphConditionalHandleCreate(&h_chk, b_admm, 0, cudaGraphCondAssignDefault));
+    CK(cudaGraphConditionalHandleCreate(&h_rho, b_admm, 0, cudaGraphCondAssignDefault));
+    Handles H;
+    H.admm = (unsigned long long)h_admm;
+    H.pcg = (unsigned long long)h_pcg;
+    H.chk = (unsigned long long)h_chk;
+    H.rho = (unsigned long long)h_rho;
+    cudaGraph_t b_pcg, b_chk, b_rho, b_inf, g_out;
+    CK(cudaStreamBeginCaptureToGraph(s, b_admm, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    enq_rhs(H);
+    enq_pcg_init(H);
+    b_pcg = add_cond_in_capture(h_pcg, cudaGraphCondTypeWhile);
+    enq_post_pcg(H);
+    b_chk = add_cond_in_capture(h_chk, cudaGraphCondTypeIf);
+    enq_rho_flag(H);
+    b_rho = add_cond_in_capture(h_rho, cudaGraphCondTypeIf);
+    enq_admm_cond(H);
+    CK(cudaStreamEndCapture(s, &g_out));
+    CK(cudaStreamBeginCaptureToGraph(s, b_pcg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    enq_pcg_iter(H);
+    CK(cudaStreamEndCapture(s, &g_out));
+    CK(cudaGraphConditionalHandleCreate(&h_inf, b_chk, 0, cudaGraphCondAssignDefault));
+    H.inf = (unsigned long long)h_inf;
+    CK(cudaStreamBeginCaptureToGraph(s, b_chk, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    enq_check(H, 0);
+    b_inf = add_cond_in_capture(h_inf, cudaGraphCondTypeIf);
+    CK(cudaStreamEndCapture(s, &g_out));
+    CK(cudaStreamBeginCaptureToGraph(s, b_inf, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    enq_infeas(H);
+    CK(cudaStreamEndCapture(s, &g_out));
+    CK(cudaStreamBeginCaptureToGraph(s, b_rho, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    enq_rho(H);
+    CK(cudaStreamEndCapture(s, &g_out));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+  }
+
+  // ------------------------------------------------------- eager loop
+  void run_eager() {
+    Handles H{};
+    for (;;) {
+      pull_ctl();
+      if (hc.done || hc.error || hc.iter >= hc.max_iter) break;
+      enq_rhs(H);
+      enq_pcg_init(H);
+      pull_ctl();
+      while (hc.pcg_active && !hc.error) {
+        enq_pcg_iter(H);
+        pull_ctl();
+      }
+      enq_post_pcg(H);
+      pull_ctl();
+      if (hc.is_check && !hc.error) {
+        enq_check(H, 0);
+        pull_ctl();
+        if (hc.inf_branch) enq_infeas(H);
+      }
+      enq_rho_flag(H);
+      enq_rho(H);
+    }
+  }
+
+  // ------------------------------------------------------------ solve
+  void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) {
+    CK(cudaSetDevice(device));
+    const double w0 = now_s();
+    CK(cudaEventRecord(ev0, s));
+    // reset the per-solve state (solver.hpp:412, :430-443)
+    pull_ctl();
+    hc.iter = 0;
+    hc.done = 0;
+    hc.error = 0;
+    hc.status = QPCG_STATUS_MAX_ITER_REACHED;
+    hc.pcg_total = 0;
+    hc.rho_update_count = 0;
+    hc.n_calls = hc.n_checks = hc.n_rho = 0;
+    hc.pcg_active = 0;
+    hc.red_counter = 0;
+    push_ctl();
+    // initial residuals and PCG tolerance (solver.hpp:436-441)
+    enq_residuals_fresh(1);
+    if (opt.mode == QPCG_MODE_EAGER) {
+      run_eager();
+    } else {
+      if (!exec) build_graph();
+      CK(cudaGraphLaunch(exec, s));
+    }
+    pull_ctl();
+    if (hc.error == kErrNotPD)
+      throw NotPositiveDefinite("pcg: encountered direction of nonpositive curvature");
+    if (hc.error == kErrInvalid) {
+      if (hc.n_rho > 0 && !(hc.rho > T(0))) throw InvalidArgument("kkt operator: rho must be positive");
+      throw InvalidArgument("pcg: warm start must be finite");
+    }
+    if (!hc.residuals_current) enq_residuals_fresh(2);
+    k_unscale<T><<<grid_for(std::max(D.n, D.m)), kThreads, 0, s>>>(D);
+    CK_LAUNCH();
+    if (hc.status != 1 && hc.status != 2)
+      launch_spmv<T, 1, SumOp>(D.Po, D.pPo, GatherVec<T>{D.xo}, EpiStore<T>{D.pxo}, s);
+    k_objective<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D);
+    CK_LAUNCH();
+    CK(cudaEventRecord(ev1, s));
+    pull_ctl();
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    const double td = now_s();
+    download(x, D.xo, sizeof(T) * D.n);
+    download(z, D.zo, sizeof(T) * D.m);
+    download(y, D.yo, sizeof(T) * D.m);
+    const bool has_cert = hc.status == 1 || hc.status == 2;
+    if (has_cert) download(cert, D.cert, sizeof(T) * (hc.status == 1 ? D.m : D.n));
+    CK(cudaStreamSynchronize(s));
+    const double d2h = now_s() - td;
+    have_solved = true;
+    if (info) {
+      std::memset(info, 0, sizeof(*info));
+      info->status = int32_t(hc.status);
+      info->iterations = hc.iter;
+      info->pcg_iterations_total = hc.pcg_total;
+      info->objective = double(hc.objective);
+      info->r_prim_inf = double(hc.rp_o);
+      info->r_dual_inf = double(hc.rd_o);
+      info->equil_passes = equil_passes;
+      info->rho_update_count = hc.rho_update_count;
+      info->equil_residual = double(equil_residual);
+      info->rho_final = double(hc.rho);
+      info->certificate_valid = has_cert;
+      info->n = D.n;
+      info->m = D.m;
+      info->setup_seconds = setup_seconds;
+      info->solve_seconds = ms * 1e-3;
+      info->h2d_seconds = h2d_seconds;
+      info->d2h_seconds = opt.input_memory == QPCG_MEM_HOST ? d2h : 0.0;
+      info->h2d_bytes = h2d_bytes;
+      info->d2h_bytes = opt.input_memory == QPCG_MEM_HOST
+                            ? sizeof(T) * (uint64_t(D.n) + 2ull * D.m) +
+                                  (has_cert ? sizeof(T) * (hc.status == 1 ? D.m : D.n) : 0)
+                            : 0;
+      info->runtime_seconds = now_s() - w0;
+    }
+  }
+
+  // ------------------------------------------------- OSQP-style updates
+  void warm_start(const T* x, const T* z, const T* y) {  // solver.hpp:413-428
+    CK(cudaSetDevice(device));
+    const uint32_t n = D.n, m = D.m;
+    T* tx = vec(n, false);
+    T* tz = vec(m, false);
+    T* ty = vec(m, false);
+    upload(tx, x, sizeof(T) * n);
+    upload(tz, z, sizeof(T) * m);
+    upload(ty, y, sizeof(T) * m);
+    unsigned long long* key = alloc<unsigned long long>(1);
+    CK(cudaMemsetAsync(key, 0xff, 8, s));
+    validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(tx, n, 1, key);
+    validate_values_kernel<T><<<grid_for(m), kThreads, 0, s>>>(tz, m, 1, key);
+    validate_values_kernel<T><<<grid_for(m), kThreads, 0, s>>>(ty, m, 1, key);
+    unsigned long long k;
+    CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (k != ~0ull) throw InvalidArgument("solve: warm start must be finite");
+    const T c = hc.c;
+    T *X = D.x, *XT = D.xt, *Z = D.z, *Y = D.y, *di = D.d_inv, *e = D.e, *ei = D.e_inv;
+    for_n(n, [=] __device__(uint32_t i) {
+      const T v = di[i] * tx[i];
+      X[i] = v;
+      XT[i] = v;
+    }, s);
+    for_n(m, [=] __device__(uint32_t j) {
+      Z[j] = e[j] * tz[j];
+      Y[j] = (ei[j] * ty[j]) * c;
+    }, s);
+    // keep the invariant zt == A x~ used by the fused r0 (pcg_warm = x)
+    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.xt}, EpiStore<T>{D.zt}, s);
+    CK(cudaStreamSynchronize(s));
+  }
+
+  void update_rho(T rho) {  // linsys.hpp:153-157
+    if (!(rho > T(0))) throw InvalidArgument("kkt operator: rho must be positive");
+    CK(cudaSetDevice(device));
+    pull_ctl();
+    hc.rho = rho;
+    push_ctl();
+    k_precond<T><<<grid_for(D.n), kThreads, 0, s>>>(D, 1);
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(s));
+  }
+
+  // Not in the reference: rescale with the existing D, E, c.
+  void update_vectors(const T* q, const T* l, const T* u) {
+    CK(cudaSetDevice(device));
+    const uint32_t n = D.n, m = D.m;
+    if (q) upload(D.q_o, q, sizeof(T) * n);
+    if (l) upload(D.l_o, l, sizeof(T) * m);
+    if (u) upload(D.u_o, u, sizeof(T) * m);
+    unsigned long long* key = alloc<unsigned long long>(1);
+    CK(cudaMemsetAsync(key, 0xff, 8, s));
+    validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.q_o, n, kValQFinite, key);
+    validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(D.l_o, D.u_o, m, key);
+    unsigned long long k;
+    CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (k != ~0ull) throw InvalidArgument(validation_message(k));
+    const T c = hc.c;
+    T *qs = D.q, *qo = D.q_o, *d = D.d, *e = D.e, *ls = D.l, *us = D.u, *lo = D.l_o, *uo = D.u_o;
+    for_n(n, [=] __device__(uint32_t i) { qs[i] = c * (d[i] * qo[i]); }, s);
+    for_n(m, [=] __device__(uint32_t j) {
+      ls[j] = e[j] * lo[j];
+      us[j] = e[j] * uo[j];
+    }, s);
+    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q_o, n, D.red, &D.ctl->red_counter,
+                                                      &D.ctl->q_inf_orig);
+    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q, n, D.red, &D.ctl->red_counter,
+                                                      &D.ctl->q_inf_scaled);
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(s));
+    pull_ctl();
+  }
+};
+
+}  // namespace qpcg_b200
+
+// =====================================================================
+// C-ABI
+// =====================================================================
+using namespace qpcg_b200;
+
+struct qpcg_workspace {
+  int precision = 64;
+  std::unique_ptr<Workspace<double>> w64;
+  std::unique_ptr<Workspace<float>> w32;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(qpcg_workspace* ws, F&& f) {
+  std::string* msg = ws ? &ws->err : &g_last_error;
+  try {
+    f();
+    return QPCG_OK;
+  } catch (const InvalidArgument& e) {
+    *msg = e.what();
+    return QPCG_ERR_INVALID;
+  } catch (const NotPositiveDefinite& e) {
+    *msg = e.what();
+    return QPCG_ERR_NOT_PD;
+  } catch (const OutOfMemory& e) {
+    *msg = e.what();
+    return QPCG_ERR_OOM;
+  } catch (const CudaError& e) {
+    *msg = e.what();
+    return QPCG_ERR_CUDA;
+  } catch (const std::exception& e) {
+    *msg = e.what();
+    return QPCG_ERR_RUNTIME;
+  }
+}
+
+template <typename T, typename CsrT>
+HostCsr<T> host_csr(const CsrT* c) {
+  return HostCsr<T>{c->rows, c->cols, c->nnz, c->values, c->row_ptr, c->col_indices};
+}
+
+template <typename T>
+std::unique_ptr<Workspace<T>>& slot(qpcg_workspace* ws);
+template <>
+std::unique_ptr<Workspace<double>>& slot<double>(qpcg_workspace* ws) { return ws->w64; }
+template <>
+std::unique_ptr<Workspace<float>>& slot<float>(qpcg_workspace* ws) { return ws->w32; }
+
+template <typename T, typename CsrT>
+int setup_impl(qpcg_workspace** out, const CsrT* p, const T* q, const CsrT* a, const T* l,
+               const T* u, const qpcg_settings* s, const qpcg_options* o) {
+  if (out == nullptr || p == nullptr || a == nullptr || q == nullptr || l == nullptr ||
+      u == nullptr) {
+    g_last_error = "setup: null argument";
+    return QPCG_ERR_INVALID;
+  }
+  auto* ws = new qpcg_workspace();
+  ws->precision = sizeof(T) * 8;
+  qpcg_settings st;
+  qpcg_default_settings(&st);
+  if (s) st = *s;
+  qpcg_options op;
+  qpcg_default_options(&op);
+  if (o) op = *o;
+  const int rc = guarded(ws, [&] {
+    slot<T>(ws).reset(new Workspace<T>());
+    slot<T>(ws)->setup(host_csr<T>(p), q, host_csr<T>(a), l, u, st, op);
+  });
+  if (rc != QPCG_OK) {
+    g_last_error = ws->err;
+    delete ws;
+    *out = nullptr;
+    return rc;
+  }
+  *out = ws;
+  return rc;
+}
+
+template <typename T>
+Workspace<T>* get(qpcg_workspace* ws) {
+  if (ws == nullptr || !slot<T>(ws)) throw InvalidArgument("workspace: wrong precision or null");
+  return slot<T>(ws).get();
+}
+
+template <typename T, typename CsrT>
+int solve_problem_impl(const CsrT* p, const T* q, const CsrT* a, const T* l, const T* u,
+                       const qpcg_settings* s, const qpcg_options* o, const T* wx, const T* wz,
+                       const T* wy, qpcg_info* info, T* x, T* z, T* y, T* cert, char* msg,
+                       size_t msg_len) {
+  const double t0 = now_s();
+  qpcg_workspace* ws = nullptr;
+  int rc = setup_impl<T>(&ws, p, q, a, l, u, s, o);
+  if (rc == QPCG_OK && wx != nullptr)
+    rc = guarded(ws, [&] { get<T>(ws)->warm_start(wx, wz, wy); });
+  if (rc == QPCG_OK) rc = guarded(ws, [&] { get<T>(ws)->solve(info, x, z, y, cert); });
+  if (rc == QPCG_OK && info) info->runtime_seconds = now_s() - t0;  // solver.hpp:392 -> :537
+  if (rc != QPCG_OK && msg && msg_len) {
+    const std::string& e = ws ? ws->err : g_last_error;
+    std::snprintf(msg, msg_len, "%s", e.c_str());
+  }
+  delete ws;
+  return rc;
+}
+
+template <typename T>
+uint32_t calls_of(Workspace<T>* w, qpcg_pcg_call* out, uint32_t cap) {
+  const uint32_t n = std::min(w->hc.n_calls, w->hc.diag_cap);
+  std::vector<DiagRec<T>> recs(n);
+  if (n) {
+    cudaMemcpy(recs.data(), w->D.calls, sizeof(DiagRec<T>) * n, cudaMemcpyDeviceToHost);
+  }
+  for (uint32_t i = 0; i < n && i < cap; ++i) {
+    out[i].admm_iter = recs[i].admm_iter;
+    out[i].iterations = recs[i].iterations;
+    out[i].eps = double(recs[i].eps);
+    out[i].r_prim_scaled_inf = double(recs[i].rp);
+    out[i].r_dual_scaled_inf = double(recs[i].rd);
+    out[i].converged = int32_t(recs[i].converged);
+    out[i].reserved_ = 0;
+  }
+  return n;
+}
+template <typename T>
+uint32_t rhos_of(Workspace<T>* w, qpcg_rho_update* out, uint32_t cap) {
+  const uint32_t n = std::min(w->hc.n_rho, w->hc.diag_cap);
+  std::vector<RhoRec<T>> recs(n);
+  if (n) cudaMemcpy(recs.data(), w->D.rhos, sizeof(RhoRec<T>) * n, cudaMemcpyDeviceToHost);
+  for (uint32_t i = 0; i < n && i < cap; ++i) {
+    out[i].admm_iter = recs[i].admm_iter;
+    out[i].reserved_ = 0;
+    out[i].rho_before = double(recs[i].before);
+    out[i].rho_after = double(recs[i].after);
+  }
+  return n;
+}
+template <typename T>
+uint32_t checks_of(Workspace<T>* w, uint32_t* out, uint32_t cap) {
+  const uint32_t n = std::min(w->hc.n_checks, w->hc.diag_cap);
+  std::vector<uint32_t> recs(n);
+  if (n) cudaMemcpy(recs.data(), w->D.checks, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost);
+  for (uint32_t i = 0; i < n && i < cap; ++i) out[i] = recs[i];
+  return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+void qpcg_default_settings(qpcg_settings* s) {
+  std::memset(s, 0, sizeof(*s));
+  s->alpha = 1.6;
+  s->sigma = 1e-6;
+  s->rho_bar_init = 0.1;
+  s->eps_abs = 1e-3;
+  s->eps_rel = 1e-3;
+  s->eps_pinf = 1e-4;
+  s->eps_dinf = 1e-4;
+  s->max_admm_iter = 50000;
+  s->check_interval = 5;
+  s->rho_update_interval = 10;
+  s->scaling_enabled = 1;
+  s->lambda_pcg = 0.15;
+  s->eps_pcg_min = 1e-7;
+  s->eps_equil = 1e-3;
+  s->equil_max_passes = 10;
+}
+
+void qpcg_default_options(qpcg_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->device = -1;
+  o->input_memory = QPCG_MEM_HOST;
+  o->mode = QPCG_MODE_GRAPH;
+  o->record_diagnostics = 0;
+  o->virtual_shards = 1;
+}
+
+int qpcg_validate_settings(const qpcg_settings* s, char* msg, size_t msg_len) {
+  try {
+    Workspace<double>::validate_settings(*s);
+    return QPCG_OK;
+  } catch (const std::exception& e) {
+    if (msg && msg_len) std::snprintf(msg, msg_len, "%s", e.what());
+    return QPCG_ERR_INVALID;
+  }
+}
+
+const char* qpcg_version(void) { return "qpcg-b200 0.1 (sm_100a)"; }
+
+int qpcg_f64_setup(qpcg_workspace** ws, const qpcg_csr_f64* p, const double* q,
+                   const qpcg_csr_f64* a, const double* l, const double* u,
+                   const qpcg_settings* s, const qpcg_options* o) {
+  return setup_impl<double>(ws, p, q, a, l, u, s, o);
+}
+int qpcg_f32_setup(qpcg_workspace** ws, const qpcg_csr_f32* p, const float* q,
+                   const qpcg_csr_f32* a, const float* l, const float* u, const qpcg_settings* s,
+                   const qpcg_options* o) {
+  return setup_impl<float>(ws, p, q, a, l, u, s, o);
+}
+int qpcg_f64_warm_start(qpcg_workspace* ws, const double* x, const double* z, const double* y) {
+  return guarded(ws, [&] { get<double>(ws)->warm_start(x, z, y); });
+}
+int qpcg_f32_warm_start(qpcg_workspace* ws, const float* x, const float* z, const float* y) {
+  return guarded(ws, [&] { get<float>(ws)->warm_start(x, z, y); });
+}
+int qpcg_f64_update_rho(qpcg_workspace* ws, double rho) {
+  return guarded(ws, [&] { get<double>(ws)->update_rho(rho); });
+}
+int qpcg_f32_update_rho(qpcg_workspace* ws, double rho) {
+  return guarded(ws, [&] { get<float>(ws)->update_rho(float(rho)); });
+}
+int qpcg_f64_update_vectors(qpcg_workspace* ws, const double* q, const double* l, const double* u) {
+  return guarded(ws, [&] { get<double>(ws)->update_vectors(q, l, u); });
+}
+int qpcg_f32_update_vectors(qpcg_workspace* ws, const float* q, const float* l, const float* u) {
+  return guarded(ws, [&] { get<float>(ws)->update_vectors(q, l, u); });
+}
+int qpcg_f64_solve(qpcg_workspace* ws, qpcg_info* info, double* x, double* z, double* y,
+                   double* cert) {
+  return guarded(ws, [&] { get<double>(ws)->solve(info, x, z, y, cert); });
+}
+int qpcg_f32_solve(qpcg_workspace* ws, qpcg_info* info, float* x, float* z, float* y,
+                   float* cert) {
+  return guarded(ws, [&] { get<float>(ws)->solve(info, x, z, y, cert); });
+}
+int qpcg_f64_solve_problem(const qpcg_csr_f64* p, const double* q, const qpcg_csr_f64* a,
+                           const double* l, const double* u, const qpcg_settings* s,
+                           const qpcg_options* o, const double* wx, const double* wz,
+                           const double* wy, qpcg_info* info, double* x, double* z, double* y,
+                           double* cert, char* msg, size_t msg_len) {
+  return solve_problem_impl<double>(p, q, a, l, u, s, o, wx, wz, wy, info, x, z, y, cert, msg,
+                                    msg_len);
+}
+int qpcg_f32_solve_problem(const qpcg_csr_f32* p, const float* q, const qpcg_csr_f32* a,
+                           const float* l, const float* u, const qpcg_settings* s,
+                           const qpcg_options* o, const float* wx, const float* wz,
+                           const float* wy, qpcg_info* info, float* x, float* z, float* y,
+                           float* cert, char* msg, size_t msg_len) {
+  return solve_problem_impl<float>(p, q, a, l, u, s, o, wx, wz, wy, info, x, z, y, cert, msg,
+                                   msg_len);
+}
+void qpcg_cleanup(qpcg_workspace* ws) { delete ws; }
+const char* qpcg_last_error(const qpcg_workspace* ws) {
+  return ws ? ws->err.c_str() : g_last_error.c_str();
+}
+
+uint32_t qpcg_get_pcg_calls(const qpcg_workspace* ws, qpcg_pcg_call* out, uint32_t cap) {
+  auto* w = const_cast<qpcg_workspace*>(ws);
+  if (!w) return 0;
+  return w->w64 ? calls_of(w->w64.get(), out, cap) : w->w32 ? calls_of(w->w32.get(), out, cap) : 0;
+}
+uint32_t qpcg_get_rho_updates(const qpcg_workspace* ws, qpcg_rho_update* out, uint32_t cap) {
+  auto* w = const_cast<qpcg_workspace*>(ws);
+  if (!w) return 0;
+  return w->w64 ? rhos_of(w->w64.get(), out, cap) : w->w32 ? rhos_of(w->w32.get(), out, cap) : 0;
+}
+uint32_t qpcg_get_check_iterations(const qpcg_workspace* ws, uint32_t* out, uint32_t cap) {
+  auto* w = const_cast<qpcg_workspace*>(ws);
+  if (!w) return 0;
+  return w->w64 ? checks_of(w->w64.get(), out, cap)
+                : w->w32 ? checks_of(w->w32.get(), out, cap) : 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,358 @@
+// setup.cuh — device-side setup: validation, symmetrize_upper, transpose_csr,
+// modified Ruiz equilibration and the operator's diagonal caches.
+//
+// Everything here is bit-exact with the reference (SURVEY.md §8(c) parity
+// ladder rungs 1-2):
+//   * transpose_csr (sparse.hpp:207-232): stable radix sort of entry indices by
+//     column => each output row lists source rows in increasing order, exactly
+//     the reference's row-major scatter order; the permutation is kept so the
+//     scaled A^T can be re-derived from scaled A (scaling.hpp:175) by a gather.
+//   * symmetrize_upper (sparse.hpp:237-281): output row j = [mirrored strict-
+//     upper entries of column j in source-row order] ++ [input row j].
+//   * Ruiz (scaling.hpp:92-187): max-reductions are order-free; scalings are
+//     elementwise products in the reference's order ((v*d_row)*d_col); the
+//     one sequential sum (mean of P column norms, :156-158) runs as a single
+//     ordered chain that skips exact zeros (x + 0 == x for x >= 0).
+//   * diag_ata (sparse.hpp:401-408) = per-A^T-row sequential sum of squares;
+//     extract_diagonal (sparse.hpp:382-397) = first diagonal match per row.
+#pragma once
+
+#include "spmv.cuh"
+
+namespace qpcg_b200 {
+
+// -------------------------------------------------------- visitor kernels
+// Calls f(row, k) for every stored entry, driven by a plan (load balanced).
+template <typename T, class F>
+__global__ void __launch_bounds__(kThreads) plan_visit_kernel(DevCsr<T> M, SpmvPlan<T> P, F f) {
+  if (blockIdx.x < P.nb_items) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t it = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (it >= P.n_items) return;
+    const WorkItem item = P.items[it];
+    for (uint32_t k = item.beg + lane; k < item.end; k += 32) f(item.row, k);
+  } else {
+    const uint32_t idx = (blockIdx.x - P.nb_items) * kThreads + threadIdx.x;
+    if (idx >= P.n_short) return;
+    const uint32_t r = P.short_rows[idx];
+    for (uint32_t k = M.rp[r]; k < M.rp[r + 1]; ++k) f(r, k);
+  }
+}
+template <typename T, class F>
+void plan_visit(const DevCsr<T>& M, const SpmvPlan<T>& P, F f, cudaStream_t s) {
+  if (P.grid() == 0) return;
+  plan_visit_kernel<T, F><<<P.grid(), kThreads, 0, s>>>(M, P, f);
+  CK_LAUNCH();
+}
+
+struct RowOfFn {
+  uint32_t* row_of;
+  __device__ void operator()(uint32_t r, uint32_t k) const { row_of[k] = r; }
+};
+template <typename T>
+struct ScaleRowColFn {  // v = (v * dr[row]) * dc[col]  (scale_rows then scale_columns)
+  T* val;
+  const uint32_t* ci;
+  const T* dr;
+  const T* dc;
+  __device__ void operator()(uint32_t r, uint32_t k) const { val[k] = (val[k] * dr[r]) * dc[ci[k]]; }
+};
+
+template <typename F>
+__global__ void for_n_kernel(uint32_t n, F f) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) f(i);
+}
+template <typename F>
+void for_n(uint32_t n, F f, cudaStream_t s) {
+  if (n == 0) return;
+  for_n_kernel<F><<<grid_for(n), kThreads, 0, s>>>(n, f);
+  CK_LAUNCH();
+}
+
+// ---------------------------------------------------------- validation
+// Error keys: the first violation in the reference's check order wins.
+// Key layout (uint64): [category:8][row or index:32][pos:24]
+enum ValCat : uint32_t {
+  kValPRowPtr = 1,  // P csr row loop
+  kValARowPtr = 2,  // A csr row loop
+  kValPBelow = 3,   // problem: P has entries below diagonal
+  kValPFinite = 4,
+  kValAFinite = 5,
+  kValQFinite = 6,
+  kValBounds = 7,
+};
+
+__device__ __forceinline__ void val_report(unsigned long long* key, uint32_t cat, uint32_t idx,
+                                           uint32_t pos) {
+  const unsigned long long k = ((unsigned long long)cat << 56) |
+                               ((unsigned long long)idx << 24) | (pos & 0xffffffu);
+  atomicMin(key, k);
+}
+
+// sparse.hpp:110-123 per-row checks; pos 0 = nondecreasing, 2j+1 = bound of
+// j-th entry, 2j+2 = ordering of j-th entry
+__global__ void validate_csr_rows_kernel(const uint32_t* rp, const uint32_t* ci, uint32_t rows,
+                                         uint32_t cols, uint32_t cat, int check_upper,
+                                         unsigned long long* key) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const uint32_t b = rp[r], e = rp[r + 1];
+    if (e < b) {
+      val_report(key, cat, r, 0);
+      continue;
+    }
+    for (uint32_t k = b; k < e; ++k) {
+      const uint32_t j = k - b;
+      if (ci[k] >= cols) {
+        val_report(key, cat, r, 2 * j + 1);
+        break;
+      }
+      if (k > b && ci[k] <= ci[k - 1]) {
+        val_report(key, cat, r, 2 * j + 2);
+        break;
+      }
+    }
+    if (check_upper) {
+      for (uint32_t k = b; k < e; ++k)
+        if (ci[k] < r) {
+          val_report(key, kValPBelow, r, k - b);
+          break;
+        }
+    }
+  }
+}
+
+template <typename T>
+__global__ void validate_values_kernel(const T* v, uint32_t n, uint32_t cat,
+                                       unsigned long long* key) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (!isfinite(v[i])) val_report(key, cat, i, 0);
+}
+
+// problem.hpp:86-91 per bound: NaN (pos 0), inf-side (pos 1), l > u (pos 2)
+template <typename T>
+__global__ void validate_bounds_kernel(const T* l, const T* u, uint32_t m, unsigned long long* key) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const T li = l[i], ui = u[i];
+    if (isnan(li) || isnan(ui))
+      val_report(key, kValBounds, i, 0);
+    else if (li == (T)INFINITY || ui == -(T)INFINITY)
+      val_report(key, kValBounds, i, 1);
+    else if (li > ui)
+      val_report(key, kValBounds, i, 2);
+  }
+}
+
+inline const char* validation_message(unsigned long long key) {
+  const uint32_t cat = uint32_t(key >> 56);
+  const uint32_t pos = uint32_t(key & 0xffffffu);
+  switch (cat) {
+    case kValPRowPtr:
+    case kValARowPtr:
+      if (pos == 0) return "csr: row_ptr must be nondecreasing";
+      if (pos & 1u) return "csr: column index out of bounds";
+      return "csr: column indices must be strictly increasing within a row";
+    case kValPBelow: return "problem: P has entries below diagonal";
+    case kValPFinite: return "problem: P not finite";
+    case kValAFinite: return "problem: A not finite";
+    case kValQFinite: return "problem: q not finite";
+    case kValBounds:
+      if (pos == 0) return "problem: bounds contain NaN";
+      if (pos == 1) return "problem: l must be < +inf and u > -inf";
+      return "problem: l must not exceed u";
+  }
+  return "problem: invalid";
+}
+
+// ------------------------------------------------------------ transpose
+struct TransposeMap {
+  uint32_t* perm = nullptr;  // [nnz] output position -> source entry index
+};
+
+__global__ void count_cols_kernel(const uint32_t* ci, uint32_t nnz, uint32_t* cnt) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += gridDim.x * blockDim.x)
+    atomicAdd(cnt + ci[k], 1u);
+}
+
+inline int bits_for(uint32_t n) {
+  int b = 1;
+  while (b < 32 && (1ull << b) < (unsigned long long)n) ++b;
+  return b;
+}
+
+// Structure of the transpose of (rows x cols, row_of[], ci[]):
+// out_rp [cols+1], out_ci [nnz] (= source rows), perm [nnz].
+inline void transpose_structure(const uint32_t* ci, const uint32_t* row_of, uint32_t cols,
+                                uint32_t nnz, uint32_t* out_rp, uint32_t* out_ci, uint32_t* perm,
+                                CubTemp& tmp, cudaStream_t s) {
+  CK(cudaMemsetAsync(out_rp, 0, sizeof(uint32_t) * (cols + 1), s));
+  if (nnz == 0) return;
+  uint32_t *cnt, *keys_out, *idx;
+  CK(cudaMalloc(&cnt, sizeof(uint32_t) * (cols + 1)));
+  CK(cudaMalloc(&keys_out, sizeof(uint32_t) * nnz));
+  CK(cudaMalloc(&idx, sizeof(uint32_t) * nnz));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (cols + 1), s));
+  count_cols_kernel<<<grid_for(nnz), kThreads, 0, s>>>(ci, nnz, cnt);
+  CK_LAUNCH();
+  exclusive_scan_u32(cnt, out_rp, cols + 1, tmp, s);  // cnt[cols] == 0 -> out_rp[cols] = nnz
+  iota_kernel<<<grid_for(nnz), kThreads, 0, s>>>(idx, nnz);
+  CK_LAUNCH();
+  size_t b = 0;
+  const int nb = bits_for(cols);
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, b, ci, keys_out, idx, perm, nnz, 0, nb, s));
+  tmp.ensure(b);
+  CK(cub::DeviceRadixSort::SortPairs(tmp.ptr, b, ci, keys_out, idx, perm, nnz, 0, nb, s));
+  const uint32_t* perm_c = perm;
+  for_n(nnz, [=] __device__(uint32_t i) { out_ci[i] = row_of[perm_c[i]]; }, s);
+  CK(cudaStreamSynchronize(s));
+  CK(cudaFree(cnt));
+  CK(cudaFree(keys_out));
+  CK(cudaFree(idx));
+}
+
+template <typename T>
+void gather_values(const T* src, const uint32_t* perm, uint32_t nnz, T* dst, cudaStream_t s) {
+  for_n(nnz, [=] __device__(uint32_t i) { dst[i] = src[perm[i]]; }, s);
+}
+
+// ---------------------------------------------------- symmetrize_upper
+// Returns nnz of the full matrix; fills the device arrays of `out` (allocated
+// here).  up_row_of is the row of each upper entry.
+template <typename T>
+uint32_t symmetrize_upper_dev(const DevCsr<T>& up, const uint32_t* up_row_of, DevCsr<T>& out,
+                              CubTemp& tmp, cudaStream_t s) {
+  const uint32_t n = up.rows, nnz = up.nnz;
+  // strict-upper entries, in source order
+  uint32_t *flags, *pos, *sel, *sel_cols, *lower_rp, *lower_ci, *lower_perm;
+  CK(cudaMalloc(&flags, sizeof(uint32_t) * (nnz + 1)));
+  CK(cudaMalloc(&pos, sizeof(uint32_t) * (nnz + 1)));
+  const uint32_t* ci = up.ci;
+  for_n(nnz, [=] __device__(uint32_t k) { flags[k] = ci[k] != up_row_of[k]; }, s);
+  exclusive_scan_u32(flags, pos, nnz, tmp, s);
+  const uint32_t nstrict = scan_total(flags, pos, nnz, s);
+  CK(cudaMalloc(&sel, sizeof(uint32_t) * (nstrict + 1)));
+  CK(cudaMalloc(&sel_cols, sizeof(uint32_t) * (nstrict + 1)));
+  CK(cudaMalloc(&lower_rp, sizeof(uint32_t) * (n + 1)));
+  CK(cudaMalloc(&lower_ci, sizeof(uint32_t) * (nstrict + 1)));
+  CK(cudaMalloc(&lower_perm, sizeof(uint32_t) * (nstrict + 1)));
+  for_n(nnz, [=] __device__(uint32_t k) {
+    if (flags[k]) {
+      sel[pos[k]] = k;
+      sel_cols[pos[k]] = ci[k];
+    }
+  }, s);
+  // lower part = transpose of the strict upper part (rows ordered by source row)
+  uint32_t* sel_rows;
+  CK(cudaMalloc(&sel_rows, sizeof(uint32_t) * (nstrict + 1)));
+  for_n(nstrict, [=] __device__(uint32_t i) { sel_rows[i] = up_row_of[sel[i]]; }, s);
+  transpose_structure(sel_cols, sel_rows, n, nstrict, lower_rp, lower_ci, lower_perm, tmp, s);
+  // out row j: lower_cnt(j) + upper_len(j)
+  uint32_t *cnt;
+  CK(cudaMalloc(&cnt, sizeof(uint32_t) * (n + 1)));
+  const uint32_t* urp = up.rp;
+  for_n(n + 1, [=] __device__(uint32_t j) {
+    cnt[j] = j < n ? (lower_rp[j + 1] - lower_rp[j]) + (urp[j + 1] - urp[j]) : 0u;
+  }, s);
+  out.rows = out.cols = n;
+  out.nnz = nstrict + nnz;
+  CK(cudaMalloc(&out.rp, sizeof(uint32_t) * (n + 1)));
+  CK(cudaMalloc(&out.ci, sizeof(uint32_t) * (out.nnz + 1)));
+  CK(cudaMalloc(&out.val, sizeof(T) * (out.nnz + 1)));
+  exclusive_scan_u32(cnt, out.rp, n + 1, tmp, s);
+  uint32_t* orp = out.rp;
+  uint32_t* oci = out.ci;
+  T* ov = out.val;
+  const T* uv = up.val;
+  // mirrored entries
+  for_n(nstrict, [=] __device__(uint32_t i) {
+    const uint32_t j = sel_cols[lower_perm[i]];  // output row (= source column)
+    const uint32_t dst = orp[j] + (i - lower_rp[j]);
+    oci[dst] = lower_ci[i];
+    ov[dst] = uv[sel[lower_perm[i]]];
+  }, s);
+  // own entries
+  for_n(nnz, [=] __device__(uint32_t k) {
+    const uint32_t j = up_row_of[k];
+    const uint32_t dst = orp[j] + (lower_rp[j + 1] - lower_rp[j]) + (k - urp[j]);
+    oci[dst] = ci[k];
+    ov[dst] = uv[k];
+  }, s);
+  CK(cudaStreamSynchronize(s));
+  for (void* p : {(void*)flags, (void*)pos, (void*)sel, (void*)sel_cols, (void*)lower_rp,
+                  (void*)lower_ci, (void*)lower_perm, (void*)sel_rows, (void*)cnt})
+    CK(cudaFree(p));
+  return out.nnz;
+}
+
+// ------------------------------------------------------- row reductions
+template <typename T>
+struct StoreEpi {
+  T* out;
+  __device__ bool init() { return true; }
+  __device__ void operator()(uint32_t r, const T (&s)[1]) const { out[r] = s[0]; }
+};
+
+template <typename T>
+void row_inf_norms(const DevCsr<T>& M, const SpmvPlan<T>& P, T* out, cudaStream_t s) {
+  if (M.rows == 0) return;
+  launch_spmv<T, 1, MaxAbsOp>(M, P, GatherNone<T, 1>{}, StoreEpi<T>{out}, s);
+}
+
+// diag_ata: warp per A^T row, sequential sum of squares in stored order.
+template <typename T>
+__global__ void diag_ata_kernel(DevCsr<T> AT, T* out) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < AT.rows; r += nwarps) {
+    const uint32_t b = AT.rp[r], e = AT.rp[r + 1];
+    T s = T(0);
+    for (uint32_t k0 = b; k0 < e; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      const T v = k < e ? AT.val[k] : T(0);
+      const T sq = v * v;
+      const uint32_t cnt = min(32u, e - k0);
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const T t = __shfl_sync(0xffffffffu, sq, j);
+        s += t;
+      }
+    }
+    if (lane == 0) out[r] = s;
+  }
+}
+
+// extract_diagonal
+template <typename T>
+__global__ void extract_diag_kernel(DevCsr<T> P, T* out) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < P.rows; r += gridDim.x * blockDim.x) {
+    T d = T(0);
+    for (uint32_t k = P.rp[r]; k < P.rp[r + 1]; ++k)
+      if (P.ci[k] == r) {
+        d = P.val[k];
+        break;
+      }
+    out[r] = d;
+  }
+}
+
+// Sequential sum of v[0..n) in index order (skipping exact zeros, which do
+// not change a non-negative running sum), then divided by n: the mean of
+// scaling.hpp:156-158.  One block; warp 0 does the ordered chain.
+template <typename T>
+__global__ void ordered_mean_kernel(const T* v, uint32_t n, T* out) {
+  if (threadIdx.x >= 32) return;
+  const uint32_t lane = threadIdx.x;
+  T s = T(0);
+  for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const T x = i < n ? v[i] : T(0);
+    uint32_t mask = __ballot_sync(0xffffffffu, x != T(0));
+    while (mask) {
+      const int j = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const T t = __shfl_sync(0xffffffffu, x, j);
+      s += t;
+    }
+  }
+  if (lane == 0) *out = s / T(n);
+}
+
+}  // namespace qpcg_b200

@@ -1,0 +1,358 @@
+// spmv.cuh — deterministic, skew-robust CSR SpMV for sm_100a.
+//
+// Reference semantics: `spmv` (sparse.hpp:283-303), y[r] = sum_k val[k] *
+// x[col[k]].  The reference sums each row left to right; here:
+//   * rows with <= kShortRowMax nnz ("S bin") run one thread per row and sum
+//     left to right — bit-identical to the reference for those rows;
+//   * longer rows are cut into work items of <= kChunk nnz ("W bin"), one
+//     warp per item, lanes striding the item with coalesced loads; lanes
+//     combine with a fixed xor-butterfly and multi-item rows combine their
+//     per-item partials in item order.  The order is fixed per matrix, so
+//     results are reproducible run to run.
+// The plan (bins + items) is built once on the device at setup from row_ptr
+// alone (row-length statistics), so A, A^T and P of any
+// skew (portfolio: one 141k-nnz row next to 141k one-nnz rows; svm A^T: 1000
+// rows of 151k) are load-balanced by the hardware block scheduler.
+//
+// The kernel is templated on
+//   NCOL   number of gathered vectors sharing one pass over the matrix
+//          (e.g. A^T (rho z - y) and A^T (rho z~) in one stream, SURVEY §7
+//          hard part 4b),
+//   Op     SumOp (dot of row with gathered vectors) or MaxAbsOp (row_inf_norms,
+//          sparse.hpp:324-330),
+//   Gather functor producing the NCOL gathered values for a column index,
+//   Epi    functor consuming (row, sums[NCOL]) — the fused epilogue.
+#pragma once
+
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace qpcg_b200 {
+
+struct WorkItem {
+  uint32_t row, beg, end, lr;  // lr: long-row index, UINT32_MAX if single item
+};
+
+template <typename T>
+struct SpmvPlan {
+  uint32_t n_items = 0, n_short = 0, n_long = 0, n_partials = 0;
+  uint32_t nb_items = 0, nb_short = 0;
+  WorkItem* items = nullptr;    // [n_items], longest first
+  uint32_t* short_rows = nullptr;  // [n_short], increasing row order
+  uint2* lrinfo = nullptr;      // [n_long] {partial base, item count}
+  T* partials = nullptr;        // [n_partials * kMaxCols]
+  uint32_t* counters = nullptr; // [n_long], zero between launches
+  uint32_t grid() const { return nb_items + nb_short; }
+};
+
+constexpr int kMaxCols = 3;
+
+// ------------------------------------------------------------------ ops
+struct SumOp {
+  template <typename T>
+  __device__ __forceinline__ static void acc(T& a, T v, T g) { a += v * g; }
+  template <typename T>
+  __device__ __forceinline__ static T warp(T a) { return warp_sum(a); }
+  template <typename T>
+  __device__ __forceinline__ static T join(T a, T b) { return a + b; }
+  static constexpr bool kNeedsGather = true;
+};
+struct MaxAbsOp {
+  template <typename T>
+  __device__ __forceinline__ static void acc(T& a, T v, T) {
+    T x = v < T(0) ? -v : v;
+    a = x > a ? x : a;
+  }
+  template <typename T>
+  __device__ __forceinline__ static T warp(T a) { return warp_max(a); }
+  template <typename T>
+  __device__ __forceinline__ static T join(T a, T b) { return b > a ? b : a; }
+  static constexpr bool kNeedsGather = false;
+};
+
+// gather helpers
+template <typename T>
+struct GatherVec {  // x[c]
+  const T* __restrict__ x;
+  __device__ __forceinline__ void init() {}
+  __device__ __forceinline__ void operator()(uint32_t c, T (&g)[1]) const { g[0] = __ldg(x + c); }
+};
+template <typename T, int N>
+struct GatherNone {
+  __device__ __forceinline__ void init() {}
+  __device__ __forceinline__ void operator()(uint32_t, T (&g)[N]) const {
+#pragma unroll
+    for (int j = 0; j < N; ++j) g[j] = T(0);
+  }
+};
+
+// --------------------------------------------------------------- kernel
+template <typename T, int NCOL, class Op, class Gather, class Epi, int U = 4>
+__global__ void __launch_bounds__(kThreads) spmv_kernel(DevCsr<T> M, SpmvPlan<T> P, Gather gather,
+                                                       Epi epi) {
+  // functors load their device-resident scalars (rho, flags) once per thread;
+  // an inactive epilogue (e.g. a skipped certificate pass) exits immediately
+  if (!epi.init()) return;
+  gather.init();
+  const T* __restrict__ val = M.val;
+  const uint32_t* __restrict__ ci = M.ci;
+  if (blockIdx.x < P.nb_items) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t it = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (it >= P.n_items) return;
+    const WorkItem item = P.items[it];
+    T acc[NCOL];
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
+    uint32_t k = item.beg + lane;
+    const uint32_t end = item.end;
+    for (; k + 32u * (U - 1) < end; k += 32u * U) {
+      uint32_t c[U];
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        v[u] = ld_stream(val + k + 32u * u);
+        if (Op::kNeedsGather) c[u] = ld_stream(ci + k + 32u * u);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        T g[NCOL];
+        if (Op::kNeedsGather) gather(c[u], g);
+#pragma unroll
+        for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v[u], Op::kNeedsGather ? g[j] : T(0));
+      }
+    }
+    for (; k < end; k += 32u) {
+      const T v = ld_stream(val + k);
+      T g[NCOL];
+      if (Op::kNeedsGather) gather(ld_stream(ci + k), g);
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v, Op::kNeedsGather ? g[j] : T(0));
+    }
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) acc[j] = Op::warp(acc[j]);
+    if (lane != 0) return;
+    if (item.lr == 0xffffffffu) {
+      epi(item.row, acc);
+      return;
+    }
+    // multi-item row: publish the partial, the last item to finish combines
+    // all partials in item order (deterministic).
+    const uint2 info = P.lrinfo[item.lr];
+    const uint32_t chunk = (item.beg - M.rp[item.row]) / kChunk;
+    T* part = P.partials + (size_t)(info.x + chunk) * kMaxCols;
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) part[j] = acc[j];
+    __threadfence();
+    const uint32_t prev = atomicAdd(P.counters + item.lr, 1u);
+    if (prev != info.y - 1) return;
+    __threadfence();
+    T tot[NCOL];
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) tot[j] = T(0);
+    for (uint32_t q = 0; q < info.y; ++q) {
+      const T* pp = P.partials + (size_t)(info.x + q) * kMaxCols;
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) tot[j] = Op::join(tot[j], __ldcg(pp + j));
+    }
+    P.counters[item.lr] = 0u;
+    epi(item.row, tot);
+  } else {
+    const uint32_t idx = (blockIdx.x - P.nb_items) * kThreads + threadIdx.x;
+    if (idx >= P.n_short) return;
+    const uint32_t r = P.short_rows[idx];
+    const uint32_t b = __ldg(M.rp + r), e = __ldg(M.rp + r + 1);
+    T acc[NCOL];
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
+    for (uint32_t k = b; k < e; ++k) {
+      const T v = ld_stream(val + k);
+      T g[NCOL];
+      if (Op::kNeedsGather) gather(ld_stream(ci + k), g);
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v, Op::kNeedsGather ? g[j] : T(0));
+    }
+    epi(r, acc);
+  }
+}
+
+template <typename T, int NCOL, class Op, class Gather, class Epi>
+void launch_spmv(const DevCsr<T>& M, const SpmvPlan<T>& P, const Gather& g, const Epi& e,
+                 cudaStream_t s) {
+  if (P.grid() == 0) return;
+  spmv_kernel<T, NCOL, Op, Gather, Epi><<<P.grid(), kThreads, 0, s>>>(M, P, g, e);
+  CK_LAUNCH();
+}
+
+// ------------------------------------------------------------ plan build
+__global__ void plan_classify_kernel(const uint32_t* __restrict__ rp, uint32_t rows,
+                                     uint32_t* is_short, uint32_t* nch, uint32_t* is_multi,
+                                     uint32_t* multi_nch) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const uint32_t len = rp[r + 1] - rp[r];
+    const uint32_t s = len <= kShortRowMax;
+    const uint32_t c = s ? 0u : ceil_div(len, kChunk);
+    is_short[r] = s;
+    nch[r] = c;
+    is_multi[r] = c > 1;
+    multi_nch[r] = c > 1 ? c : 0u;
+  }
+}
+
+__global__ void plan_emit_kernel(const uint32_t* __restrict__ rp, uint32_t rows,
+                                 const uint32_t* is_short, const uint32_t* short_pos,
+                                 const uint32_t* nch, const uint32_t* item_off,
+                                 const uint32_t* lr_idx, const uint32_t* pbase,
+                                 uint32_t* short_rows, WorkItem* items, uint32_t* item_len,
+                                 uint2* lrinfo) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    if (is_short[r]) {
+      short_rows[short_pos[r]] = r;
+      continue;
+    }
+    const uint32_t c = nch[r], b = rp[r], e = rp[r + 1];
+    const uint32_t lr = c > 1 ? lr_idx[r] : 0xffffffffu;
+    if (c > 1) lrinfo[lr] = make_uint2(pbase[r], c);
+    for (uint32_t q = 0; q < c; ++q) {
+      WorkItem w;
+      w.row = r;
+      w.beg = b + q * kChunk;
+      w.end = min(e, w.beg + kChunk);
+      w.lr = lr;
+      items[item_off[r] + q] = w;
+      item_len[item_off[r] + q] = kChunk - (w.end - w.beg);  // sort key: longest first
+    }
+  }
+}
+
+__global__ void iota_kernel(uint32_t* out, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = i;
+}
+
+__global__ void plan_gather_items_kernel(const WorkItem* in, const uint32_t* order, uint32_t n,
+                                         WorkItem* out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = in[order[i]];
+}
+
+// Scratch-backed helpers for cub device calls.
+struct CubTemp {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (ptr) CK(cudaFree(ptr));
+    CK(cudaMalloc(&ptr, b));
+    bytes = b;
+  }
+  ~CubTemp() {
+    if (ptr) cudaFree(ptr);
+  }
+};
+
+inline void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint32_t n, CubTemp& tmp,
+                               cudaStream_t s) {
+  if (n == 0) return;
+  size_t b = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, b, in, out, n, s));
+  tmp.ensure(b);
+  CK(cub::DeviceScan::ExclusiveSum(tmp.ptr, b, in, out, n, s));
+}
+
+inline uint32_t grid_for(uint64_t n, int threads = kThreads) {
+  uint64_t g = (n + threads - 1) / threads;
+  if (g > 8u * kNumSMs * 8u) g = 8u * kNumSMs * 8u;
+  return g == 0 ? 1u : uint32_t(g);
+}
+
+// Total of an exclusive scan: last exclusive value + last input.
+inline uint32_t scan_total(const uint32_t* in, const uint32_t* ex, uint32_t n, cudaStream_t s) {
+  if (n == 0) return 0;
+  uint32_t a = 0, b = 0;
+  CK(cudaMemcpyAsync(&a, ex + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&b, in + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return a + b;
+}
+
+template <typename T>
+void plan_free(SpmvPlan<T>& P) {
+  cudaFree(P.items);
+  cudaFree(P.short_rows);
+  cudaFree(P.lrinfo);
+  cudaFree(P.partials);
+  cudaFree(P.counters);
+  P = SpmvPlan<T>{};
+}
+
+// Build the plan for a CSR structure whose row_ptr lives on the device.
+template <typename T>
+SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaStream_t s) {
+  SpmvPlan<T> P;
+  if (rows == 0) return P;
+  uint32_t *is_short, *nch, *is_multi, *multi_nch, *short_pos, *item_off, *lr_idx, *pbase;
+  const size_t bytes = sizeof(uint32_t) * rows;
+  CK(cudaMalloc(&is_short, bytes));
+  CK(cudaMalloc(&nch, bytes));
+  CK(cudaMalloc(&is_multi, bytes));
+  CK(cudaMalloc(&multi_nch, bytes));
+  CK(cudaMalloc(&short_pos, bytes));
+  CK(cudaMalloc(&item_off, bytes));
+  CK(cudaMalloc(&lr_idx, bytes));
+  CK(cudaMalloc(&pbase, bytes));
+  plan_classify_kernel<<<grid_for(rows), kThreads, 0, s>>>(d_rp, rows, is_short, nch, is_multi,
+                                                          multi_nch);
+  CK_LAUNCH();
+  exclusive_scan_u32(is_short, short_pos, rows, tmp, s);
+  exclusive_scan_u32(nch, item_off, rows, tmp, s);
+  exclusive_scan_u32(is_multi, lr_idx, rows, tmp, s);
+  exclusive_scan_u32(multi_nch, pbase, rows, tmp, s);
+  P.n_short = scan_total(is_short, short_pos, rows, s);
+  P.n_items = scan_total(nch, item_off, rows, s);
+  P.n_long = scan_total(is_multi, lr_idx, rows, s);
+  P.n_partials = scan_total(multi_nch, pbase, rows, s);
+  CK(cudaMalloc(&P.short_rows, sizeof(uint32_t) * (P.n_short ? P.n_short : 1)));
+  CK(cudaMalloc(&P.items, sizeof(WorkItem) * (P.n_items ? P.n_items : 1)));
+  CK(cudaMalloc(&P.lrinfo, sizeof(uint2) * (P.n_long ? P.n_long : 1)));
+  CK(cudaMalloc(&P.partials, sizeof(T) * kMaxCols * (P.n_partials ? P.n_partials : 1)));
+  CK(cudaMalloc(&P.counters, sizeof(uint32_t) * (P.n_long ? P.n_long : 1)));
+  CK(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * (P.n_long ? P.n_long : 1), s));
+  WorkItem* items_tmp = nullptr;
+  uint32_t *keys = nullptr, *keys_out = nullptr, *order = nullptr, *order_out = nullptr;
+  const uint32_t ni = P.n_items ? P.n_items : 1;
+  CK(cudaMalloc(&items_tmp, sizeof(WorkItem) * ni));
+  CK(cudaMalloc(&keys, sizeof(uint32_t) * ni));
+  CK(cudaMalloc(&keys_out, sizeof(uint32_t) * ni));
+  CK(cudaMalloc(&order, sizeof(uint32_t) * ni));
+  CK(cudaMalloc(&order_out, sizeof(uint32_t) * ni));
+  plan_emit_kernel<<<grid_for(rows), kThreads, 0, s>>>(d_rp, rows, is_short, short_pos, nch,
+                                                      item_off, lr_idx, pbase, P.short_rows,
+                                                      items_tmp, keys, P.lrinfo);
+  CK_LAUNCH();
+  if (P.n_items > 0) {
+    // stable sort of items by length (longest first) for a balanced tail
+    iota_kernel<<<grid_for(P.n_items), kThreads, 0, s>>>(order, P.n_items);
+    CK_LAUNCH();
+    size_t b = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, b, keys, keys_out, order, order_out, P.n_items, 0,
+                                       12, s));
+    tmp.ensure(b);
+    CK(cub::DeviceRadixSort::SortPairs(tmp.ptr, b, keys, keys_out, order, order_out, P.n_items, 0,
+                                       12, s));
+    plan_gather_items_kernel<<<grid_for(P.n_items), kThreads, 0, s>>>(items_tmp, order_out,
+                                                                     P.n_items, P.items);
+    CK_LAUNCH();
+  }
+  P.nb_items = ceil_div(P.n_items, kWarpsPerBlock);
+  P.nb_short = ceil_div(P.n_short, kThreads);
+  CK(cudaStreamSynchronize(s));
+  for (void* p : {(void*)is_short, (void*)nch, (void*)is_multi, (void*)multi_nch, (void*)short_pos,
+                  (void*)item_off, (void*)lr_idx, (void*)pbase, (void*)items_tmp, (void*)keys,
+                  (void*)keys_out, (void*)order, (void*)order_out})
+    CK(cudaFree(p));
+  return P;
+}
+
+}  // namespace qpcg_b200

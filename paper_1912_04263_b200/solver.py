@@ -1,0 +1,200 @@
+"""Host-side mirror of the reference's solve entry point over the C-ABI.
+
+``solve(problem, settings, initial=None, diag=None)`` has the meaning of
+``qpcg::solve`` (solver.hpp:386-541) and raises the same error classes
+(``ValueError`` for std::invalid_argument, ``NotPositiveDefiniteError``).
+``Workspace`` is the OSQP-style split (setup / warm_start / update_rho /
+update_vectors / solve) of include/qpcg_b200.h.
+
+There is no CPU fallback: if ``libqpcg_b200.so`` is missing or no CUDA
+device is present, loading fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import _abi
+from .problem import (NotPositiveDefiniteError, QpProblem, Settings, SolveDiagnostics,
+                      WarmStart, outcome_from_c)
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqpcg_b200.so")
+
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    """Load the engine's C-ABI library (never falls back to anything else)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"qpcg-b200: CUDA engine not built ({LIB_PATH} missing); "
+                          "run __graft_entry__.build() / python -m paper_1912_04263_b200.build")
+    lib = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    for pre in ("f64", "f32"):
+        getattr(lib, f"qpcg_{pre}_setup").argtypes = [C.POINTER(vp), vp, vp, vp, vp, vp, vp, vp]
+        getattr(lib, f"qpcg_{pre}_warm_start").argtypes = [vp, vp, vp, vp]
+        getattr(lib, f"qpcg_{pre}_update_rho").argtypes = [vp, C.c_double]
+        getattr(lib, f"qpcg_{pre}_update_vectors").argtypes = [vp, vp, vp, vp]
+        getattr(lib, f"qpcg_{pre}_solve").argtypes = [vp, vp, vp, vp, vp, vp]
+        getattr(lib, f"qpcg_{pre}_solve_problem").argtypes = [vp] * 15 + [C.c_char_p, C.c_size_t]
+    lib.qpcg_cleanup.argtypes = [vp]
+    lib.qpcg_last_error.argtypes = [vp]
+    lib.qpcg_last_error.restype = C.c_char_p
+    lib.qpcg_version.restype = C.c_char_p
+    lib.qpcg_get_pcg_calls.argtypes = [vp, vp, C.c_uint32]
+    lib.qpcg_get_pcg_calls.restype = C.c_uint32
+    lib.qpcg_get_rho_updates.argtypes = [vp, vp, C.c_uint32]
+    lib.qpcg_get_rho_updates.restype = C.c_uint32
+    lib.qpcg_get_check_iterations.argtypes = [vp, vp, C.c_uint32]
+    lib.qpcg_get_check_iterations.restype = C.c_uint32
+    _lib = lib
+    return lib
+
+
+def _raise(rc: int, msg: str):
+    if rc == _abi.QPCG_ERR_INVALID:
+        raise ValueError(msg)
+    if rc == _abi.QPCG_ERR_NOT_PD:
+        raise NotPositiveDefiniteError(msg)
+    if rc == _abi.QPCG_ERR_OOM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def _pre(dtype) -> str:
+    if dtype == np.float64:
+        return "f64"
+    if dtype == np.float32:
+        return "f32"
+    raise TypeError(f"unsupported dtype {dtype}")
+
+
+def make_options(device: int = -1, mode: str = "graph", record_diagnostics: bool = False,
+                 device_memory: bool = False) -> _abi.Options:
+    o = _abi.Options()
+    o.device = device
+    o.input_memory = _abi.MEM_DEVICE if device_memory else _abi.MEM_HOST
+    o.mode = _abi.MODE_EAGER if mode == "eager" else _abi.MODE_GRAPH
+    o.record_diagnostics = 1 if record_diagnostics else 0
+    o.virtual_shards = 1
+    return o
+
+
+class Workspace:
+    """OSQP-style workspace: setup once, then solve / warm_start / update_*."""
+
+    def __init__(self, problem: QpProblem, settings: Settings | None = None, device: int = -1,
+                 mode: str = "graph", record_diagnostics: bool = False):
+        self.lib = load_library()
+        self.problem = problem
+        self.dtype = problem.dtype
+        self.pre = _pre(self.dtype)
+        self.settings = settings or Settings()
+        self._opts = make_options(device, mode, record_diagnostics)
+        self._s = self.settings.to_c()
+        self._pv, self._av = problem.p_upper.view(), problem.a.view()
+        self.ws = C.c_void_p()
+        rc = getattr(self.lib, f"qpcg_{self.pre}_setup")(
+            C.byref(self.ws), C.addressof(self._pv), _abi.ptr(problem.q), C.addressof(self._av),
+            _abi.ptr(problem.l), _abi.ptr(problem.u), C.addressof(self._s),
+            C.addressof(self._opts))
+        if rc != _abi.QPCG_OK:
+            self.ws = None
+            _raise(rc, self.lib.qpcg_last_error(None).decode())
+
+    def _check(self, rc):
+        if rc != _abi.QPCG_OK:
+            _raise(rc, self.lib.qpcg_last_error(self.ws).decode())
+
+    def warm_start(self, x, z, y):
+        a = [np.ascontiguousarray(v, self.dtype) for v in (x, z, y)]
+        self._check(getattr(self.lib, f"qpcg_{self.pre}_warm_start")(self.ws, *[_abi.ptr(v) for v in a]))
+
+    def update_rho(self, rho: float):
+        self._check(getattr(self.lib, f"qpcg_{self.pre}_update_rho")(self.ws, C.c_double(rho)))
+
+    def update_vectors(self, q=None, l=None, u=None):
+        a = [None if v is None else np.ascontiguousarray(v, self.dtype) for v in (q, l, u)]
+        self._check(getattr(self.lib, f"qpcg_{self.pre}_update_vectors")(self.ws, *[_abi.ptr(v) for v in a]))
+
+    def solve(self, diag: SolveDiagnostics | None = None):
+        n, m = self.problem.n, self.problem.m
+        x, z, y = np.zeros(n, self.dtype), np.zeros(m, self.dtype), np.zeros(m, self.dtype)
+        cert = np.zeros(max(n, m), self.dtype)
+        info = _abi.Info()
+        self._check(getattr(self.lib, f"qpcg_{self.pre}_solve")(
+            self.ws, C.addressof(info), _abi.ptr(x), _abi.ptr(z), _abi.ptr(y), _abi.ptr(cert)))
+        if diag is not None:
+            fetch_diagnostics(self.lib, self.ws, diag)
+        return outcome_from_c(info, x, z, y, cert)
+
+    def close(self):
+        if self.ws:
+            self.lib.qpcg_cleanup(self.ws)
+            self.ws = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def fetch_diagnostics(lib, ws, diag: SolveDiagnostics):
+    k = lib.qpcg_get_pcg_calls(ws, None, 0)
+    buf = (_abi.PcgCall * max(k, 1))()
+    lib.qpcg_get_pcg_calls(ws, buf, k)
+    diag.pcg_calls = [dict(admm_iter=c.admm_iter, iterations=c.iterations, eps=c.eps,
+                           r_prim_scaled_inf=c.r_prim_scaled_inf,
+                           r_dual_scaled_inf=c.r_dual_scaled_inf, converged=bool(c.converged))
+                      for c in buf[:k]]
+    k = lib.qpcg_get_rho_updates(ws, None, 0)
+    rb = (_abi.RhoUpdate * max(k, 1))()
+    lib.qpcg_get_rho_updates(ws, rb, k)
+    diag.rho_updates = [dict(admm_iter=r.admm_iter, rho_before=r.rho_before, rho_after=r.rho_after)
+                        for r in rb[:k]]
+    k = lib.qpcg_get_check_iterations(ws, None, 0)
+    cb = (C.c_uint32 * max(k, 1))()
+    lib.qpcg_get_check_iterations(ws, cb, k)
+    diag.check_iterations = list(cb[:k])
+
+
+def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | None = None,
+          diag: SolveDiagnostics | None = None, device: int = -1, mode: str = "graph"):
+    """Drop-in for qpcg::solve (solver.hpp:386-541) on the B200 engine."""
+    if diag is not None:
+        with Workspace(p, settings, device, mode, record_diagnostics=True) as ws:
+            if initial is not None:
+                ws.warm_start(initial.x, initial.z, initial.y)
+            return ws.solve(diag)
+    lib = load_library()
+    pre = _pre(p.dtype)
+    n, m = p.n, p.m
+    dt = p.dtype
+    s = (settings or Settings()).to_c()
+    o = make_options(device, mode)
+    x, z, y = np.zeros(n, dt), np.zeros(m, dt), np.zeros(m, dt)
+    cert = np.zeros(max(n, m), dt)
+    info = _abi.Info()
+    pv, av = p.p_upper.view(), p.a.view()
+    w = [None, None, None] if initial is None else [np.ascontiguousarray(v, dt) for v in
+                                                      (initial.x, initial.z, initial.y)]
+    msg = C.create_string_buffer(512)
+    rc = getattr(lib, f"qpcg_{pre}_solve_problem")(
+        C.addressof(pv), _abi.ptr(p.q), C.addressof(av), _abi.ptr(p.l), _abi.ptr(p.u),
+        C.addressof(s), C.addressof(o), *[_abi.ptr(v) for v in w], C.addressof(info),
+        _abi.ptr(x), _abi.ptr(z), _abi.ptr(y), _abi.ptr(cert), msg, 512)
+    if rc != _abi.QPCG_OK:
+        _raise(rc, msg.value.decode())
+    return outcome_from_c(info, x, z, y, cert)
