@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""bench.py — B200 ADMM/PCG QP engine on BASELINE.json's headline workload.
+
+Metric (BASELINE.json): "QP solve time to eps=1e-3 (s) and PCG-iteration HBM
+GB/s vs roofline".  A *step* is one complete solve — qpcg_f64_solve_problem,
+i.e. the reference's `qpcg::solve` timed region (solver.hpp:392 -> :537:
+symmetrize, transpose, Ruiz, ADMM/PCG loop, unscale, objective) — of the
+workload `config` names (default: BASELINE configs[1], lasso with 10^4
+features x 10^5 samples at 15 % density, generated with the reference's own
+RNG and recipes; fp64; settings {"lambda_pcg": 0.01}).
+
+* value       seconds per solve with the problem already resident in HBM
+              (device-pointer inputs), CUDA events on the engine's stream.
+* e2e         the same through the reference-facing C-ABI with pinned HOST
+              arrays: H2D of P, q, A, l, u and D2H of x, z, y inside the step.
+* roofline    the dominant kernel (the A^T SpMV of the PCG operator apply,
+              Kp = P p + sigma p + A^T (rho A p)) timed with CUDA events on the
+              engine stream right after the timed region; algorithmic bytes per
+              SURVEY.md §8(d); peak = MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline  the reference itself (oracle/_ref, unmodified headers) on the
+              same instance, 1 core (it is single threaded): its setup
+              phases and hot-path operators are timed on a bounded sample and
+              the solve time is extrapolated with the solve's iteration counts.
+
+--impl reference runs only the reference CPU arm (rank 0), same metric/config.
+Multi-GPU (torchrun): each rank solves an independent instance ("replicas",
+weak scaling) until the row-sharded path lands; value = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QP solve time to eps=1e-3 (s) and PCG-iteration HBM GB/s vs roofline"
+WORKLOADS = {
+    "1": "random QP n=1000 m=10000 (reference recipe, P 3 nnz/row)",
+    "1p": "random QP n=1000 m=10000, P ~15% dense",
+    "2": "lasso 1e4 features x 1e5 samples, 15% dense (n=120000, m=120000, nnz(A)=1.5e8)",
+    "3": "huber 1e5 x 1e4, 15% dense (n=310000, m=300000, nnz(A)=1.5e8)",
+    "4": "svm 1e6 samples x 1e3 features, 15% dense (n=1001000, m=2000000, nnz(A)=1.5e8)",
+    "5a": "portfolio N~1e8 (n=142835, m=142836, nnz(A)=1.0e8)",
+    "5b": "control/MPC gen_control scale 13 (nnz(A)=1.39e8)",
+}
+COUNTS_FILE = os.path.join(ROOT, "profiles", "solve_counts.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="2", choices=sorted(WORKLOADS))
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--lambda-pcg", type=float, default=0.01)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps")
+    ap.add_argument("--kernel-reps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="graph", choices=["graph", "eager"])
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,utilization.gpu,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for l in self.lines:
+            p = [x.strip() for x in l.split(",")]
+            if len(p) >= 8:
+                rows.append(p)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        loaded = [r for r in rows if (num(r[3]) or 0) > 0] or rows
+        sm = [num(r[0]) for r in loaded if num(r[0]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": num(rows[0][1]), "samples": len(rows),
+                "samples_under_load": len(loaded), "reasons": reasons}
+
+
+# ---------------------------------------------------------- engine calls
+def _views(arrs, n, m, dev):
+    """CSR views (host numpy or device torch tensors) for the C-ABI."""
+    from paper_1912_04263_b200 import _abi
+    def p(a):
+        return C.c_void_p(a.data_ptr() if dev else a.ctypes.data)
+    pv, prp, pci, q, av, arp, aci, l, u = arrs
+    P = _abi.CsrF64()
+    P.rows, P.cols, P.nnz = n, n, int(pv.shape[0])
+    P.values, P.row_ptr, P.col_indices = p(pv), p(prp), p(pci)
+    A = _abi.CsrF64()
+    A.rows, A.cols, A.nnz = m, n, int(av.shape[0])
+    A.values, A.row_ptr, A.col_indices = p(av), p(arp), p(aci)
+    return P, A, p(q), p(l), p(u)
+
+
+class Engine:
+    def __init__(self, problem, settings, device, stream_ptr, dtype, mode):
+        import torch
+        from paper_1912_04263_b200 import _abi, solver
+        self.lib = solver.load_library()
+        self.torch = torch
+        self.n, self.m = problem.n, problem.m
+        self.settings = settings.to_c()
+        self.dtype = dtype
+        self.pre = "f64" if dtype == np.float64 else "f32"
+        tdt = torch.float64 if dtype == np.float64 else torch.float32
+        host = [problem.p_upper.values.astype(dtype), problem.p_upper.row_ptr,
+                problem.p_upper.col_indices, problem.q.astype(dtype),
+                problem.a.values.astype(dtype), problem.a.row_ptr, problem.a.col_indices,
+                problem.l.astype(dtype), problem.u.astype(dtype)]
+        # pinned host copies (e2e) and HBM-resident copies (value)
+        self.host = [torch.from_numpy(np.ascontiguousarray(h)).pin_memory() for h in host]
+        self.dev = [t.to(f"cuda:{device}", non_blocking=False) for t in self.host]
+        torch.cuda.synchronize()
+        self.host_np = [t.numpy() for t in self.host]
+        self.out_dev = [torch.empty(k, dtype=tdt, device=f"cuda:{device}")
+                        for k in (self.n, self.m, self.m, max(self.n, self.m))]
+        self.out_host = [torch.empty(k, dtype=tdt).pin_memory()
+                         for k in (self.n, self.m, self.m, max(self.n, self.m))]
+        self.bytes_in = sum(int(t.numel() * t.element_size()) for t in self.host)
+        self.opts = {}
+        for memkind in ("device", "host"):
+            o = _abi.Options()
+            o.device = device
+            o.input_memory = _abi.MEM_DEVICE if memkind == "device" else _abi.MEM_HOST
+            o.mode = _abi.MODE_EAGER if mode == "eager" else _abi.MODE_GRAPH
+            o.record_diagnostics = 0
+            o.virtual_shards = 1
+            o.stream = C.c_void_p(stream_ptr)
+            self.opts[memkind] = o
+        self._abi = _abi
+        self.msg = C.create_string_buffer(512)
+
+    def solve(self, memkind: str):
+        _abi = self._abi
+        dev = memkind == "device"
+        arrs = self.dev if dev else self.host_np
+        P, A, q, l, u = _views(arrs, self.n, self.m, dev)
+        outs = self.out_dev if dev else self.out_host
+        op = (lambda t: C.c_void_p(t.data_ptr()))
+        info = _abi.Info()
+        rc = getattr(self.lib, f"qpcg_{self.pre}_solve_problem")(
+            C.addressof(P), q, C.addressof(A), l, u, C.addressof(self.settings),
+            C.addressof(self.opts[memkind]), None, None, None, C.addressof(info),
+            *[op(t) for t in outs], self.msg, 512)
+        if rc != 0:
+            raise RuntimeError(f"solve failed rc={rc}: {self.msg.value.decode()}")
+        return info
+
+    def kernel_timing(self, reps: int):
+        """CUDA-event timing of the PCG-iteration kernels on a set-up workspace."""
+        _abi = self._abi
+        P, A, q, l, u = _views(self.dev, self.n, self.m, True)
+        ws = C.c_void_p()
+        rc = getattr(self.lib, f"qpcg_{self.pre}_setup")(
+            C.byref(ws), C.addressof(P), q, C.addressof(A), l, u, C.addressof(self.settings),
+            C.addressof(self.opts["device"]))
+        if rc != 0:
+            raise RuntimeError(self.lib.qpcg_last_error(None).decode())
+        try:
+            out = np.zeros(6)
+            self.lib.qpcg_bench_kernels.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
+            rc = self.lib.qpcg_bench_kernels(ws, reps, out.ctypes.data)
+            if rc != 0:
+                raise RuntimeError(self.lib.qpcg_last_error(ws).decode())
+        finally:
+            self.lib.qpcg_cleanup(ws)
+        return out
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_baseline(problem, counts: dict, budget_reps: int = 1) -> dict:
+    """The reference (oracle/_ref, unmodified headers, 1 core) on a bounded
+    sample of the same instance; solve time extrapolated from its measured
+    components and the solve's iteration counts."""
+    from oracle import oracle as O  # cpu_baseline leg only
+    lib = O.ref_lib()
+    P, A, q, l, u = _views([problem.p_upper.values, problem.p_upper.row_ptr,
+                            problem.p_upper.col_indices, problem.q, problem.a.values,
+                            problem.a.row_ptr, problem.a.col_indices, problem.l, problem.u],
+                           problem.n, problem.m, False)
+    out = np.zeros(9)
+    t0 = time.time()
+    rc = lib.qref_time_components_f64(C.byref(P), q, C.byref(A), l, u,
+                                      C.c_uint32(budget_reps), C.c_void_p(out.ctypes.data))
+    if rc != 0:
+        raise RuntimeError(lib.qref_last_error().decode())
+    wall = time.time() - t0
+    t_sym, t_trans, t_ruiz1, t_op, t_k, t_at, t_a, t_res = (float(v) for v in out[:8])
+    passes = int(counts.get("equil_passes", 10))
+    iters = int(counts["iterations"])
+    pcg = int(counts["pcg_iterations_total"])
+    checks = iters // 5
+    # solve() = symmetrize + transpose + Ruiz + operator build + loop.  Ruiz:
+    # the measured 1-pass call includes two transposes of A and the copies; each
+    # further pass costs the pass body only (estimated as the 1-pass time minus
+    # the two transposes).  Loop: per ADMM step the rhs A^T spmv, the PCG r0
+    # K-apply and z~ = A x~; one K-apply per PCG iteration; per check the
+    # residuals (3 spmv) and, while unsolved, the A^T infeasibility spmv.
+    pass_body = max(t_ruiz1 - 2.0 * t_trans, 0.0)
+    setup = t_sym + t_trans + t_ruiz1 + (passes - 1) * pass_body + t_op
+    loop = iters * (t_at + t_k + t_a) + pcg * t_k + checks * (t_res + t_at)
+    return {"value": setup + loop, "unit": "s", "cores": 1, "kind": "reference",
+            "sample": (f"oracle/_ref (unmodified reference headers, g++ -O3 -ffp-contract=off, "
+                       f"1 thread) on the same instance: symmetrize {t_sym:.2f}s, transpose "
+                       f"{t_trans:.2f}s, 1-pass Ruiz {t_ruiz1:.2f}s, operator build {t_op:.2f}s, "
+                       f"K-apply {t_k:.3f}s, A^T spmv {t_at:.3f}s, A spmv {t_a:.3f}s, residuals "
+                       f"{t_res:.3f}s ({wall:.1f}s of CPU); solve time EXTRAPOLATED to {passes} "
+                       f"Ruiz passes, {iters} ADMM / {pcg} PCG iterations, {checks} checks"),
+            "extrapolated": True, "nproc": os.cpu_count(),
+            "components_s": {"symmetrize": t_sym, "transpose": t_trans, "ruiz_1pass": t_ruiz1,
+                             "operator_build": t_op, "k_apply": t_k, "at_spmv": t_at,
+                             "a_spmv": t_a, "residuals": t_res, "setup_est": setup,
+                             "loop_est": loop}}
+
+
+def load_counts(config: str) -> dict:
+    try:
+        with open(COUNTS_FILE) as f:
+            return json.load(f)[config]
+    except Exception:
+        return {"iterations": 300, "pcg_iterations_total": 1500, "equil_passes": 10,
+                "source": "default guess (no recorded B200 solve)"}
+
+
+def save_counts(config: str, info) -> None:
+    try:
+        data = {}
+        if os.path.exists(COUNTS_FILE):
+            with open(COUNTS_FILE) as f:
+                data = json.load(f)
+        data[config] = {"iterations": int(info.iterations),
+                        "pcg_iterations_total": int(info.pcg_iterations_total),
+                        "equil_passes": int(info.equil_passes), "status": int(info.status),
+                        "objective": float(info.objective),
+                        "source": "B200 engine solve of the same instance (bench.py)"}
+        os.makedirs(os.path.dirname(COUNTS_FILE), exist_ok=True)
+        with open(COUNTS_FILE, "w") as f:
+            json.dump(data, f, indent=1, sort_keys=True)
+    except Exception:
+        pass
+
+
+def peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+def ncu_traffic(config: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d.get(config, {}).get("at_pass_dram_bytes")
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------- arms
+def run_reference(args, rank: int) -> None:
+    if rank != 0:
+        return
+    from paper_1912_04263_b200 import generators
+    problem = generators.config(args.config, seed=0)
+    counts = load_counts(args.config)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(problem, counts)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = float(np.mean(vals))
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference RNG + recipes, SURVEY.md §8(d))",
+            "config": {"workload": WORKLOADS[args.config], "config_id": args.config,
+                       "settings": {"lambda_pcg": args.lambda_pcg}, "iteration_counts": counts},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_1912_04263_b200 import generators
+    from paper_1912_04263_b200.problem import Settings
+    dtype = np.float64 if args.dtype == "f64" else np.float32
+    tg = time.time()
+    problem = generators.config(args.config, seed=rank)
+    gen_s = time.time() - tg
+    settings = Settings(lambda_pcg=args.lambda_pcg)
+    stream = torch.cuda.Stream(device=local)
+    with torch.cuda.stream(stream):
+        eng = Engine(problem, settings, local, stream.cuda_stream, dtype, args.mode)
+        for _ in range(args.warmup):
+            info = eng.solve("device")
+        def barrier():
+            if dist is not None:
+                dist.barrier()
+        # ---- timed region: K device-resident solves
+        barrier()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local)
+        clocks.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        infos = []
+        for _ in range(args.steps):
+            infos.append(eng.solve("device"))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        clk = clocks.stop()
+        ms = e0.elapsed_time(e1) / args.steps
+        # ---- e2e: host pinned arrays through the C-ABI
+        ke = args.e2e_steps or args.steps
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        einfos = [eng.solve("host") for _ in range(ke)]
+        f1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_e2e = f0.elapsed_time(f1) / ke
+        # ---- dominant kernel, CUDA events on the engine stream
+        kt = eng.kernel_timing(args.kernel_reps)
+    if dist is not None:
+        t = torch.tensor([ms, ms_e2e], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_e2e = float(t[0]), float(t[1])
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    last = infos[-1]
+    save_counts(args.config, last)
+    pk = peaks()
+    S = 8 if dtype == np.float64 else 4
+    at_ms, pcg_ms = kt[1], kt[2]
+    achieved = kt[4] / (at_ms * 1e-3) / 1e9
+    loop_s = last.solve_seconds
+    roofline = {"bound": "hbm", "kernel": "spmv A^T pass of the PCG operator (Kp = P p + sigma p + A^T t)",
+                "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "peak_source": pk["source"],
+                "traffic": ncu_traffic(args.config),
+                "algorithmic_bytes_per_launch": kt[4], "launch_ms": at_ms,
+                "a_pass": {"ms": kt[0], "bytes": kt[3], "achieved": kt[3] / (kt[0] * 1e-3) / 1e9},
+                "pcg_iteration": {"ms": pcg_ms, "bytes": kt[5],
+                                  "achieved": kt[5] / (pcg_ms * 1e-3) / 1e9,
+                                  "frac": kt[5] / (pcg_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
+                "frac_of_nominal_8TBs": achieved / 8000.0}
+    line = {"metric": METRIC, "value": ms * 1e-3, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.dtype, "data": "synthetic (reference RNG + recipes, SURVEY.md §8(d))",
+            "config": {"workload": WORKLOADS[args.config], "config_id": args.config,
+                       "n": problem.n, "m": problem.m, "nnz_P_upper": problem.p_upper.nnz,
+                       "nnz_A": problem.a.nnz, "settings": {"lambda_pcg": args.lambda_pcg},
+                       "parallelism": "single" if world == 1 else f"replicas{world}",
+                       "l2": "inputs larger than L2 (A and A^T streams ~%.1f GB per PCG iteration)"
+                             % (kt[5] / 1e9),
+                       "mode": args.mode},
+            "solve": {"status": int(last.status), "iterations": int(last.iterations),
+                      "pcg_iterations_total": int(last.pcg_iterations_total),
+                      "objective": last.objective, "r_prim_inf": last.r_prim_inf,
+                      "r_dual_inf": last.r_dual_inf, "equil_passes": int(last.equil_passes),
+                      "setup_s": last.setup_seconds, "loop_s": loop_s,
+                      "live_pcg_gbs": (kt[5] * last.pcg_iterations_total) / loop_s / 1e9
+                      if loop_s > 0 else None},
+            "gpu_launches": int(sum(i.kernel_launches for i in infos)),
+            "clocks": clk, "roofline": roofline,
+            "e2e": {"value": ms_e2e * 1e-3, "unit": "s",
+                    "h2d_bytes_per_step": int(einfos[-1].h2d_bytes),
+                    "d2h_bytes_per_step": int(einfos[-1].d2h_bytes)},
+            "generation_s": gen_s}
+    if not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(problem, {
+                "iterations": int(last.iterations),
+                "pcg_iterations_total": int(last.pcg_iterations_total),
+                "equil_passes": int(last.equil_passes)})
+        except Exception as e:  # reported, never silently replaced
+            line["cpu_baseline"] = {"value": None, "error": repr(e)}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -124,6 +124,8 @@ typedef struct {
   double d2h_seconds;            /* result download inside solve */
   uint64_t h2d_bytes;
   uint64_t d2h_bytes;
+  uint64_t kernel_launches;      /* launches of the engine's own kernels (setup
+                                    counted on the first solve of a workspace) */
 } qpcg_info;
 
 /* ---- per-ADMM-iteration diagnostics (SolveDiagnostics, solver.hpp:148-167) */
@@ -159,7 +161,9 @@ typedef struct {
   int32_t record_diagnostics; /* 1: keep per-PCG-call records */
   int32_t virtual_shards;  /* >1: hold A as G row blocks on one device and sum
                               the A^T partials in shard order */
-  int32_t reserved_[3];
+  int32_t reserved_;
+  void* stream;            /* cudaStream_t to run on (NULL: the workspace
+                              creates its own non-blocking stream) */
 } qpcg_options;
 
 typedef struct qpcg_workspace qpcg_workspace;

@@ -575,14 +575,13 @@ uint32_t qref_pcg_cap_f32(uint32_t n) { return qpcg::detail::pcg_iteration_cap<f
 
 // ---- bounded CPU-baseline sample --------------------------------------------
 // Times the reference's own setup phases and hot-path operators on a problem:
-// out[0] symmetrize_upper + transpose_csr (solver.hpp:397-398) seconds,
-// out[1] one Ruiz pass (ruiz_equilibrate with max_passes = 1, scaling.hpp:92),
-// out[2] ReducedKktOperator construction (linsys.hpp:39-61),
-// out[3] one K-apply (linsys.hpp:80-90, mean of `reps`),
-// out[4] one A^T spmv (admm_step rhs, solver.hpp:352),
-// out[5] one A spmv (z~ = A x~, solver.hpp:360),
-// out[6] compute_residuals (solver.hpp:191-208),
-// out[7] total seconds spent in this call.
+// out[0] symmetrize_upper (solver.hpp:397), out[1] transpose_csr (:398),
+// out[2] ruiz_equilibrate with max_passes = 1 (scaling.hpp:92-187; includes its
+// copies and two transposes), out[3] ReducedKktOperator construction
+// (linsys.hpp:39-61), out[4] one K-apply (linsys.hpp:80-90), out[5] one A^T
+// spmv (admm_step rhs, solver.hpp:352), out[6] one A spmv (z~ = A x~,
+// solver.hpp:360), out[7] compute_residuals (solver.hpp:191-208), out[8] total
+// seconds spent in this call.  Operator timings are means over `reps`.
 int qref_time_components_f64(const qpcg_csr_f64* p, const double* q,
                              const qpcg_csr_f64* a, const double* l,
                              const double* u, uint32_t reps, double* out) {
@@ -593,29 +592,31 @@ int qref_time_components_f64(const qpcg_csr_f64* p, const double* q,
     const size_t n = pu.rows, m = A.rows;
     double t = now_s();
     const auto pf = qpcg::symmetrize_upper(pu);
-    const auto at = qpcg::transpose_csr(A);
     out[0] = now_s() - t;
+    t = now_s();
+    const auto at = qpcg::transpose_csr(A);
+    out[1] = now_s() - t;
     t = now_s();
     const auto sp = qpcg::ruiz_equilibrate(pf, vec(q, n), A, vec(l, m), vec(u, m),
                                            1e-3, 1);
-    out[1] = now_s() - t;
+    out[2] = now_s() - t;
     t = now_s();
     qpcg::ReducedKktOperator<double> op(sp.p_full, sp.a, sp.a_t, 1e-6, 0.1);
-    out[2] = now_s() - t;
+    out[3] = now_s() - t;
     std::vector<double> x(n, 1.0), o, zt(m, 1.0), yv(m, 0.5), ax;
     t = now_s();
     for (uint32_t r = 0; r < reps; ++r) op.apply(x, o);
-    out[3] = (now_s() - t) / reps;
-    t = now_s();
-    for (uint32_t r = 0; r < reps; ++r) qpcg::spmv(sp.a_t, zt, o);
     out[4] = (now_s() - t) / reps;
     t = now_s();
-    for (uint32_t r = 0; r < reps; ++r) qpcg::spmv(sp.a, x, ax);
+    for (uint32_t r = 0; r < reps; ++r) qpcg::spmv(sp.a_t, zt, o);
     out[5] = (now_s() - t) / reps;
     t = now_s();
-    for (uint32_t r = 0; r < reps; ++r) (void)qpcg::compute_residuals(sp, x, zt, yv);
+    for (uint32_t r = 0; r < reps; ++r) qpcg::spmv(sp.a, x, ax);
     out[6] = (now_s() - t) / reps;
-    out[7] = now_s() - t0;
+    t = now_s();
+    for (uint32_t r = 0; r < reps; ++r) (void)qpcg::compute_residuals(sp, x, zt, yv);
+    out[7] = (now_s() - t) / reps;
+    out[8] = now_s() - t0;
   });
 }
 

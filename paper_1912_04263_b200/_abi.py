@@ -56,7 +56,8 @@ class Info(C.Structure):
                 ("n", C.c_uint32), ("m", C.c_uint32), ("reserved_", C.c_uint32),
                 ("setup_seconds", C.c_double), ("solve_seconds", C.c_double),
                 ("h2d_seconds", C.c_double), ("d2h_seconds", C.c_double),
-                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("kernel_launches", C.c_uint64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved_"}
@@ -76,7 +77,7 @@ class RhoUpdate(C.Structure):
 class Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("input_memory", C.c_int32), ("mode", C.c_int32),
                 ("record_diagnostics", C.c_int32), ("virtual_shards", C.c_int32),
-                ("reserved_", C.c_int32 * 3)]
+                ("reserved_", C.c_int32), ("stream", C.c_void_p)]
 
 
 def default_settings() -> Settings:

@@ -41,7 +41,7 @@ struct Ctl {
   T objective;
   // reductions / diagnostics
   uint32_t red_counter, n_calls, n_checks, n_rho;
-  uint32_t inf_branch, rho_branch, diag_cap, pad_;
+  uint32_t inf_branch, rho_branch, diag_cap, n_inf, n_rho_branch, pad_;
 };
 
 // diagnostics records (device side, converted to qpcg_pcg_call on the host)
@@ -646,6 +646,7 @@ __global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Hand
     }
   }
   C->inf_branch = inf;
+  C->n_inf += inf;
   set_cond(H.inf, inf);
 }
 
@@ -707,6 +708,7 @@ __global__ void k_rho_flag(Dev<T> D, Handles H) {
   Ctl<T>* C = D.ctl;
   const uint32_t f = !C->error && !C->done && (C->iter % C->rho_interval) == 0;
   C->rho_branch = f;
+  C->n_rho_branch += f;
   set_cond(H.rho, f);
 }
 

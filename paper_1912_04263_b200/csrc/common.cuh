@@ -37,7 +37,14 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
   throw CudaError(msg);
 }
 #define CK(x) ::qpcg_b200::cuda_check((x), #x, __FILE__, __LINE__)
-#define CK_LAUNCH() ::qpcg_b200::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+// every launch of one of our kernels goes through CK_LAUNCH, which also counts it
+// (host-side launches; graph-executed kernels are counted from device counters)
+inline thread_local uint64_t g_launches = 0;
+#define CK_LAUNCH()                                                                   \
+  do {                                                                                \
+    ++::qpcg_b200::g_launches;                                                        \
+    ::qpcg_b200::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
+  } while (0)
 
 // ------------------------------------------------------------ constants
 constexpr int kNumSMs = 148;           // B200

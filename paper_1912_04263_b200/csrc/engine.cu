@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../../include/qpcg_b200.h"
+#include "../../include/qpcg_b200_ops.h"
 #include "admm.cuh"
 #include "setup.cuh"
 
@@ -108,6 +109,9 @@ class Workspace {
   uint64_t h2d_bytes = 0;
   std::string err;
   bool have_solved = false;
+  bool own_stream = true;
+  uint64_t setup_launches = 0;
+  bool have_counted_setup = false;
 
   ~Workspace() {
     if (exec) cudaGraphExecDestroy(exec);
@@ -116,7 +120,7 @@ class Workspace {
     for (SpmvPlan<T>* p : {&D.pP, &D.pA, &D.pAT}) plan_free(*p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (s) cudaStreamDestroy(s);
+    if (s && own_stream) cudaStreamDestroy(s);
   }
 
   template <typename U>
@@ -161,13 +165,19 @@ class Workspace {
   void setup(const HostCsr<T>& Pu, const T* q, const HostCsr<T>& A, const T* l, const T* u,
              const qpcg_settings& st, const qpcg_options& op) {
     const double w0 = now_s();
+    const uint64_t l0 = g_launches;
     set = st;
     opt = op;
     validate_settings(st);
     device = op.device;
     if (device < 0) CK(cudaGetDevice(&device));
     CK(cudaSetDevice(device));
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    if (op.stream != nullptr) {
+      s = static_cast<cudaStream_t>(op.stream);
+      own_stream = false;
+    } else {
+      CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    }
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
     const uint32_t n = Pu.rows, m = A.rows;
@@ -342,6 +352,7 @@ class Workspace {
     CK(cudaEventElapsedTime(&ms, ev0, ev1));
     setup_seconds = ms * 1e-3;
     setup_wall = now_s() - w0;
+    setup_launches = g_launches - l0;
   }
 
   uint32_t equil_passes = 0;
@@ -627,13 +638,21 @@ class Workspace {
     hc.n_calls = hc.n_checks = hc.n_rho = 0;
     hc.pcg_active = 0;
     hc.red_counter = 0;
+    hc.n_inf = 0;
+    hc.n_rho_branch = 0;
     push_ctl();
+    uint64_t graph_build = 0;
+    const uint64_t l0 = g_launches;
     // initial residuals and PCG tolerance (solver.hpp:436-441)
     enq_residuals_fresh(1);
     if (opt.mode == QPCG_MODE_EAGER) {
       run_eager();
     } else {
-      if (!exec) build_graph();
+      if (!exec) {
+        const uint64_t b0 = g_launches;
+        build_graph();
+        graph_build = g_launches - b0;
+      }
       CK(cudaGraphLaunch(exec, s));
     }
     pull_ctl();
@@ -659,6 +678,10 @@ class Workspace {
     download(z, D.zo, sizeof(T) * D.m);
     download(y, D.yo, sizeof(T) * D.m);
     const bool has_cert = hc.status == 1 || hc.status == 2;
+    uint64_t launches = g_launches - l0 - graph_build;
+    if (opt.mode != QPCG_MODE_EAGER)  // kernels executed inside the graph
+      launches += 7ull * hc.iter + 5ull * hc.pcg_total + 2ull * hc.n_checks + 4ull * hc.n_inf +
+                  2ull * hc.n_rho_branch;
     if (has_cert) download(cert, D.cert, sizeof(T) * (hc.status == 1 ? D.m : D.n));
     CK(cudaStreamSynchronize(s));
     const double d2h = now_s() - td;
@@ -688,7 +711,9 @@ class Workspace {
                                   (has_cert ? sizeof(T) * (hc.status == 1 ? D.m : D.n) : 0)
                             : 0;
       info->runtime_seconds = now_s() - w0;
+      info->kernel_launches = launches + (have_counted_setup ? 0 : setup_launches);
     }
+    have_counted_setup = true;
   }
 
   // ------------------------------------------------- OSQP-style updates
@@ -735,6 +760,107 @@ class Workspace {
     k_precond<T><<<grid_for(D.n), kThreads, 0, s>>>(D, 1);
     CK_LAUNCH();
     CK(cudaStreamSynchronize(s));
+  }
+
+  // ----------------------------------------------------- debug / bench
+  void debug_scaled(T* pv, uint32_t* prp, uint32_t* pci, T* q, T* av, T* atv, uint32_t* atrp,
+                    uint32_t* atci, T* l, T* u, T* d, T* e, double* scal) {
+    CK(cudaSetDevice(device));
+    auto dl = [&](void* dst, const void* src, size_t b) {
+      if (dst) CK(cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToHost, s));
+    };
+    dl(pv, D.P.val, sizeof(T) * D.P.nnz);
+    dl(prp, D.P.rp, 4 * (size_t(D.n) + 1));
+    dl(pci, D.P.ci, 4 * size_t(D.P.nnz));
+    dl(q, D.q, sizeof(T) * D.n);
+    dl(av, D.A.val, sizeof(T) * D.A.nnz);
+    dl(atv, D.AT.val, sizeof(T) * D.AT.nnz);
+    dl(atrp, D.AT.rp, 4 * (size_t(D.n) + 1));
+    dl(atci, D.AT.ci, 4 * size_t(D.AT.nnz));
+    dl(l, D.l, sizeof(T) * D.m);
+    dl(u, D.u, sizeof(T) * D.m);
+    dl(d, D.d, sizeof(T) * D.n);
+    dl(e, D.e, sizeof(T) * D.m);
+    CK(cudaStreamSynchronize(s));
+    if (scal) {
+      scal[0] = double(hc.c);
+      scal[1] = double(hc.c_inv);
+      scal[2] = double(equil_passes);
+      scal[3] = double(equil_residual);
+    }
+  }
+
+  void debug_operator(const T* x, T* kx, T* dinv) {
+    CK(cudaSetDevice(device));
+    pull_ctl();
+    const Ctl<T> saved = hc;
+    hc.pcg_active = 1;
+    hc.error = 0;
+    push_ctl();
+    CK(cudaMemcpyAsync(D.p, x, sizeof(T) * D.n, cudaMemcpyHostToDevice, s));
+    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
+    launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
+    if (kx) CK(cudaMemcpyAsync(kx, D.kp, sizeof(T) * D.n, cudaMemcpyDeviceToHost, s));
+    if (dinv) CK(cudaMemcpyAsync(dinv, D.dinv, sizeof(T) * D.n, cudaMemcpyDeviceToHost, s));
+    hc = saved;
+    push_ctl();
+    CK(cudaStreamSynchronize(s));
+  }
+
+  // CUDA-event timing of the PCG-iteration kernels (bench.py roofline)
+  void bench_kernels(uint32_t reps, double* out) {
+    CK(cudaSetDevice(device));
+    pull_ctl();
+    const Ctl<T> saved = hc;
+    Ctl<T> run = hc;
+    run.pcg_active = 1;
+    run.error = 0;
+    run.done = 0;
+    run.rm = T(1);
+    run.thr = T(0);
+    run.best_norm = (T)INFINITY;
+    run.pcg_cap = 0xffffffffu;
+    run.k = 0;
+    fill(D.p, D.n, T(1));
+    fill(D.r, D.n, T(1));
+    std::vector<cudaEvent_t> ev(2 * reps);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    double acc[3] = {0, 0, 0};
+    for (int which = 0; which < 3; ++which) {
+      for (uint32_t i = 0; i < reps; ++i) {
+        hc = run;
+        push_ctl();
+        CK(cudaEventRecord(ev[2 * i], s));
+        if (which == 0)
+          launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
+        else if (which == 1)
+          launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
+        else
+          enq_pcg_iter(Handles{});
+        CK(cudaEventRecord(ev[2 * i + 1], s));
+      }
+      CK(cudaStreamSynchronize(s));
+      double tot = 0;
+      for (uint32_t i = 0; i < reps; ++i) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
+        tot += ms;
+      }
+      acc[which] = tot / reps;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    hc = saved;
+    push_ctl();
+    CK(cudaStreamSynchronize(s));
+    const double S = sizeof(T);
+    auto mb = [&](const DevCsr<T>& M) { return double(M.nnz) * (S + 4) + (double(M.rows) + 1) * 4; };
+    const double n = D.n, m = D.m;
+    out[0] = acc[0];
+    out[1] = acc[1];
+    out[2] = acc[2];
+    out[3] = mb(D.A) + S * n + S * m;                    // read A, p; write t
+    out[4] = mb(D.AT) + mb(D.P) + S * m + 2 * S * n;     // read A^T, P, t, p; write Kp
+    out[5] = mb(D.A) + mb(D.AT) + mb(D.P) + S * (2 * m + 11 * n);
   }
 
   // Not in the reference: rescale with the existing D, E, c.
@@ -1035,6 +1161,97 @@ uint32_t qpcg_get_check_iterations(const qpcg_workspace* ws, uint32_t* out, uint
   if (!w) return 0;
   return w->w64 ? checks_of(w->w64.get(), out, cap)
                 : w->w32 ? checks_of(w->w32.get(), out, cap) : 0;
+}
+
+int qpcg_debug_dims(const qpcg_workspace* ws, uint64_t* dims) {
+  if (!ws) return QPCG_ERR_INVALID;
+  auto fill = [&](auto* w) {
+    dims[0] = w->D.n;
+    dims[1] = w->D.m;
+    dims[2] = w->D.P.nnz;
+    dims[3] = w->D.A.nnz;
+    dims[4] = w->equil_passes;
+    dims[5] = 0;
+  };
+  if (ws->w64) fill(ws->w64.get());
+  else if (ws->w32) fill(ws->w32.get());
+  else return QPCG_ERR_INVALID;
+  return QPCG_OK;
+}
+
+int qpcg_debug_scaled(const qpcg_workspace* ws, void* pv, uint32_t* prp, uint32_t* pci, void* q,
+                      void* av, void* atv, uint32_t* atrp, uint32_t* atci, void* l, void* u,
+                      void* d, void* e, double* scal) {
+  auto* w = const_cast<qpcg_workspace*>(ws);
+  return guarded(w, [&] {
+    if (w->w64)
+      w->w64->debug_scaled((double*)pv, prp, pci, (double*)q, (double*)av, (double*)atv, atrp,
+                           atci, (double*)l, (double*)u, (double*)d, (double*)e, scal);
+    else
+      get<float>(w)->debug_scaled((float*)pv, prp, pci, (float*)q, (float*)av, (float*)atv, atrp,
+                                  atci, (float*)l, (float*)u, (float*)d, (float*)e, scal);
+  });
+}
+
+int qpcg_debug_operator(qpcg_workspace* ws, const void* x, void* kx, void* dinv) {
+  return guarded(ws, [&] {
+    if (ws && ws->w64)
+      ws->w64->debug_operator((const double*)x, (double*)kx, (double*)dinv);
+    else
+      get<float>(ws)->debug_operator((const float*)x, (float*)kx, (float*)dinv);
+  });
+}
+
+int qpcg_bench_kernels(qpcg_workspace* ws, uint32_t reps, double* out) {
+  return guarded(ws, [&] {
+    if (ws && ws->w64)
+      ws->w64->bench_kernels(reps, out);
+    else
+      get<float>(ws)->bench_kernels(reps, out);
+  });
+}
+
+}  // extern "C"
+
+template <typename T, typename CsrT>
+static int op_spmv_impl(const CsrT* mv, const T* x, T* y, int device) {
+  return guarded(nullptr, [&] {
+    if (device >= 0) CK(cudaSetDevice(device));
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CubTemp tmp;
+    DevCsr<T> M{mv->rows, mv->cols, mv->nnz, nullptr, nullptr, nullptr};
+    T *dx, *dy;
+    CK(cudaMalloc(&M.val, sizeof(T) * (M.nnz + 1)));
+    CK(cudaMalloc(&M.ci, 4 * (size_t(M.nnz) + 1)));
+    CK(cudaMalloc(&M.rp, 4 * (size_t(M.rows) + 1)));
+    CK(cudaMalloc(&dx, sizeof(T) * (M.cols + 1)));
+    CK(cudaMalloc(&dy, sizeof(T) * (M.rows + 1)));
+    CK(cudaMemcpyAsync(M.val, mv->values, sizeof(T) * M.nnz, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(M.ci, mv->col_indices, 4 * size_t(M.nnz), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(M.rp, mv->row_ptr, 4 * (size_t(M.rows) + 1), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dx, x, sizeof(T) * M.cols, cudaMemcpyHostToDevice, s));
+    SpmvPlan<T> P = plan_build<T>(M.rp, M.rows, tmp, s);
+    launch_spmv<T, 1, SumOp>(M, P, GatherVec<T>{dx}, EpiStore<T>{dy}, s);
+    CK(cudaMemcpyAsync(y, dy, sizeof(T) * M.rows, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    plan_free(P);
+    cudaFree(M.val);
+    cudaFree(M.ci);
+    cudaFree(M.rp);
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaStreamDestroy(s);
+  });
+}
+
+extern "C" {
+
+int qpcg_f64_op_spmv(const qpcg_csr_f64* m, const double* x, double* y, int device) {
+  return op_spmv_impl<double>(m, x, y, device);
+}
+int qpcg_f32_op_spmv(const qpcg_csr_f32* m, const float* x, float* y, int device) {
+  return op_spmv_impl<float>(m, x, y, device);
 }
 
 }  // extern "C"

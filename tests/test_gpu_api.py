@@ -1,0 +1,102 @@
+"""The OSQP-style workspace API and error behaviour through the C-ABI."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1912_04263_b200 import generators as G, solver
+from paper_1912_04263_b200.problem import NotPositiveDefiniteError, Settings, WarmStart
+from _util import dense_qp, kat_problems, kkt_ok, rel
+
+pytestmark = pytest.mark.gpu
+S = Settings(lambda_pcg=0.01)
+
+
+def test_warm_start_matches_oracle():
+    p = G.generate("huber", 4, 2)
+    o = O.oracle_solve(p, S)
+    w = WarmStart(o.x * 0.95, o.z, o.y * 1.05)
+    g = solver.solve(p, S, initial=w, device=0)
+    ow = O.oracle_solve(p, S, warm=w)
+    assert g.status == ow.status == "solved"
+    assert rel(g.objective, ow.objective) < 1e-3
+
+
+def test_warm_start_from_solution_converges_fast():
+    p = G.generate("lasso", 5, 0)
+    with solver.Workspace(p, S, device=0) as ws:
+        a = ws.solve()
+        ws.warm_start(a.x, a.z, a.y)
+        b = ws.solve()
+    assert b.status == "solved" and b.iterations <= a.iterations
+
+
+def test_repeated_solve_continues_from_state():
+    p = G.generate("svm", 4, 0)
+    with solver.Workspace(p, S, device=0) as ws:
+        a = ws.solve()
+        b = ws.solve()  # OSQP semantics: iterates and rho persist
+    assert b.status == "solved" and b.iterations <= a.iterations
+
+
+def test_update_rho_and_vectors():
+    p = G.generate("control", 4, 0)
+    with solver.Workspace(p, S, device=0) as ws:
+        a = ws.solve()
+        ws.update_rho(1.0)
+        b = ws.solve()
+        assert b.status == "solved" and kkt_ok(p, b, S)
+        # receding-horizon style update of the bounds
+        l2, u2 = p.l * 0.9, p.u * 0.9
+        ws.update_vectors(l=l2, u=u2)
+        c = ws.solve()
+    from paper_1912_04263_b200.problem import QpProblem
+    p2 = QpProblem(p.p_upper, p.q, p.a, l2, u2)
+    assert c.status == "solved" and kkt_ok(p2, c, S)
+    fresh = O.oracle_solve(p2, S)
+    assert rel(c.objective, fresh.objective) < 1e-2
+    with pytest.raises(ValueError, match="rho must be positive"):
+        with solver.Workspace(p, S, device=0) as ws:
+            ws.update_rho(-1.0)
+
+
+def test_invalid_problems_raise_reference_messages():
+    k = kat_problems()
+    cases = []
+    p = k["two_var"]; p.l = np.array([5.0]); p.u = np.array([1.0]); cases.append(p)
+    p = kat_problems()["two_var"]; p.q = np.array([0.0, np.inf]); cases.append(p)
+    p = kat_problems()["two_var"]; p.a.col_indices = p.a.col_indices[::-1].copy(); cases.append(p)
+    p = dense_qp([[1.0, 0.0], [1.0, 1.0]], [0, 0], [[1.0, 1.0]], [0], [1])
+    p.p_upper.col_indices[:] = [0, 0, 1]; p.p_upper.row_ptr[:] = [0, 1, 3]; cases.append(p)
+    for p in cases:
+        with pytest.raises(ValueError) as eo:
+            O.oracle_solve(p, Settings())
+        with pytest.raises(ValueError) as eg:
+            solver.solve(p, Settings(), device=0)
+        assert str(eg.value) == str(eo.value)
+    with pytest.raises(ValueError, match="alpha"):
+        solver.solve(k["two_var"], Settings(alpha=2.5), device=0)
+
+
+def test_not_positive_definite():
+    p = dense_qp([[-5.0, 0.0], [0.0, -5.0]], [1.0, 1.0], [[1.0, 0.0]], [-1.0], [1.0])
+    with pytest.raises(NotPositiveDefiniteError):
+        O.oracle_solve(p, Settings())
+    with pytest.raises(NotPositiveDefiniteError):
+        solver.solve(p, Settings(), device=0)
+
+
+def test_max_iter_status():
+    p = G.generate("portfolio", 4, 0)
+    s = Settings(lambda_pcg=0.01, max_admm_iter=7)
+    g = solver.solve(p, s, device=0)
+    o = O.oracle_solve(p, s)
+    assert g.status == o.status == "max_iter_reached" and g.iterations == o.iterations == 7
+
+
+def test_reentrant_workspaces():
+    p1, p2 = G.generate("lasso", 4, 0), G.generate("svm", 4, 1)
+    w1, w2 = solver.Workspace(p1, S, device=0), solver.Workspace(p2, S, device=0)
+    a, b = w1.solve(), w2.solve()
+    a2 = solver.solve(p1, S, device=0)
+    assert np.array_equal(a.x, a2.x) and b.status == "solved"
+    w1.close(); w2.close()

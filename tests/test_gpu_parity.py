@@ -1,0 +1,118 @@
+"""End-to-end parity of the B200 engine with the oracle (SURVEY.md §8(c)
+protocol): same status; both solutions pass an independent KKT check on the
+ORIGINAL data; objective and x within 1e-3 relative OR within 2x the oracle's
+own reorder noise (oracle on the row-reversed twin); iteration counts reported."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1912_04263_b200 import generators as G, solver
+from paper_1912_04263_b200.problem import Settings, SolveDiagnostics
+from _util import kat_problems, kkt_ok, rel, reversed_twin, xrel
+
+pytestmark = pytest.mark.gpu
+S = Settings(lambda_pcg=0.01)
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_outputs.json")))
+
+
+def check_parity(p, s, g, o, tol=1e-3):
+    assert g.status == o.status, (g.status, o.status)
+    if o.status == "solved":
+        slack = 1.0 if p.dtype == np.float64 else 2.0
+        assert kkt_ok(p, g, s, slack), "engine solution fails the KKT re-check on original data"
+        assert kkt_ok(p, o, s, slack)
+        ro, rx = rel(g.objective, o.objective), xrel(g.x, o.x)
+        if ro > tol or rx > tol:
+            tw = O.oracle_solve(reversed_twin(p), s)  # oracle's own reorder noise
+            assert tw.status == o.status
+            no, nx = rel(tw.objective, o.objective), xrel(tw.x, o.x)
+            assert ro <= max(tol, 2 * no) and rx <= max(tol, 2 * nx), (ro, no, rx, nx)
+    elif o.status in ("primal_infeasible", "dual_infeasible"):
+        assert g.objective == o.objective
+        assert np.allclose(g.certificate, o.certificate, atol=1e-6)
+
+
+@pytest.mark.parametrize("cls", G.CLASSES)
+@pytest.mark.parametrize("scale", [1, 3, 5, 7])
+def test_classes_f64(cls, scale):
+    for seed in (0, 1):
+        p = G.generate(cls, scale, seed)
+        g = solver.solve(p, S, device=0)
+        o = O.oracle_solve(p, S)
+        check_parity(p, S, g, o)
+        assert abs(g.iterations - o.iterations) <= 50  # reported band; parity gate is above
+
+
+@pytest.mark.parametrize("cls", G.CLASSES)
+def test_classes_f32(cls):
+    p = G.generate(cls, 4, 0).astype(np.float32)
+    s = Settings(lambda_pcg=0.01, eps_abs=3e-3, eps_rel=3e-3)  # SPEC acceptance 10
+    g = solver.solve(p, s, device=0)
+    o = O.oracle_solve(p, s)
+    assert g.status == o.status
+    if o.status == "solved":
+        assert rel(g.objective, o.objective) < 3e-2
+
+
+@pytest.mark.parametrize("cls", ["lasso", "svm", "random", "control"])
+def test_default_settings_status_match(cls):
+    p = G.generate(cls, 4, 0)
+    s = Settings(max_admm_iter=2000)
+    g = solver.solve(p, s, device=0)
+    o = O.oracle_solve(p, s)
+    assert g.status == o.status
+
+
+@pytest.mark.parametrize("name", list(kat_problems()))
+def test_kat_solves(name):
+    p = kat_problems()[name]
+    g = solver.solve(p, Settings(), device=0)
+    gg = GOLD["solves"][name]
+    assert g.status == gg["status"]
+    assert g.iterations == gg["iterations"]
+    assert np.allclose(g.x, gg["x"], rtol=1e-6, atol=1e-9)
+    if gg["certificate"]:
+        assert np.allclose(g.certificate, gg["certificate"], atol=1e-12)
+        assert g.objective == gg["objective"]
+
+
+@pytest.mark.parametrize("cfg", ["1", "1p"])
+def test_config1(cfg):
+    p = G.config(cfg)
+    g = solver.solve(p, S, device=0)
+    o = O.oracle_solve(p, S)
+    check_parity(p, S, g, o)
+
+
+def test_graph_and_eager_are_bitwise_identical():
+    p = G.generate("huber", 5, 1)
+    a = solver.solve(p, S, device=0, mode="graph")
+    b = solver.solve(p, S, device=0, mode="eager")
+    assert a.iterations == b.iterations and a.pcg_iterations_total == b.pcg_iterations_total
+    assert np.array_equal(a.x, b.x) and np.array_equal(a.y, b.y) and a.objective == b.objective
+
+
+def test_run_to_run_determinism():
+    p = G.generate("portfolio", 5, 0)
+    a = solver.solve(p, S, device=0)
+    b = solver.solve(p, S, device=0)
+    assert np.array_equal(a.x, b.x) and a.iterations == b.iterations
+
+
+def test_cadence_matches_reference():
+    """SPEC acceptance 7: checks every 5, rho every 10, eps from the last residuals."""
+    p = G.generate("lasso", 4, 0)
+    dg, do = SolveDiagnostics(), SolveDiagnostics()
+    g = solver.solve(p, S, diag=dg, device=0)
+    o = O.oracle_solve(p, S, diag=do)
+    assert dg.check_iterations == list(range(5, g.iterations + 1, 5))
+    assert [r["admm_iter"] for r in dg.rho_updates] == \
+        [i for i in range(10, g.iterations + 1, 10) if i < g.iterations or g.status != "solved"]
+    for c in dg.pcg_calls:
+        want = max(0.01 * np.sqrt(c["r_prim_scaled_inf"] * c["r_dual_scaled_inf"]), 1e-7)
+        assert c["eps"] == pytest.approx(want, rel=1e-15, abs=0)
+    k = min(len(dg.pcg_calls), len(do.pcg_calls), 10)
+    assert [c["iterations"] for c in dg.pcg_calls[:k]] == [c["iterations"] for c in do.pcg_calls[:k]]
