@@ -7,7 +7,7 @@ i.e. the reference's `qpcg::solve` timed region (solver.hpp:392 -> :537:
 symmetrize, transpose, Ruiz, ADMM/PCG loop, unscale, objective) — of the
 workload `config` names (default: BASELINE configs[1], lasso with 10^4
 features x 10^5 samples at 15 % density, generated with the reference's own
-RNG and recipes; fp64; settings {"lambda_pcg": 0.01}).
+RNG and recipes; fp64; settings {"lambda_pcg": 1e-3} (0.01, the survey's choice, diverges at this size — DESIGN.md §2).
 
 * value       seconds per solve with the problem already resident in HBM
               (device-pointer inputs), CUDA events on the engine's stream.
@@ -56,6 +56,10 @@ WORKLOADS = {
 COUNTS_FILE = os.path.join(ROOT, "profiles", "solve_counts.json")
 
 
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -64,7 +68,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="2", choices=sorted(WORKLOADS))
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--lambda-pcg", type=float, default=0.01)
+    ap.add_argument("--lambda-pcg", type=float, default=1e-3)
     ap.add_argument("--e2e-steps", type=int, default=0, help="0: same as --steps")
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -356,12 +360,16 @@ def main():
     tg = time.time()
     problem = generators.config(args.config, seed=rank)
     gen_s = time.time() - tg
+    log(f"generated config {args.config}: n={problem.n} m={problem.m} nnz(A)={problem.a.nnz} in {gen_s:.1f}s")
     settings = Settings(lambda_pcg=args.lambda_pcg)
     stream = torch.cuda.Stream(device=local)
     with torch.cuda.stream(stream):
         eng = Engine(problem, settings, local, stream.cuda_stream, dtype, args.mode)
-        for _ in range(args.warmup):
+        for i in range(args.warmup):
+            t = time.time()
             info = eng.solve("device")
+            log(f"warmup {i}: status={info.status} iters={info.iterations} pcg={info.pcg_iterations_total} "
+                f"setup={info.setup_seconds:.3f}s loop={info.solve_seconds:.3f}s wall={time.time() - t:.2f}s")
         def barrier():
             if dist is not None:
                 dist.barrier()
@@ -392,7 +400,9 @@ def main():
         barrier()
         ms_e2e = f0.elapsed_time(f1) / ke
         # ---- dominant kernel, CUDA events on the engine stream
+        log(f"timed: {ms:.2f} ms/solve, e2e {ms_e2e:.2f} ms/solve")
         kt = eng.kernel_timing(args.kernel_reps)
+        log(f"kernels: A {kt[0]:.4f} ms, A^T {kt[1]:.4f} ms, PCG iteration {kt[2]:.4f} ms")
     if dist is not None:
         t = torch.tensor([ms, ms_e2e], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

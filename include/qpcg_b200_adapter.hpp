@@ -1,0 +1,182 @@
+// qpcg_b200_adapter.hpp — drop-in C++ front end for the reference's API.
+//
+// Include AFTER the reference's own headers (it uses qpcg::QpProblem,
+// qpcg::Settings, qpcg::WarmStart, qpcg::SolveDiagnostics, qpcg::SolveOutcome
+// from solver.hpp) and link libqpcg_b200.so.  It provides
+//
+//   template <typename T>
+//   qpcg::SolveOutcome<T> qpcg::b200::solve(const QpProblem<T>&, const Settings<T>&,
+//                                           const WarmStart<T>* = nullptr,
+//                                           SolveDiagnostics<T>* = nullptr);
+//
+// with the exact signature and semantics of qpcg::solve (solver.hpp:386-389)
+// and the same exception classes (std::invalid_argument,
+// qpcg::NotPositiveDefiniteError, std::runtime_error), so the reference's
+// bench runner swaps with one line at runner.hpp:84:
+//
+//   const SolveOutcome<T> out = qpcg::b200::solve(p, settings);
+//
+// SolveDiagnostics::on_iteration (a per-iteration host callback on scaled
+// iterates) is not supported by the device-resident loop; pcg_calls,
+// check_iterations and rho_updates are filled.
+#ifndef QPCG_B200_ADAPTER_HPP
+#define QPCG_B200_ADAPTER_HPP
+
+#include <chrono>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "qpcg_b200.h"
+
+namespace qpcg::b200 {
+
+namespace adapter_detail {
+
+inline qpcg_csr_f64 view(const qpcg::CsrMatrix<double>& m) {
+  return qpcg_csr_f64{m.rows, m.cols, m.nnz(), m.values.data(), m.row_ptr.data(),
+                      m.col_indices.data()};
+}
+inline qpcg_csr_f32 view(const qpcg::CsrMatrix<float>& m) {
+  return qpcg_csr_f32{m.rows, m.cols, m.nnz(), m.values.data(), m.row_ptr.data(),
+                      m.col_indices.data()};
+}
+
+template <typename T>
+qpcg_settings settings(const qpcg::Settings<T>& s) {
+  qpcg_settings c;
+  qpcg_default_settings(&c);
+  c.alpha = double(s.alpha);
+  c.sigma = double(s.sigma);
+  c.rho_bar_init = double(s.rho_bar_init);
+  c.eps_abs = double(s.eps_abs);
+  c.eps_rel = double(s.eps_rel);
+  c.eps_pinf = double(s.eps_pinf);
+  c.eps_dinf = double(s.eps_dinf);
+  c.max_admm_iter = s.max_admm_iter;
+  c.check_interval = s.check_interval;
+  c.rho_update_interval = s.rho_update_interval;
+  c.scaling_enabled = s.scaling_enabled ? 1u : 0u;
+  c.lambda_pcg = double(s.lambda_pcg);
+  c.eps_pcg_min = double(s.eps_pcg_min);
+  c.eps_equil = double(s.eps_equil);
+  c.equil_max_passes = s.equil_max_passes;
+  return c;
+}
+
+[[noreturn]] inline void rethrow(int rc, const std::string& msg) {
+  if (rc == QPCG_ERR_INVALID) throw std::invalid_argument(msg);
+  if (rc == QPCG_ERR_NOT_PD) throw qpcg::NotPositiveDefiniteError(msg);
+  throw std::runtime_error(msg);
+}
+
+template <typename T>
+struct Api;
+template <>
+struct Api<double> {
+  static int setup(qpcg_workspace** w, const qpcg_csr_f64* p, const double* q,
+                   const qpcg_csr_f64* a, const double* l, const double* u,
+                   const qpcg_settings* s, const qpcg_options* o) {
+    return qpcg_f64_setup(w, p, q, a, l, u, s, o);
+  }
+  static int warm(qpcg_workspace* w, const double* x, const double* z, const double* y) {
+    return qpcg_f64_warm_start(w, x, z, y);
+  }
+  static int solve(qpcg_workspace* w, qpcg_info* i, double* x, double* z, double* y,
+                   double* c) {
+    return qpcg_f64_solve(w, i, x, z, y, c);
+  }
+};
+template <>
+struct Api<float> {
+  static int setup(qpcg_workspace** w, const qpcg_csr_f32* p, const float* q,
+                   const qpcg_csr_f32* a, const float* l, const float* u,
+                   const qpcg_settings* s, const qpcg_options* o) {
+    return qpcg_f32_setup(w, p, q, a, l, u, s, o);
+  }
+  static int warm(qpcg_workspace* w, const float* x, const float* z, const float* y) {
+    return qpcg_f32_warm_start(w, x, z, y);
+  }
+  static int solve(qpcg_workspace* w, qpcg_info* i, float* x, float* z, float* y, float* c) {
+    return qpcg_f32_solve(w, i, x, z, y, c);
+  }
+};
+
+struct WsGuard {
+  qpcg_workspace* w = nullptr;
+  ~WsGuard() { qpcg_cleanup(w); }
+};
+
+}  // namespace adapter_detail
+
+// solver.hpp:386-541, on the B200
+template <typename T>
+qpcg::SolveOutcome<T> solve(const qpcg::QpProblem<T>& p, const qpcg::Settings<T>& s,
+                            std::type_identity_t<const qpcg::WarmStart<T>*> initial = nullptr,
+                            std::type_identity_t<qpcg::SolveDiagnostics<T>*> diag = nullptr) {
+  using namespace adapter_detail;
+  static_assert(std::is_same_v<T, double> || std::is_same_v<T, float>);
+  const auto pv = view(p.p_upper);
+  const auto av = view(p.a);
+  const qpcg_settings cs = settings(s);
+  qpcg_options opt;
+  qpcg_default_options(&opt);
+  opt.record_diagnostics = diag != nullptr ? 1 : 0;
+  if (p.q.size() != p.p_upper.rows) throw std::invalid_argument("problem: q length must equal n");
+  if (p.l.size() != p.a.rows || p.u.size() != p.a.rows)
+    throw std::invalid_argument("problem: bound lengths must equal m");
+  const auto t_start = std::chrono::steady_clock::now();  // solver.hpp:392
+  WsGuard g;
+  int rc = Api<T>::setup(&g.w, &pv, p.q.data(), &av, p.l.data(), p.u.data(), &cs, &opt);
+  if (rc != QPCG_OK) rethrow(rc, qpcg_last_error(nullptr));
+  const size_t n = p.p_upper.rows, m = p.a.rows;
+  if (initial != nullptr) {
+    if (initial->x.size() != n || initial->z.size() != m || initial->y.size() != m)
+      throw std::invalid_argument("solve: warm start dimension mismatch");
+    rc = Api<T>::warm(g.w, initial->x.data(), initial->z.data(), initial->y.data());
+    if (rc != QPCG_OK) rethrow(rc, qpcg_last_error(g.w));
+  }
+  qpcg::SolveOutcome<T> out;
+  out.x.resize(n);
+  out.z.resize(m);
+  out.y.resize(m);
+  std::vector<T> cert(n > m ? n : m);
+  qpcg_info info;
+  rc = Api<T>::solve(g.w, &info, out.x.data(), out.z.data(), out.y.data(), cert.data());
+  if (rc != QPCG_OK) rethrow(rc, qpcg_last_error(g.w));
+  out.status = static_cast<qpcg::SolveStatus>(info.status);
+  if (info.certificate_valid)
+    out.certificate.assign(cert.begin(),
+                           cert.begin() + (info.status == QPCG_STATUS_PRIMAL_INFEASIBLE ? m : n));
+  out.objective = T(info.objective);
+  out.iterations = info.iterations;
+  out.pcg_iterations_total = info.pcg_iterations_total;
+  out.r_prim_inf = T(info.r_prim_inf);
+  out.r_dual_inf = T(info.r_dual_inf);
+  out.runtime_seconds =  // solver.hpp:537-539: setup through objective
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  out.equil_passes = info.equil_passes;
+  out.equil_residual = T(info.equil_residual);
+  out.rho_final = T(info.rho_final);
+  out.rho_update_count = info.rho_update_count;
+  if (diag != nullptr) {
+    std::vector<qpcg_pcg_call> calls(qpcg_get_pcg_calls(g.w, nullptr, 0));
+    qpcg_get_pcg_calls(g.w, calls.data(), uint32_t(calls.size()));
+    for (const auto& c : calls)
+      diag->pcg_calls.push_back({c.admm_iter, T(c.eps), T(c.r_prim_scaled_inf),
+                                 T(c.r_dual_scaled_inf), c.iterations, c.converged != 0});
+    std::vector<uint32_t> checks(qpcg_get_check_iterations(g.w, nullptr, 0));
+    qpcg_get_check_iterations(g.w, checks.data(), uint32_t(checks.size()));
+    for (auto it : checks) diag->check_iterations.push_back(it);
+    std::vector<qpcg_rho_update> rho(qpcg_get_rho_updates(g.w, nullptr, 0));
+    qpcg_get_rho_updates(g.w, rho.data(), uint32_t(rho.size()));
+    for (const auto& r : rho)
+      diag->rho_updates.push_back({r.admm_iter, T(r.rho_before), T(r.rho_after)});
+  }
+  return out;
+}
+
+}  // namespace qpcg::b200
+
+#endif  // QPCG_B200_ADAPTER_HPP

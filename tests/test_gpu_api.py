@@ -65,8 +65,10 @@ def test_invalid_problems_raise_reference_messages():
     p = k["two_var"]; p.l = np.array([5.0]); p.u = np.array([1.0]); cases.append(p)
     p = kat_problems()["two_var"]; p.q = np.array([0.0, np.inf]); cases.append(p)
     p = kat_problems()["two_var"]; p.a.col_indices = p.a.col_indices[::-1].copy(); cases.append(p)
-    p = dense_qp([[1.0, 0.0], [1.0, 1.0]], [0, 0], [[1.0, 1.0]], [0], [1])
-    p.p_upper.col_indices[:] = [0, 0, 1]; p.p_upper.row_ptr[:] = [0, 1, 3]; cases.append(p)
+    from paper_1912_04263_b200.problem import CsrMatrix, QpProblem
+    below = CsrMatrix(2, 2, np.array([1.0, 1.0, 1.0]), np.array([0, 1, 3], np.uint32),
+                      np.array([0, 0, 1], np.uint32))  # (1,0) is below the diagonal
+    cases.append(QpProblem(below, np.zeros(2), CsrMatrix.from_dense([[1.0, 1.0]]), np.zeros(1), np.ones(1)))
     for p in cases:
         with pytest.raises(ValueError) as eo:
             O.oracle_solve(p, Settings())
