@@ -88,6 +88,9 @@ struct Dev {
   T *ax, *px, *aty, *rdual;
   // outputs (unscaled)
   T *xo, *zo, *yo, *cert, *pxo;
+  // interleaved gather operands of the two-column passes
+  pair_t<T>* g2m;  // [m] {rho z - y, rho z~}
+  pair_t<T>* g2n;  // [n] {x~, alpha x~ + (1 - alpha) x}
   // diagnostics
   DiagRec<T>* calls;
   uint32_t* checks;
@@ -205,17 +208,32 @@ __device__ __forceinline__ T prow_dot(const DevCsr<T>& P, uint32_t r, const T* x
 // rhs pass over A^T (admm_step, solver.hpp:351-355) fused with the PCG r0
 // operator apply (linsys.hpp:218-219, 80-90): col0 = rho z - y, col1 = rho z~
 // (A x~_prev == z~ from the previous step, reused bit-exactly).
+// The two gathered columns are packed by k_pack_rhs into one interleaved
+// array so each nnz costs a single 16-byte gather (one L2 sector) instead of
+// three scattered 8-byte ones.
 template <typename T>
 struct GatherRhs {
-  const T *z, *y, *zt;
-  const Ctl<T>* ctl;
-  T rho;
-  __device__ __forceinline__ void init() { rho = ctl->rho; }
+  const pair_t<T>* g2;
+  __device__ __forceinline__ void init() {}
   __device__ __forceinline__ void operator()(uint32_t c, T (&g)[2]) const {
-    g[0] = rho * __ldg(z + c) - __ldg(y + c);
-    g[1] = rho * __ldg(zt + c);
+    const pair_t<T> v = __ldg(g2 + c);
+    g[0] = v.x;
+    g[1] = v.y;
   }
 };
+// {rho z - y, rho z~} (solver.hpp:351; linsys.hpp:84-85 with A x~ = z~)
+template <typename T>
+__global__ void k_pack_rhs(Dev<T> D) {
+  const Ctl<T>* C = D.ctl;
+  if (C->error) return;
+  const T rho = C->rho;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.m; i += gridDim.x * blockDim.x) {
+    pair_t<T> v;
+    v.x = rho * D.z[i] - D.y[i];
+    v.y = rho * D.zt[i];
+    D.g2m[i] = v;
+  }
+}
 template <typename T>
 struct EpiRhs {
   Dev<T> D;
@@ -264,20 +282,13 @@ struct EpiKp {
 // col1 (check iterations only) = A x_new with x_new formed on the fly exactly
 // as solver.hpp:366-367 forms it, feeding compute_residuals' A x (:196).
 template <typename T>
-struct GatherAdmm {
-  const T *xt, *x;
-  const Ctl<T>* ctl;
-  T alpha, one_m_alpha;
-  bool two;
-  __device__ __forceinline__ void init() {
-    alpha = ctl->alpha;
-    one_m_alpha = T(1) - alpha;
-    two = ((ctl->iter + 1) % ctl->check_interval) == 0;
-  }
+struct GatherAdmm {  // {x~, x_new} packed by k_pcg_fin
+  const pair_t<T>* g2;
+  __device__ __forceinline__ void init() {}
   __device__ __forceinline__ void operator()(uint32_t c, T (&g)[2]) const {
-    const T a = __ldg(xt + c);
-    g[0] = a;
-    g[1] = two ? alpha * a + one_m_alpha * __ldg(x + c) : T(0);
+    const pair_t<T> v = __ldg(g2 + c);
+    g[0] = v.x;
+    g[1] = v.y;
   }
 };
 template <typename T>
@@ -511,14 +522,25 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(Dev<T> D) {
 }
 
 // PCG exit: x~ = 0 (b == 0) or best iterate (cap); PcgCall record.
+// also packs {x~, x_new} for the z~ pass; x_new = alpha x~ + (1 - alpha) x is
+// formed exactly as solver.hpp:366-367 (only needed on check iterations).
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_pcg_fin(Dev<T> D) {
   Ctl<T>* C = D.ctl;
   if (C->error) return;
   const uint32_t ex = C->pcg_exit;
-  if (ex != kPcgConverged) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
-      D.xt[i] = ex == kPcgZeroRhs ? T(0) : D.best[i];
+  const bool two = ((C->iter + 1) % C->check_interval) == 0;
+  const T alpha = C->alpha, oma = T(1) - alpha;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+    T xt = D.xt[i];
+    if (ex != kPcgConverged) {
+      xt = ex == kPcgZeroRhs ? T(0) : D.best[i];
+      D.xt[i] = xt;
+    }
+    pair_t<T> v;
+    v.x = xt;
+    v.y = two ? alpha * xt + oma * D.x[i] : T(0);
+    D.g2n[i] = v;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     C->pcg_total += C->k;
@@ -650,10 +672,15 @@ __global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Hand
   set_cond(H.inf, inf);
 }
 
-// Infeasibility tests' vector parts (support sum :248-262, q'v :281) and the
-// decision (solver.hpp:483-494).
+// Infeasibility tests (solver.hpp:236-297, 481-495).  Both tests are
+// conjunctions, so they are evaluated cheapest-first and each A-sized pass
+// over the ORIGINAL matrices runs only while its certificate is still
+// possible (the SpMV epilogues read need_pinf / need_dinf): same booleans as
+// the reference, far fewer matrix streams on ordinary (feasible) solves.
+// Stage 1: the vector parts — support sum and infinite-bound tests of the
+// primal certificate (:248-263), q'v of the dual one (:281).
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_infeas(Dev<T> D) {
+__global__ void __launch_bounds__(kThreads) k_infeas_vec(Dev<T> D) {
   Ctl<T>* C = D.ctl;
   if (C->error || !C->inf_branch) return;
   const uint32_t n = D.n, m = D.m;
@@ -688,11 +715,25 @@ __global__ void __launch_bounds__(kThreads) k_infeas(Dev<T> D) {
   if (threadIdx.x != 0) return;
   C->support = tot[0];
   C->qv = tot[2];
-  const T atv = bits_to_value(C->atv_inf_bits, T(0));
-  const T pv = bits_to_value(C->pv_inf_bits, T(0));
-  const bool primal = C->need_pinf && !(atv > eps_p) && tot[1] == T(0) && tot[0] < eps_p;
-  const bool dual = C->need_dinf && !(pv > C->eps_dinf) && (tot[2] < C->eps_dinf) &&
-                    C->dinf_bad == 0;
+  if (C->need_pinf && !(tot[1] == T(0) && tot[0] < eps_p)) C->need_pinf = 0;
+  if (C->need_dinf && !(tot[2] < C->eps_dinf)) C->need_dinf = 0;
+}
+
+// Stage 2 (after the P_orig pass): |P v| <= eps (:280)
+template <typename T>
+__global__ void k_infeas_mid(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (C->error || !C->inf_branch) return;
+  if (C->need_dinf && bits_to_value(C->pv_inf_bits, T(0)) > C->eps_dinf) C->need_dinf = 0;
+}
+
+// Stage 3: decision after the A_orig^T (primal) and A_orig (dual) passes
+template <typename T>
+__global__ void k_infeas(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (C->error || !C->inf_branch) return;
+  const bool primal = C->need_pinf && !(bits_to_value(C->atv_inf_bits, T(0)) > C->eps_pinf);
+  const bool dual = C->need_dinf && C->dinf_bad == 0;
   if (primal) {
     C->status = 1;
     C->done = 1;

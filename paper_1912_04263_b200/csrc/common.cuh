@@ -46,6 +46,29 @@ inline thread_local uint64_t g_launches = 0;
     ::qpcg_b200::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
   } while (0)
 
+// ------------------------------------------------------- device memory
+// All engine allocations are stream-ordered from the device's default memory
+// pool with an unbounded release threshold: a solve's ~9 GB (config 2) is
+// recycled from the pool by the next workspace instead of being unmapped and
+// re-mapped (cudaMalloc/cudaFree of multi-GB buffers costs ~100 ms per solve).
+inline thread_local cudaStream_t g_alloc_stream = nullptr;
+template <typename U>
+inline cudaError_t dmalloc(U** p, size_t bytes) {
+  return cudaMallocAsync(reinterpret_cast<void**>(p), bytes ? bytes : 1, g_alloc_stream);
+}
+inline cudaError_t dfree(void* p) { return p ? cudaFreeAsync(p, g_alloc_stream) : cudaSuccess; }
+inline void configure_pool(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+  uint64_t thr = ~0ull;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+}
+struct AllocScope {  // routes dmalloc/dfree of this thread to stream s
+  cudaStream_t prev;
+  explicit AllocScope(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+  ~AllocScope() { g_alloc_stream = prev; }
+};
+
 // ------------------------------------------------------------ constants
 constexpr int kNumSMs = 148;           // B200
 constexpr int kThreads = 256;          // default block size
@@ -149,9 +172,18 @@ __device__ __forceinline__ double t_div<double>(double a, double b) { return __d
 template <>
 __device__ __forceinline__ float t_div<float>(float a, float b) { return __fdiv_rn(a, b); }
 
+// interleaved pair type for two-column gathers (one 16/8-byte load per nnz)
 template <typename T>
-__host__ __device__ __forceinline__ T t_inf() {
-  return T(1.0) / T(0.0);
-}
+struct Pair;
+template <>
+struct Pair<double> {
+  using type = double2;
+};
+template <>
+struct Pair<float> {
+  using type = float2;
+};
+template <typename T>
+using pair_t = typename Pair<T>::type;
 
 }  // namespace qpcg_b200

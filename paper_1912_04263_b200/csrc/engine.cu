@@ -101,6 +101,8 @@ class Workspace {
   qpcg_options opt{};
   std::vector<void*> allocs;
   uint32_t* permA = nullptr;  // transpose permutation of A
+  uint32_t* p_rows = nullptr;  // rows of P_full with entries (ordered mean)
+  uint32_t n_prows = 0;
   T* ruiz_scal = nullptr;      // [mean, qinf, gamma, c, dev]
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -116,8 +118,15 @@ class Workspace {
   ~Workspace() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
-    for (void* p : allocs) cudaFree(p);
-    for (SpmvPlan<T>* p : {&D.pP, &D.pA, &D.pAT}) plan_free(*p);
+    {
+      AllocScope scope(s);
+      for (void* p : allocs) dfree(p);
+      for (SpmvPlan<T>* p : {&D.pP, &D.pA, &D.pAT}) plan_free(*p);
+      if (tmp.ptr) dfree(tmp.ptr);
+      tmp.ptr = nullptr;
+      tmp.bytes = 0;
+      if (s) cudaStreamSynchronize(s);
+    }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (s && own_stream) cudaStreamDestroy(s);
@@ -126,7 +135,7 @@ class Workspace {
   template <typename U>
   U* alloc(size_t count) {
     void* p = nullptr;
-    CK(cudaMalloc(&p, sizeof(U) * (count ? count : 1)));
+    CK(dmalloc(&p, sizeof(U) * (count ? count : 1)));
     allocs.push_back(p);
     return static_cast<U*>(p);
   }
@@ -178,6 +187,8 @@ class Workspace {
     } else {
       CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     }
+    configure_pool(device);
+    AllocScope scope(s);
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
     const uint32_t n = Pu.rows, m = A.rows;
@@ -313,6 +324,8 @@ class Workspace {
     D.z = vec(m); D.y = vec(m); D.zt = vec(m); D.dy = vec(m); D.t = vec(m); D.ax = vec(m);
     D.zo = vec(m); D.yo = vec(m);
     D.cert = vec(std::max(n, m));
+    D.g2m = alloc<pair_t<T>>(m);
+    D.g2n = alloc<pair_t<T>>(n);
     const uint32_t cap = op.record_diagnostics ? st.max_admm_iter : 0u;
     D.calls = alloc<DiagRec<T>>(cap);
     D.checks = alloc<uint32_t>(cap);
@@ -435,6 +448,17 @@ class Workspace {
     deviation = T(1);
     passes = 0;
     const T eps = T(st.eps_equil);
+    {  // rows of P_full with entries, for the ordered mean (structure is fixed)
+      uint32_t* flags = alloc<uint32_t>(n + 1);
+      uint32_t* pos = alloc<uint32_t>(n + 1);
+      p_rows = alloc<uint32_t>(n + 1);
+      nonempty_flags_kernel<<<grid_for(n), kThreads, 0, s>>>(D.P.rp, n, flags);
+      CK_LAUNCH();
+      exclusive_scan_u32(flags, pos, n, tmp, s);
+      n_prows = scan_total(flags, pos, n, s);
+      compact_kernel<<<grid_for(n), kThreads, 0, s>>>(flags, pos, n, p_rows);
+      CK_LAUNCH();
+    }
     T* mean = ruiz_scal + 0;
     T* qinf = ruiz_scal + 1;
     T* gamma = ruiz_scal + 2;
@@ -453,7 +477,7 @@ class Workspace {
       plan_visit(D.AT, D.pAT, ScaleRowColFn<T>{D.AT.val, D.AT.ci, dx, dz}, s);
       // cost scaling
       row_inf_norms(D.P, D.pP, pn, s);
-      ordered_mean_kernel<T><<<1, 32, 0, s>>>(pn, n, mean);
+      ordered_mean_kernel<T><<<1, 256, 0, s>>>(pn, p_rows, n_prows, n, mean);
       CK_LAUNCH();
       k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q, n, D.red, &D.ctl->red_counter, qinf);
       CK_LAUNCH();
@@ -468,8 +492,9 @@ class Workspace {
 
   // ------------------------------------------------------ enqueue helpers
   void enq_rhs(const Handles&) {
-    launch_spmv<T, 2, SumOp>(D.AT, D.pAT, GatherRhs<T>{D.z, D.y, D.zt, D.ctl, T(0)},
-                             EpiRhs<T>{D, T(0)}, s);
+    k_pack_rhs<T><<<grid_for(D.m), kThreads, 0, s>>>(D);
+    CK_LAUNCH();
+    launch_spmv<T, 2, SumOp>(D.AT, D.pAT, GatherRhs<T>{D.g2m}, EpiRhs<T>{D, T(0)}, s);
   }
   void enq_pcg_init(const Handles& H) {
     k_pcg_init<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D, H);
@@ -488,8 +513,8 @@ class Workspace {
   void enq_post_pcg(const Handles& H) {
     k_pcg_fin<T><<<grid_for(D.n), kThreads, 0, s>>>(D);
     CK_LAUNCH();
-    launch_spmv<T, 2, SumOp>(D.A, D.pA, GatherAdmm<T>{D.xt, D.x, D.ctl, T(0), T(0), false},
-                             EpiAdmm<T>{D, T(0), T(0), T(0), false}, s);
+    launch_spmv<T, 2, SumOp>(D.A, D.pA, GatherAdmm<T>{D.g2n}, EpiAdmm<T>{D, T(0), T(0), T(0), false},
+                             s);
     k_xupdate<T><<<grid_for(D.n), kThreads, 0, s>>>(D, H);
     CK_LAUNCH();
   }
@@ -499,15 +524,19 @@ class Workspace {
     CK_LAUNCH();
   }
   void enq_infeas(const Handles&) {
+    k_infeas_vec<T><<<red_grid<T>(std::max(D.n, D.m)), kThreads, 0, s>>>(D);
+    CK_LAUNCH();
     launch_spmv<T, 1, SumOp>(
         D.ATo, D.pATo, GatherCertY<T>{D.e, D.dy, D.ctl, T(0), T(0)},
         EpiNormMax<T>{&D.ctl->atv_inf_bits, &D.ctl->need_pinf}, s);
     launch_spmv<T, 1, SumOp>(D.Po, D.pPo, GatherCertX<T>{D.d, D.dx, D.ctl, T(0)},
                              EpiNormMax<T>{&D.ctl->pv_inf_bits, &D.ctl->need_dinf}, s);
+    k_infeas_mid<T><<<1, 1, 0, s>>>(D);
+    CK_LAUNCH();
     launch_spmv<T, 1, SumOp>(
         D.Ao, D.pAo, GatherCertX<T>{D.d, D.dx, D.ctl, T(0)},
         EpiDualRows<T>{D.l_o, D.u_o, &D.ctl->dinf_bad, &D.ctl->need_dinf, T(0), D.ctl}, s);
-    k_infeas<T><<<red_grid<T>(std::max(D.n, D.m)), kThreads, 0, s>>>(D);
+    k_infeas<T><<<1, 1, 0, s>>>(D);
     CK_LAUNCH();
   }
   void enq_rho_flag(const Handles& H) {
@@ -625,6 +654,7 @@ class Workspace {
   // ------------------------------------------------------------ solve
   void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) {
     CK(cudaSetDevice(device));
+    AllocScope scope(s);
     const double w0 = now_s();
     CK(cudaEventRecord(ev0, s));
     // reset the per-solve state (solver.hpp:412, :430-443)
@@ -680,7 +710,7 @@ class Workspace {
     const bool has_cert = hc.status == 1 || hc.status == 2;
     uint64_t launches = g_launches - l0 - graph_build;
     if (opt.mode != QPCG_MODE_EAGER)  // kernels executed inside the graph
-      launches += 7ull * hc.iter + 5ull * hc.pcg_total + 2ull * hc.n_checks + 4ull * hc.n_inf +
+      launches += 8ull * hc.iter + 5ull * hc.pcg_total + 2ull * hc.n_checks + 6ull * hc.n_inf +
                   2ull * hc.n_rho_branch;
     if (has_cert) download(cert, D.cert, sizeof(T) * (hc.status == 1 ? D.m : D.n));
     CK(cudaStreamSynchronize(s));
@@ -719,6 +749,7 @@ class Workspace {
   // ------------------------------------------------- OSQP-style updates
   void warm_start(const T* x, const T* z, const T* y) {  // solver.hpp:413-428
     CK(cudaSetDevice(device));
+    AllocScope scope(s);
     const uint32_t n = D.n, m = D.m;
     T* tx = vec(n, false);
     T* tz = vec(m, false);
@@ -792,6 +823,7 @@ class Workspace {
 
   void debug_operator(const T* x, T* kx, T* dinv) {
     CK(cudaSetDevice(device));
+    AllocScope scope(s);
     pull_ctl();
     const Ctl<T> saved = hc;
     hc.pcg_active = 1;
@@ -810,6 +842,7 @@ class Workspace {
   // CUDA-event timing of the PCG-iteration kernels (bench.py roofline)
   void bench_kernels(uint32_t reps, double* out) {
     CK(cudaSetDevice(device));
+    AllocScope scope(s);
     pull_ctl();
     const Ctl<T> saved = hc;
     Ctl<T> run = hc;
@@ -866,6 +899,7 @@ class Workspace {
   // Not in the reference: rescale with the existing D, E, c.
   void update_vectors(const T* q, const T* l, const T* u) {
     CK(cudaSetDevice(device));
+    AllocScope scope(s);
     const uint32_t n = D.n, m = D.m;
     if (q) upload(D.q_o, q, sizeof(T) * n);
     if (l) upload(D.l_o, l, sizeof(T) * m);
@@ -1219,14 +1253,15 @@ static int op_spmv_impl(const CsrT* mv, const T* x, T* y, int device) {
     if (device >= 0) CK(cudaSetDevice(device));
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    AllocScope scope(s);
     CubTemp tmp;
     DevCsr<T> M{mv->rows, mv->cols, mv->nnz, nullptr, nullptr, nullptr};
     T *dx, *dy;
-    CK(cudaMalloc(&M.val, sizeof(T) * (M.nnz + 1)));
-    CK(cudaMalloc(&M.ci, 4 * (size_t(M.nnz) + 1)));
-    CK(cudaMalloc(&M.rp, 4 * (size_t(M.rows) + 1)));
-    CK(cudaMalloc(&dx, sizeof(T) * (M.cols + 1)));
-    CK(cudaMalloc(&dy, sizeof(T) * (M.rows + 1)));
+    CK(dmalloc(&M.val, sizeof(T) * (M.nnz + 1)));
+    CK(dmalloc(&M.ci, 4 * (size_t(M.nnz) + 1)));
+    CK(dmalloc(&M.rp, 4 * (size_t(M.rows) + 1)));
+    CK(dmalloc(&dx, sizeof(T) * (M.cols + 1)));
+    CK(dmalloc(&dy, sizeof(T) * (M.rows + 1)));
     CK(cudaMemcpyAsync(M.val, mv->values, sizeof(T) * M.nnz, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(M.ci, mv->col_indices, 4 * size_t(M.nnz), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(M.rp, mv->row_ptr, 4 * (size_t(M.rows) + 1), cudaMemcpyHostToDevice, s));
@@ -1236,11 +1271,14 @@ static int op_spmv_impl(const CsrT* mv, const T* x, T* y, int device) {
     CK(cudaMemcpyAsync(y, dy, sizeof(T) * M.rows, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     plan_free(P);
-    cudaFree(M.val);
-    cudaFree(M.ci);
-    cudaFree(M.rp);
-    cudaFree(dx);
-    cudaFree(dy);
+    dfree(M.val);
+    dfree(M.ci);
+    dfree(M.rp);
+    dfree(dx);
+    dfree(dy);
+    if (tmp.ptr) dfree(tmp.ptr);
+    tmp.ptr = nullptr;
+    CK(cudaStreamSynchronize(s));
     cudaStreamDestroy(s);
   });
 }

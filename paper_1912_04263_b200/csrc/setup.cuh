@@ -187,9 +187,9 @@ inline void transpose_structure(const uint32_t* ci, const uint32_t* row_of, uint
   CK(cudaMemsetAsync(out_rp, 0, sizeof(uint32_t) * (cols + 1), s));
   if (nnz == 0) return;
   uint32_t *cnt, *keys_out, *idx;
-  CK(cudaMalloc(&cnt, sizeof(uint32_t) * (cols + 1)));
-  CK(cudaMalloc(&keys_out, sizeof(uint32_t) * nnz));
-  CK(cudaMalloc(&idx, sizeof(uint32_t) * nnz));
+  CK(dmalloc(&cnt, sizeof(uint32_t) * (cols + 1)));
+  CK(dmalloc(&keys_out, sizeof(uint32_t) * nnz));
+  CK(dmalloc(&idx, sizeof(uint32_t) * nnz));
   CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (cols + 1), s));
   count_cols_kernel<<<grid_for(nnz), kThreads, 0, s>>>(ci, nnz, cnt);
   CK_LAUNCH();
@@ -204,9 +204,9 @@ inline void transpose_structure(const uint32_t* ci, const uint32_t* row_of, uint
   const uint32_t* perm_c = perm;
   for_n(nnz, [=] __device__(uint32_t i) { out_ci[i] = row_of[perm_c[i]]; }, s);
   CK(cudaStreamSynchronize(s));
-  CK(cudaFree(cnt));
-  CK(cudaFree(keys_out));
-  CK(cudaFree(idx));
+  CK(dfree(cnt));
+  CK(dfree(keys_out));
+  CK(dfree(idx));
 }
 
 template <typename T>
@@ -223,17 +223,17 @@ uint32_t symmetrize_upper_dev(const DevCsr<T>& up, const uint32_t* up_row_of, De
   const uint32_t n = up.rows, nnz = up.nnz;
   // strict-upper entries, in source order
   uint32_t *flags, *pos, *sel, *sel_cols, *lower_rp, *lower_ci, *lower_perm;
-  CK(cudaMalloc(&flags, sizeof(uint32_t) * (nnz + 1)));
-  CK(cudaMalloc(&pos, sizeof(uint32_t) * (nnz + 1)));
+  CK(dmalloc(&flags, sizeof(uint32_t) * (nnz + 1)));
+  CK(dmalloc(&pos, sizeof(uint32_t) * (nnz + 1)));
   const uint32_t* ci = up.ci;
   for_n(nnz, [=] __device__(uint32_t k) { flags[k] = ci[k] != up_row_of[k]; }, s);
   exclusive_scan_u32(flags, pos, nnz, tmp, s);
   const uint32_t nstrict = scan_total(flags, pos, nnz, s);
-  CK(cudaMalloc(&sel, sizeof(uint32_t) * (nstrict + 1)));
-  CK(cudaMalloc(&sel_cols, sizeof(uint32_t) * (nstrict + 1)));
-  CK(cudaMalloc(&lower_rp, sizeof(uint32_t) * (n + 1)));
-  CK(cudaMalloc(&lower_ci, sizeof(uint32_t) * (nstrict + 1)));
-  CK(cudaMalloc(&lower_perm, sizeof(uint32_t) * (nstrict + 1)));
+  CK(dmalloc(&sel, sizeof(uint32_t) * (nstrict + 1)));
+  CK(dmalloc(&sel_cols, sizeof(uint32_t) * (nstrict + 1)));
+  CK(dmalloc(&lower_rp, sizeof(uint32_t) * (n + 1)));
+  CK(dmalloc(&lower_ci, sizeof(uint32_t) * (nstrict + 1)));
+  CK(dmalloc(&lower_perm, sizeof(uint32_t) * (nstrict + 1)));
   for_n(nnz, [=] __device__(uint32_t k) {
     if (flags[k]) {
       sel[pos[k]] = k;
@@ -242,21 +242,21 @@ uint32_t symmetrize_upper_dev(const DevCsr<T>& up, const uint32_t* up_row_of, De
   }, s);
   // lower part = transpose of the strict upper part (rows ordered by source row)
   uint32_t* sel_rows;
-  CK(cudaMalloc(&sel_rows, sizeof(uint32_t) * (nstrict + 1)));
+  CK(dmalloc(&sel_rows, sizeof(uint32_t) * (nstrict + 1)));
   for_n(nstrict, [=] __device__(uint32_t i) { sel_rows[i] = up_row_of[sel[i]]; }, s);
   transpose_structure(sel_cols, sel_rows, n, nstrict, lower_rp, lower_ci, lower_perm, tmp, s);
   // out row j: lower_cnt(j) + upper_len(j)
   uint32_t *cnt;
-  CK(cudaMalloc(&cnt, sizeof(uint32_t) * (n + 1)));
+  CK(dmalloc(&cnt, sizeof(uint32_t) * (n + 1)));
   const uint32_t* urp = up.rp;
   for_n(n + 1, [=] __device__(uint32_t j) {
     cnt[j] = j < n ? (lower_rp[j + 1] - lower_rp[j]) + (urp[j + 1] - urp[j]) : 0u;
   }, s);
   out.rows = out.cols = n;
   out.nnz = nstrict + nnz;
-  CK(cudaMalloc(&out.rp, sizeof(uint32_t) * (n + 1)));
-  CK(cudaMalloc(&out.ci, sizeof(uint32_t) * (out.nnz + 1)));
-  CK(cudaMalloc(&out.val, sizeof(T) * (out.nnz + 1)));
+  CK(dmalloc(&out.rp, sizeof(uint32_t) * (n + 1)));
+  CK(dmalloc(&out.ci, sizeof(uint32_t) * (out.nnz + 1)));
+  CK(dmalloc(&out.val, sizeof(T) * (out.nnz + 1)));
   exclusive_scan_u32(cnt, out.rp, n + 1, tmp, s);
   uint32_t* orp = out.rp;
   uint32_t* oci = out.ci;
@@ -279,7 +279,7 @@ uint32_t symmetrize_upper_dev(const DevCsr<T>& up, const uint32_t* up_row_of, De
   CK(cudaStreamSynchronize(s));
   for (void* p : {(void*)flags, (void*)pos, (void*)sel, (void*)sel_cols, (void*)lower_rp,
                   (void*)lower_ci, (void*)lower_perm, (void*)sel_rows, (void*)cnt})
-    CK(cudaFree(p));
+    CK(dfree(p));
   return out.nnz;
 }
 
@@ -333,26 +333,55 @@ __global__ void extract_diag_kernel(DevCsr<T> P, T* out) {
   }
 }
 
-// Sequential sum of v[0..n) in index order (skipping exact zeros, which do
-// not change a non-negative running sum), then divided by n: the mean of
-// scaling.hpp:156-158.  One block; warp 0 does the ordered chain.
+// Sequential sum of v over the rows in `list` (increasing row order), divided
+// by n: the mean of scaling.hpp:156-158.  Rows outside the list are empty
+// (norm exactly 0) and x + 0 == x for the non-negative running sum, so the
+// chain is bit-identical to the reference's sum over all n rows.  One block:
+// warp 0 runs the ordered chain on a shared-memory tile while warps 1..7 stage
+// the next tile (double buffering hides the gather latency).
+constexpr int kMeanTile = 2048;
 template <typename T>
-__global__ void ordered_mean_kernel(const T* v, uint32_t n, T* out) {
-  if (threadIdx.x >= 32) return;
-  const uint32_t lane = threadIdx.x;
+__global__ void __launch_bounds__(256) ordered_mean_kernel(const T* __restrict__ v,
+                                                          const uint32_t* __restrict__ list,
+                                                          uint32_t cnt, uint32_t n, T* out) {
+  __shared__ T buf[2][kMeanTile];
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t i = tid; i < kMeanTile && i < cnt; i += blockDim.x) buf[0][i] = v[list[i]];
+  __syncthreads();
   T s = T(0);
-  for (uint32_t i0 = 0; i0 < n; i0 += 32) {
-    const uint32_t i = i0 + lane;
-    const T x = i < n ? v[i] : T(0);
-    uint32_t mask = __ballot_sync(0xffffffffu, x != T(0));
-    while (mask) {
-      const int j = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const T t = __shfl_sync(0xffffffffu, x, j);
-      s += t;
+  for (uint32_t t = 0; uint64_t(t) * kMeanTile < cnt; ++t) {
+    const uint32_t cur = t & 1u, nxt = cur ^ 1u;
+    const uint64_t base_next = uint64_t(t + 1) * kMeanTile;
+    if (tid >= 32) {
+      for (uint32_t i = tid - 32; i < kMeanTile && base_next + i < cnt; i += blockDim.x - 32)
+        buf[nxt][i] = v[list[base_next + i]];
+    } else if (tid == 0) {
+      const uint32_t m = uint32_t(min(uint64_t(kMeanTile), uint64_t(cnt) - uint64_t(t) * kMeanTile));
+      const T* b = buf[cur];
+      uint32_t i = 0;
+      for (; i + 8 <= m; i += 8) {
+        T r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = b[i + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += r[j];
+      }
+      for (; i < m; ++i) s += b[i];
     }
+    __syncthreads();
   }
-  if (lane == 0) *out = s / T(n);
+  if (tid == 0) *out = s / T(n);
+}
+
+// rows of a CSR structure with at least one stored entry, in increasing order
+__global__ void nonempty_flags_kernel(const uint32_t* rp, uint32_t rows, uint32_t* flags) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    flags[r] = rp[r + 1] > rp[r];
+}
+__global__ void compact_kernel(const uint32_t* flags, const uint32_t* pos, uint32_t rows,
+                               uint32_t* list) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    if (flags[r]) list[pos[r]] = r;
 }
 
 }  // namespace qpcg_b200

@@ -243,12 +243,12 @@ struct CubTemp {
   size_t bytes = 0;
   void ensure(size_t b) {
     if (b <= bytes) return;
-    if (ptr) CK(cudaFree(ptr));
-    CK(cudaMalloc(&ptr, b));
+    if (ptr) CK(dfree(ptr));
+    CK(dmalloc(&ptr, b));
     bytes = b;
   }
   ~CubTemp() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) dfree(ptr);  // owners free explicitly inside their AllocScope
   }
 };
 
@@ -279,11 +279,11 @@ inline uint32_t scan_total(const uint32_t* in, const uint32_t* ex, uint32_t n, c
 
 template <typename T>
 void plan_free(SpmvPlan<T>& P) {
-  cudaFree(P.items);
-  cudaFree(P.short_rows);
-  cudaFree(P.lrinfo);
-  cudaFree(P.partials);
-  cudaFree(P.counters);
+  dfree(P.items);
+  dfree(P.short_rows);
+  dfree(P.lrinfo);
+  dfree(P.partials);
+  dfree(P.counters);
   P = SpmvPlan<T>{};
 }
 
@@ -294,14 +294,14 @@ SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaSt
   if (rows == 0) return P;
   uint32_t *is_short, *nch, *is_multi, *multi_nch, *short_pos, *item_off, *lr_idx, *pbase;
   const size_t bytes = sizeof(uint32_t) * rows;
-  CK(cudaMalloc(&is_short, bytes));
-  CK(cudaMalloc(&nch, bytes));
-  CK(cudaMalloc(&is_multi, bytes));
-  CK(cudaMalloc(&multi_nch, bytes));
-  CK(cudaMalloc(&short_pos, bytes));
-  CK(cudaMalloc(&item_off, bytes));
-  CK(cudaMalloc(&lr_idx, bytes));
-  CK(cudaMalloc(&pbase, bytes));
+  CK(dmalloc(&is_short, bytes));
+  CK(dmalloc(&nch, bytes));
+  CK(dmalloc(&is_multi, bytes));
+  CK(dmalloc(&multi_nch, bytes));
+  CK(dmalloc(&short_pos, bytes));
+  CK(dmalloc(&item_off, bytes));
+  CK(dmalloc(&lr_idx, bytes));
+  CK(dmalloc(&pbase, bytes));
   plan_classify_kernel<<<grid_for(rows), kThreads, 0, s>>>(d_rp, rows, is_short, nch, is_multi,
                                                           multi_nch);
   CK_LAUNCH();
@@ -313,20 +313,20 @@ SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaSt
   P.n_items = scan_total(nch, item_off, rows, s);
   P.n_long = scan_total(is_multi, lr_idx, rows, s);
   P.n_partials = scan_total(multi_nch, pbase, rows, s);
-  CK(cudaMalloc(&P.short_rows, sizeof(uint32_t) * (P.n_short ? P.n_short : 1)));
-  CK(cudaMalloc(&P.items, sizeof(WorkItem) * (P.n_items ? P.n_items : 1)));
-  CK(cudaMalloc(&P.lrinfo, sizeof(uint2) * (P.n_long ? P.n_long : 1)));
-  CK(cudaMalloc(&P.partials, sizeof(T) * kMaxCols * (P.n_partials ? P.n_partials : 1)));
-  CK(cudaMalloc(&P.counters, sizeof(uint32_t) * (P.n_long ? P.n_long : 1)));
+  CK(dmalloc(&P.short_rows, sizeof(uint32_t) * (P.n_short ? P.n_short : 1)));
+  CK(dmalloc(&P.items, sizeof(WorkItem) * (P.n_items ? P.n_items : 1)));
+  CK(dmalloc(&P.lrinfo, sizeof(uint2) * (P.n_long ? P.n_long : 1)));
+  CK(dmalloc(&P.partials, sizeof(T) * kMaxCols * (P.n_partials ? P.n_partials : 1)));
+  CK(dmalloc(&P.counters, sizeof(uint32_t) * (P.n_long ? P.n_long : 1)));
   CK(cudaMemsetAsync(P.counters, 0, sizeof(uint32_t) * (P.n_long ? P.n_long : 1), s));
   WorkItem* items_tmp = nullptr;
   uint32_t *keys = nullptr, *keys_out = nullptr, *order = nullptr, *order_out = nullptr;
   const uint32_t ni = P.n_items ? P.n_items : 1;
-  CK(cudaMalloc(&items_tmp, sizeof(WorkItem) * ni));
-  CK(cudaMalloc(&keys, sizeof(uint32_t) * ni));
-  CK(cudaMalloc(&keys_out, sizeof(uint32_t) * ni));
-  CK(cudaMalloc(&order, sizeof(uint32_t) * ni));
-  CK(cudaMalloc(&order_out, sizeof(uint32_t) * ni));
+  CK(dmalloc(&items_tmp, sizeof(WorkItem) * ni));
+  CK(dmalloc(&keys, sizeof(uint32_t) * ni));
+  CK(dmalloc(&keys_out, sizeof(uint32_t) * ni));
+  CK(dmalloc(&order, sizeof(uint32_t) * ni));
+  CK(dmalloc(&order_out, sizeof(uint32_t) * ni));
   plan_emit_kernel<<<grid_for(rows), kThreads, 0, s>>>(d_rp, rows, is_short, short_pos, nch,
                                                       item_off, lr_idx, pbase, P.short_rows,
                                                       items_tmp, keys, P.lrinfo);
@@ -351,7 +351,7 @@ SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaSt
   for (void* p : {(void*)is_short, (void*)nch, (void*)is_multi, (void*)multi_nch, (void*)short_pos,
                   (void*)item_off, (void*)lr_idx, (void*)pbase, (void*)items_tmp, (void*)keys,
                   (void*)keys_out, (void*)order, (void*)order_out})
-    CK(cudaFree(p));
+    CK(dfree(p));
   return P;
 }
 
