@@ -154,17 +154,30 @@ typedef struct {
                              conditional while/if nodes (default) */
 #define QPCG_MODE_EAGER 1 /* host-driven loop with a sync per decision (debug) */
 
+/* Row sharding.  A is cut into G = virtual_shards x
+ * nccl_ranks contiguous nnz-balanced row blocks (qpcg_shard_cuts); every
+ * block keeps its own A_g^T, P and the n-vectors are replicated, and the A^T
+ * partials are summed across blocks once per operator apply.  Every rank
+ * passes the FULL problem (it uploads only its blocks) and receives the full
+ * x, z, y.  The sharded loop is host-driven (mode is ignored). */
 typedef struct {
   int32_t device;          /* CUDA ordinal, -1 = current */
   int32_t input_memory;    /* QPCG_MEM_HOST / QPCG_MEM_DEVICE */
   int32_t mode;            /* QPCG_MODE_* */
   int32_t record_diagnostics; /* 1: keep per-PCG-call records */
-  int32_t virtual_shards;  /* >1: hold A as G row blocks on one device and sum
-                              the A^T partials in shard order */
+  int32_t virtual_shards;  /* >1: this process holds that many row blocks on
+                              its device, combined in block order */
+  int32_t nccl_rank;       /* rank of this process in the NCCL group */
+  int32_t nccl_ranks;      /* processes (one per GPU) in the NCCL group */
   int32_t reserved_;
   void* stream;            /* cudaStream_t to run on (NULL: the workspace
                               creates its own non-blocking stream) */
+  const void* nccl_id;     /* NULL: no NCCL.  Else the QPCG_NCCL_ID_BYTES-byte
+                              id from qpcg_nccl_unique_id on rank 0, shared by
+                              all ranks (e.g. a torch.distributed broadcast) */
 } qpcg_options;
+
+#define QPCG_NCCL_ID_BYTES 128
 
 typedef struct qpcg_workspace qpcg_workspace;
 
@@ -216,6 +229,17 @@ int qpcg_f32_solve_problem(const qpcg_csr_f32* p_upper, const float* q,
                            const float* warm_z, const float* warm_y,
                            qpcg_info* info, float* x, float* z, float* y,
                            float* cert, char* msg, size_t msg_len);
+
+/* ---- row sharding --------------------------------------------------------
+ * nnz-balanced contiguous row cuts of a CSR row_ptr (host memory) into G
+ * blocks: block g owns rows [cuts[g], cuts[g+1]) with cuts[g] the first row
+ * whose row_ptr >= g*nnz/G.  Returns 1, or 0 when row_ptr is invalid (then
+ * every row is on block 0 and setup reports the reference's error). */
+int qpcg_shard_cuts(const uint32_t* row_ptr, uint32_t rows, uint32_t nnz,
+                    uint32_t blocks, uint32_t* cuts);
+/* writes QPCG_NCCL_ID_BYTES bytes (ncclGetUniqueId); QPCG_ERR_NCCL if NCCL
+ * cannot be loaded */
+int qpcg_nccl_unique_id(void* out);
 
 /* ---- common to both precisions ------------------------------------------ */
 void qpcg_cleanup(qpcg_workspace* ws);

@@ -77,7 +77,11 @@ class RhoUpdate(C.Structure):
 class Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("input_memory", C.c_int32), ("mode", C.c_int32),
                 ("record_diagnostics", C.c_int32), ("virtual_shards", C.c_int32),
-                ("reserved_", C.c_int32), ("stream", C.c_void_p)]
+                ("nccl_rank", C.c_int32), ("nccl_ranks", C.c_int32), ("reserved_", C.c_int32),
+                ("stream", C.c_void_p), ("nccl_id", C.c_void_p)]
+
+
+NCCL_ID_BYTES = 128
 
 
 def default_settings() -> Settings:

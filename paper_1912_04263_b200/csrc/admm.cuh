@@ -95,7 +95,17 @@ struct Dev {
   DiagRec<T>* calls;
   uint32_t* checks;
   RhoRec<T>* rhos;
+  // row sharding.  split == 0: the fused single-device
+  // path.  split == 1: this Dev is one row block of A; the A^T passes write
+  // n-partials into `part` and the m-side scalar reductions into `shsc`, the
+  // comm combines them across shards, and the *_finish / *_decide kernels
+  // consume the combined values (identical on every shard).
+  uint32_t split, sh_index, sh_count, pad_sh;
+  T* part;  // [2n]
+  T* shsc;  // [kShScal]
 };
+
+constexpr int kShScal = 16;
 
 constexpr int kMaxQ = 16;
 
@@ -235,6 +245,14 @@ __global__ void k_pack_rhs(Dev<T> D) {
   }
 }
 template <typename T>
+__device__ __forceinline__ void rhs_row(const Dev<T>& D, T sigma, uint32_t r, T s0, T s1) {
+  const T rhs = s0 + (sigma * D.x[r] - D.q[r]);
+  const T xt = D.xt[r];
+  const T kx = (prow_dot(D.P, r, D.xt) + sigma * xt) + s1;
+  D.b[r] = rhs;
+  D.r[r] = kx - rhs;
+}
+template <typename T>
 struct EpiRhs {
   Dev<T> D;
   T sigma;
@@ -243,11 +261,7 @@ struct EpiRhs {
     return D.ctl->error == 0;
   }
   __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[2]) const {
-    const T rhs = s[0] + (sigma * D.x[r] - D.q[r]);
-    const T xt = D.xt[r];
-    const T kx = (prow_dot(D.P, r, D.xt) + sigma * xt) + s[1];
-    D.b[r] = rhs;
-    D.r[r] = kx - rhs;
+    rhs_row(D, sigma, r, s[0], s[1]);
   }
 };
 
@@ -266,6 +280,10 @@ struct EpiAp {
 
 // Kp = (P p + sigma p) + A^T t   (linsys.hpp:86-89)
 template <typename T>
+__device__ __forceinline__ T kp_row(const Dev<T>& D, T sigma, uint32_t r, T s) {
+  return (prow_dot(D.P, r, D.p) + sigma * D.p[r]) + s;
+}
+template <typename T>
 struct EpiKp {
   Dev<T> D;
   T sigma;
@@ -274,7 +292,7 @@ struct EpiKp {
     return D.ctl->pcg_active != 0 && D.ctl->error == 0;
   }
   __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const {
-    D.kp[r] = (prow_dot(D.P, r, D.p) + sigma * D.p[r]) + s[0];
+    D.kp[r] = kp_row(D, sigma, r, s[0]);
   }
 };
 
@@ -327,15 +345,17 @@ struct EpiStore {
 
 // A^T y with P x and r_dual fused (compute_residuals, solver.hpp:197-204)
 template <typename T>
+__device__ __forceinline__ void dual_row(const Dev<T>& D, uint32_t r, T s) {
+  const T px = prow_dot(D.P, r, D.x);
+  D.aty[r] = s;
+  D.px[r] = px;
+  D.rdual[r] = px + D.q[r] + s;
+}
+template <typename T>
 struct EpiDual {
   Dev<T> D;
   __device__ __forceinline__ bool init() { return D.ctl->error == 0; }
-  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const {
-    const T px = prow_dot(D.P, r, D.x);
-    D.aty[r] = s[0];
-    D.px[r] = px;
-    D.rdual[r] = px + D.q[r] + s[0];
-  }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const { dual_row(D, r, s[0]); }
 };
 
 // certificate vectors formed on the fly (certificate_vectors, solver.hpp:318-325,
@@ -397,6 +417,65 @@ struct EpiDualRows {  // per-row sign tests of check_dual_infeasible (:283-295)
   }
 };
 
+// ---------------------------------------------------------------------
+// split (row-sharded) A^T passes: store the shard's n-partials; the comm sums
+// them across shards and the finish kernels below apply the epilogue.
+// gate: 0 always, 1 while PCG is active, 2 while the primal certificate is
+// still possible (need_pinf).
+template <typename T, int NCOL>
+struct EpiPart {
+  T* out;
+  const Ctl<T>* ctl;
+  uint32_t gate;
+  __device__ __forceinline__ bool init() {
+    if (ctl->error) return false;
+    if (gate == 1) return ctl->pcg_active != 0;
+    if (gate == 2) return ctl->inf_branch != 0 && ctl->need_pinf != 0;
+    return true;
+  }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[NCOL]) const {
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) out[(size_t)r * NCOL + j] = s[j];
+  }
+};
+
+// rhs / r0 from the combined 2-column partials (EpiRhs semantics)
+template <typename T>
+__global__ void k_rhs_finish(Dev<T> D) {
+  const Ctl<T>* C = D.ctl;
+  if (C->error) return;
+  const T sigma = C->sigma;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
+    rhs_row(D, sigma, i, D.part[2 * (size_t)i], D.part[2 * (size_t)i + 1]);
+}
+
+// A^T y, P x, r_dual from the combined partial (EpiDual semantics)
+template <typename T>
+__global__ void k_dual_finish(Dev<T> D) {
+  if (D.ctl->error) return;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
+    dual_row(D, i, D.part[i]);
+}
+
+// |A_o^T v|_inf of the combined certificate product (EpiNormMax semantics)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_atv_norm(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (C->error || !C->inf_branch || !C->need_pinf) return;
+  T v[1] = {T(0)};
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
+    v[0] = smax(v[0], tabs(D.part[i]));
+  T tot[1];
+  if (!grid_reduce<T, 1>(v, 0x1u, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x == 0) atomic_max_nonneg(&C->atv_inf_bits, tot[0]);
+}
+
+// the shard's dual-row flag as a summable scalar
+template <typename T>
+__global__ void k_flag_to_scal(Dev<T> D) {
+  D.shsc[0] = D.ctl->dinf_bad ? T(1) : T(0);
+}
+
 // =====================================================================
 // vector kernels
 // =====================================================================
@@ -450,8 +529,17 @@ __global__ void __launch_bounds__(kThreads) k_pcg_dot(Dev<T> D) {
   Ctl<T>* C = D.ctl;
   if (!C->pcg_active || C->error) return;
   T v[1] = {T(0)};
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
-    v[0] += D.p[i] * D.kp[i];
+  if (D.split) {  // Kp = (P p + sigma p) + sum_g A_g^T t_g  (EpiKp semantics)
+    const T sigma = C->sigma;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+      const T kp = kp_row(D, sigma, i, D.part[i]);
+      D.kp[i] = kp;
+      v[0] += D.p[i] * kp;
+    }
+  } else {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
+      v[0] += D.p[i] * D.kp[i];
+  }
   T tot[1];
   if (!grid_reduce<T, 1>(v, 0x0u, D.red, &C->red_counter, tot)) return;
   if (threadIdx.x != 0) return;
@@ -584,47 +672,12 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(Dev<T> D, Handles H) {
   }
 }
 
-// Residual norms (solver.hpp:205-206, 468-475) + termination (:476-495 start).
-// mode 0: loop check; mode 1: initial residuals (eps only); mode 2: final.
+// Residual bookkeeping, adaptive eps and the termination test from the 14
+// reduced norms (solver.hpp:205-206, 222-230, 468-476; linsys.hpp:170-179).
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Handles H) {
+__device__ void residuals_decide(Dev<T> D, const T (&tot)[14], int mode, Handles H) {
   Ctl<T>* C = D.ctl;
-  if (C->error) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.inf, 0);
-    return;
-  }
-  const uint32_t n = D.n, m = D.m;
   const T c_inv = C->c_inv;
-  // 0 rp_s 1 ax_s 2 z_s 3 rp_o 4 ax_o 5 z_o 6 dy_norm | 7 rd_s 8 px_s 9 aty_s
-  // 10 rd_o' 11 px_o' 12 aty_o' 13 dx_norm
-  T v[14];
-#pragma unroll
-  for (int q = 0; q < 14; ++q) v[q] = T(0);
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
-    const T ax = D.ax[i], z = D.z[i], ei = D.e_inv[i];
-    const T rp = ax - z;
-    v[0] = smax(v[0], tabs(rp));
-    v[1] = smax(v[1], tabs(ax));
-    v[2] = smax(v[2], tabs(z));
-    v[3] = smax(v[3], tabs(rp * ei));
-    v[4] = smax(v[4], tabs(ax * ei));
-    v[5] = smax(v[5], tabs(z * ei));
-    v[6] = smax(v[6], tabs((D.e[i] * D.dy[i]) * c_inv));
-  }
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const T rd = D.rdual[i], px = D.px[i], aty = D.aty[i], di = D.d_inv[i];
-    v[7] = smax(v[7], tabs(rd));
-    v[8] = smax(v[8], tabs(px));
-    v[9] = smax(v[9], tabs(aty));
-    v[10] = smax(v[10], tabs(rd * di));
-    v[11] = smax(v[11], tabs(px * di));
-    v[12] = smax(v[12], tabs(aty * di));
-    v[13] = smax(v[13], tabs(D.d[i] * D.dx[i]));
-  }
-  T tot[14];
-  if (!grid_reduce<T, 14>(v, 0x3fffu, D.red, &C->red_counter, tot)) return;
-  if (threadIdx.x != 0) return;
   C->rp_s = tot[0];
   C->ax_s = tot[1];
   C->z_s = tot[2];
@@ -672,6 +725,63 @@ __global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Hand
   set_cond(H.inf, inf);
 }
 
+// Residual norms (solver.hpp:205-206, 468-475) + termination (:476-495 start).
+// mode 0: loop check; mode 1: initial residuals (eps only); mode 2: final.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Handles H) {
+  Ctl<T>* C = D.ctl;
+  if (C->error) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.inf, 0);
+    return;
+  }
+  const uint32_t n = D.n, m = D.m;
+  const T c_inv = C->c_inv;
+  // 0 rp_s 1 ax_s 2 z_s 3 rp_o 4 ax_o 5 z_o 6 dy_norm | 7 rd_s 8 px_s 9 aty_s
+  // 10 rd_o' 11 px_o' 12 aty_o' 13 dx_norm
+  T v[14];
+#pragma unroll
+  for (int q = 0; q < 14; ++q) v[q] = T(0);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const T ax = D.ax[i], z = D.z[i], ei = D.e_inv[i];
+    const T rp = ax - z;
+    v[0] = smax(v[0], tabs(rp));
+    v[1] = smax(v[1], tabs(ax));
+    v[2] = smax(v[2], tabs(z));
+    v[3] = smax(v[3], tabs(rp * ei));
+    v[4] = smax(v[4], tabs(ax * ei));
+    v[5] = smax(v[5], tabs(z * ei));
+    v[6] = smax(v[6], tabs((D.e[i] * D.dy[i]) * c_inv));
+  }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const T rd = D.rdual[i], px = D.px[i], aty = D.aty[i], di = D.d_inv[i];
+    v[7] = smax(v[7], tabs(rd));
+    v[8] = smax(v[8], tabs(px));
+    v[9] = smax(v[9], tabs(aty));
+    v[10] = smax(v[10], tabs(rd * di));
+    v[11] = smax(v[11], tabs(px * di));
+    v[12] = smax(v[12], tabs(aty * di));
+    v[13] = smax(v[13], tabs(D.d[i] * D.dx[i]));
+  }
+  T tot[14];
+  if (!grid_reduce<T, 14>(v, 0x3fffu, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  if (D.split) {  // shard partials: every entry is a max, combined by the comm
+    for (int q = 0; q < 14; ++q) D.shsc[q] = tot[q];
+    return;
+  }
+  residuals_decide(D, tot, mode, H);
+}
+
+// split mode: the decision from the combined maxima
+template <typename T>
+__global__ void k_residuals_decide(Dev<T> D, int mode, Handles H) {
+  if (threadIdx.x != 0 || D.ctl->error) return;
+  T tot[14];
+  for (int q = 0; q < 14; ++q) tot[q] = D.shsc[q];
+  residuals_decide(D, tot, mode, H);
+}
+
 // Infeasibility tests (solver.hpp:236-297, 481-495).  Both tests are
 // conjunctions, so they are evaluated cheapest-first and each A-sized pass
 // over the ORIGINAL matrices runs only while its certificate is still
@@ -679,6 +789,13 @@ __global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Hand
 // the reference, far fewer matrix streams on ordinary (feasible) solves.
 // Stage 1: the vector parts — support sum and infinite-bound tests of the
 // primal certificate (:248-263), q'v of the dual one (:281).
+template <typename T>
+__device__ void infeas_vec_decide(Ctl<T>* C, const T (&tot)[3]) {
+  C->support = tot[0];
+  C->qv = tot[2];
+  if (C->need_pinf && !(tot[1] == T(0) && tot[0] < C->eps_pinf)) C->need_pinf = 0;
+  if (C->need_dinf && !(tot[2] < C->eps_dinf)) C->need_dinf = 0;
+}
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_infeas_vec(Dev<T> D) {
   Ctl<T>* C = D.ctl;
@@ -706,17 +823,29 @@ __global__ void __launch_bounds__(kThreads) k_infeas_vec(Dev<T> D) {
       }
     }
   }
-  if (C->need_dinf) {
+  // (n-vectors are replicated across row blocks: block 0 alone sums q'v)
+  if (C->need_dinf && (!D.split || D.sh_index == 0)) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
       v[2] += D.q_o[i] * ((D.d[i] * D.dx[i]) * sx);
   }
   T tot[3];
   if (!grid_reduce<T, 3>(v, 0x2u, D.red, &C->red_counter, tot)) return;
   if (threadIdx.x != 0) return;
-  C->support = tot[0];
-  C->qv = tot[2];
-  if (C->need_pinf && !(tot[1] == T(0) && tot[0] < eps_p)) C->need_pinf = 0;
-  if (C->need_dinf && !(tot[2] < C->eps_dinf)) C->need_dinf = 0;
+  if (D.split) {  // partials, combined by a sum (bad: a count, still 0 iff none)
+    D.shsc[0] = tot[0];
+    D.shsc[1] = tot[1];
+    D.shsc[2] = tot[2];
+    return;
+  }
+  infeas_vec_decide(C, tot);
+}
+
+template <typename T>
+__global__ void k_infeas_vec_decide(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (threadIdx.x != 0 || C->error || !C->inf_branch) return;
+  const T tot[3] = {D.shsc[0], D.shsc[1], D.shsc[2]};
+  infeas_vec_decide(C, tot);
 }
 
 // Stage 2 (after the P_orig pass): |P v| <= eps (:280)
@@ -733,7 +862,7 @@ __global__ void k_infeas(Dev<T> D) {
   Ctl<T>* C = D.ctl;
   if (C->error || !C->inf_branch) return;
   const bool primal = C->need_pinf && !(bits_to_value(C->atv_inf_bits, T(0)) > C->eps_pinf);
-  const bool dual = C->need_dinf && C->dinf_bad == 0;
+  const bool dual = C->need_dinf && (D.split ? D.shsc[0] == T(0) : C->dinf_bad == 0);
   if (primal) {
     C->status = 1;
     C->done = 1;
@@ -753,6 +882,9 @@ __global__ void k_rho_flag(Dev<T> D, Handles H) {
   set_cond(H.rho, f);
 }
 
+template <typename T>
+__device__ void rho_decide(Dev<T> D, T z_inf);
+
 // adapt_rho (solver.hpp:302-314) from the last residuals and the current |z|
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_rho(Dev<T> D) {
@@ -764,8 +896,24 @@ __global__ void __launch_bounds__(kThreads) k_rho(Dev<T> D) {
   T tot[1];
   if (!grid_reduce<T, 1>(v, 0x1u, D.red, &C->red_counter, tot)) return;
   if (threadIdx.x != 0) return;
+  if (D.split) {  // this block's max |z|, combined by a max
+    D.shsc[0] = tot[0];
+    return;
+  }
+  rho_decide(D, tot[0]);
+}
+
+template <typename T>
+__global__ void k_rho_decide(Dev<T> D) {
+  if (threadIdx.x != 0 || !D.ctl->rho_branch) return;
+  rho_decide(D, D.shsc[0]);
+}
+
+template <typename T>
+__device__ void rho_decide(Dev<T> D, T z_inf) {
+  Ctl<T>* C = D.ctl;
   const T fl = T(1e-10);
-  const T rel_prim = C->last_rp / smax(smax(C->ax_s, tot[0]), fl);
+  const T rel_prim = C->last_rp / smax(smax(C->ax_s, z_inf), fl);
   const T rel_dual = C->last_rd / smax(smax(smax(C->px_s, C->aty_s), C->q_inf_scaled), fl);
   const T rho = C->rho;
   T next;

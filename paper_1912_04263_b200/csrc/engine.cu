@@ -26,6 +26,7 @@
 #include "../../include/qpcg_b200.h"
 #include "../../include/qpcg_b200_ops.h"
 #include "admm.cuh"
+#include "comm.cuh"
 #include "setup.cuh"
 
 namespace qpcg_b200 {
@@ -171,66 +172,195 @@ class Workspace {
   void push_ctl() { CK(cudaMemcpyAsync(D.ctl, &hc, sizeof(Ctl<T>), cudaMemcpyHostToDevice, s)); }
 
   // ------------------------------------------------------------- setup
+  // The single-device setup; the sharded path (shard.cuh) runs the same
+  // phases per row block with its collectives in between.
   void setup(const HostCsr<T>& Pu, const T* q, const HostCsr<T>& A, const T* l, const T* u,
              const qpcg_settings& st, const qpcg_options& op) {
     const double w0 = now_s();
     const uint64_t l0 = g_launches;
+    begin(st, op, nullptr);
+    AllocScope scope(s);
+    CK(cudaEventRecord(ev0, s));
+    load(Pu, q, A, l, u, 0, A.rows, false);
+    ValKeys k = validate_keys();
+    raise_first(k);
+    build_structures();
+    uint32_t passes = 0;
+    T deviation = T(0);
+    if (set.scaling_enabled) {
+      ruiz_prepare();
+      deviation = T(1);
+      while (passes < set.equil_max_passes && deviation > T(set.eps_equil)) {
+        ++passes;
+        ruiz_norms();
+        ruiz_delta();
+        ruiz_scale();
+        deviation = read_scalar(ruiz_scal + 4);
+      }
+    }
+    finish_scaling(passes, deviation);
+    diag_ata_kernel<T><<<grid_for(uint64_t(D.n) * 32), kThreads, 0, s>>>(D.AT, D.diag_ata, nullptr);
+    CK_LAUNCH();
+    finish_setup();
+    CK(cudaEventRecord(ev1, s));
+    CK(cudaEventSynchronize(ev1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    setup_seconds = ms * 1e-3;
+    setup_wall = now_s() - w0;
+    setup_launches = g_launches - l0;
+  }
+
+  uint32_t equil_passes = 0;
+  T equil_residual = T(0);
+
+  // setup-phase state
+  uint32_t *pu_rp = nullptr, *pu_ci = nullptr, *a_rp = nullptr, *a_ci = nullptr;
+  T *pu_v = nullptr, *a_v = nullptr;
+  uint32_t pu_nnz = 0, pu_cols = 0, a_cols = 0;
+  uint32_t row0 = 0;  // first global row of this block of A (sharded path)
+  uint32_t nnz0 = 0;  // first global entry of this block
+  bool p_square = true, a_cols_ok = true;
+  T *rz_dx = nullptr, *rz_dz = nullptr, *rz_pn = nullptr, *rz_atn = nullptr, *rz_an = nullptr;
+
+  // settings, device, stream, pool, events
+  void begin(const qpcg_settings& st, const qpcg_options& op, cudaStream_t shared) {
     set = st;
     opt = op;
     validate_settings(st);
     device = op.device;
     if (device < 0) CK(cudaGetDevice(&device));
     CK(cudaSetDevice(device));
-    if (op.stream != nullptr) {
+    if (shared != nullptr) {
+      s = shared;
+      own_stream = false;
+    } else if (op.stream != nullptr) {
       s = static_cast<cudaStream_t>(op.stream);
       own_stream = false;
     } else {
       CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     }
     configure_pool(device);
-    AllocScope scope(s);
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
-    const uint32_t n = Pu.rows, m = A.rows;
-    // host-side shape checks that do not need the data (problem.hpp:47-58 order
-    // is preserved below by deferring these messages until after the CSR loops)
-    const bool p_square = Pu.rows == Pu.cols;
-    const bool a_cols_ok = A.cols == Pu.cols;
-    CK(cudaEventRecord(ev0, s));
+  }
+
+  // Upload P (upper), q and the row block [r0, r1) of A, l, u — the only
+  // host->device traffic of a solve.  slice == false: A as given (rows 0..m).
+  void load(const HostCsr<T>& Pu, const T* q, const HostCsr<T>& A, const T* l, const T* u,
+            uint32_t r0, uint32_t r1, bool slice) {
+    const double th = now_s();
+    const uint32_t n = Pu.rows, m = r1 - r0;
+    p_square = Pu.rows == Pu.cols;
+    a_cols_ok = A.cols == Pu.cols;
+    pu_nnz = Pu.nnz;
+    pu_cols = Pu.cols;
+    a_cols = A.cols;
     D.n = n;
     D.m = m;
-    // ---- upload (the only host->device traffic of a solve)
-    const double th = now_s();
-    uint32_t* pu_rp = alloc<uint32_t>(n + 1);
-    uint32_t* pu_ci = alloc<uint32_t>(Pu.nnz);
-    T* pu_v = alloc<T>(Pu.nnz);
-    uint32_t* a_rp = alloc<uint32_t>(m + 1);
-    uint32_t* a_ci = alloc<uint32_t>(A.nnz);
-    T* a_v = alloc<T>(A.nnz);
+    uint32_t e0 = 0, e1 = A.nnz;
+    if (slice) {  // row_ptr is valid here (shard_cuts checked it on the host)
+      e0 = host_rp(A, r0);
+      e1 = host_rp(A, r1);
+    }
+    row0 = r0;
+    nnz0 = e0;
+    const uint32_t annz = e1 - e0;
+    pu_rp = alloc<uint32_t>(n + 1);
+    pu_ci = alloc<uint32_t>(Pu.nnz);
+    pu_v = alloc<T>(Pu.nnz);
+    a_rp = alloc<uint32_t>(m + 1);
+    a_ci = alloc<uint32_t>(annz);
+    a_v = alloc<T>(annz);
     D.q_o = alloc<T>(n);
     D.l_o = alloc<T>(m);
     D.u_o = alloc<T>(m);
     upload(pu_rp, Pu.row_ptr, sizeof(uint32_t) * (n + 1));
     upload(pu_ci, Pu.col_indices, sizeof(uint32_t) * Pu.nnz);
     upload(pu_v, Pu.values, sizeof(T) * Pu.nnz);
-    upload(a_rp, A.row_ptr, sizeof(uint32_t) * (m + 1));
-    upload(a_ci, A.col_indices, sizeof(uint32_t) * A.nnz);
-    upload(a_v, A.values, sizeof(T) * A.nnz);
+    upload(a_rp, A.row_ptr + r0, sizeof(uint32_t) * (m + 1));
+    upload(a_ci, A.col_indices + e0, sizeof(uint32_t) * annz);
+    upload(a_v, A.values + e0, sizeof(T) * annz);
     upload(D.q_o, q, sizeof(T) * n);
-    upload(D.l_o, l, sizeof(T) * m);
-    upload(D.u_o, u, sizeof(T) * m);
+    upload(D.l_o, l + r0, sizeof(T) * m);
+    upload(D.u_o, u + r0, sizeof(T) * m);
+    if (slice && e0 != 0) {
+      uint32_t* rp = a_rp;
+      for_n(m + 1, [=] __device__(uint32_t i) { rp[i] -= e0; }, s);
+    }
+    D.A = DevCsr<T>{m, A.cols, annz, a_v, a_rp, a_ci};
     if (opt.input_memory == QPCG_MEM_HOST) {
       CK(cudaStreamSynchronize(s));
       h2d_seconds = now_s() - th;
     }
-    // ---- validation (problem.hpp:46-92, sparse.hpp:98-124)
-    validate_problem(Pu, A, pu_rp, pu_ci, pu_v, a_rp, a_ci, a_v, p_square, a_cols_ok);
-    DevCsr<T> Pup{n, n, Pu.nnz, pu_v, pu_rp, pu_ci};
-    D.A = DevCsr<T>{m, n, A.nnz, a_v, a_rp, a_ci};  // values replaced by scaled copy below
-    // ---- plans and structures
+  }
+  uint32_t host_rp(const HostCsr<T>& A, uint32_t r) {
+    if (opt.input_memory == QPCG_MEM_HOST) return A.row_ptr[r];
+    uint32_t v = 0;
+    CK(cudaMemcpyAsync(&v, A.row_ptr + r, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return v;
+  }
+
+  // Validation (problem.hpp:46-92, sparse.hpp:98-124): three stage keys, each
+  // the minimum (category, global index, position) found; raise_first applies
+  // the reference's check order.  Keys of row blocks combine by min.
+  struct ValKeys {
+    unsigned long long k[3];  // P rows, A rows, values/bounds
+    uint32_t ends[4];         // P row_ptr ends, A row_ptr ends (block-local)
+  };
+  ValKeys validate_keys() {
+    const uint32_t n = D.n, m = D.m;
+    ValKeys v;
+    CK(cudaMemcpyAsync(v.ends + 0, pu_rp, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(v.ends + 1, pu_rp + n, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(v.ends + 2, a_rp, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(v.ends + 3, a_rp + m, 4, cudaMemcpyDeviceToHost, s));
+    unsigned long long* key = alloc<unsigned long long>(3);
+    CK(cudaMemsetAsync(key, 0xff, 24, s));
+    CK(cudaStreamSynchronize(s));
+    const bool p_ok = v.ends[0] == 0 && v.ends[1] == pu_nnz;
+    const bool a_ok = v.ends[2] == 0 && v.ends[3] == D.A.nnz;
+    if (p_ok) {
+      validate_csr_rows_kernel<<<grid_for(n), kThreads, 0, s>>>(pu_rp, pu_ci, n, pu_cols, kValPRowPtr,
+                                                               p_square ? 1 : 0, key, 0);
+      CK_LAUNCH();
+    }
+    if (a_ok) {
+      validate_csr_rows_kernel<<<grid_for(m), kThreads, 0, s>>>(a_rp, a_ci, m, a_cols, kValARowPtr, 0,
+                                                               key + 1, row0);
+      CK_LAUNCH();
+      validate_values_kernel<T><<<grid_for(pu_nnz), kThreads, 0, s>>>(pu_v, pu_nnz, kValPFinite, key + 2, 0);
+      validate_values_kernel<T><<<grid_for(D.A.nnz), kThreads, 0, s>>>(a_v, D.A.nnz, kValAFinite, key + 2, nnz0);
+      validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.q_o, n, kValQFinite, key + 2, 0);
+      validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(D.l_o, D.u_o, m, key + 2, row0);
+      CK_LAUNCH();
+    }
+    CK(cudaMemcpyAsync(v.k, key, 24, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return v;
+  }
+  void raise_first(const ValKeys& v) const {
+    if (v.ends[0] != 0 || v.ends[1] != pu_nnz)
+      throw InvalidArgument("csr: row_ptr must start at 0 and end at nnz");
+    if ((v.k[0] >> 56) == kValPRowPtr) throw InvalidArgument(validation_message(v.k[0]));
+    if (v.ends[2] != 0 || v.ends[3] != D.A.nnz)
+      throw InvalidArgument("csr: row_ptr must start at 0 and end at nnz");
+    if ((v.k[1] >> 56) == kValARowPtr) throw InvalidArgument(validation_message(v.k[1]));
+    if (!p_square) throw InvalidArgument("problem: P must be square");
+    if (D.n == 0) throw InvalidArgument("problem: at least one variable required");
+    if ((v.k[0] >> 56) == kValPBelow) throw InvalidArgument(validation_message(v.k[0]));
+    if (!a_cols_ok) throw InvalidArgument("problem: A column count must equal n");
+    if (v.k[2] != ~0ull) throw InvalidArgument(validation_message(v.k[2]));
+  }
+
+  // symmetrize_upper, transpose_csr, plans, the original and scaled copies
+  void build_structures() {
+    const uint32_t n = D.n, m = D.m, annz = D.A.nnz;
+    DevCsr<T> Pup{n, n, pu_nnz, pu_v, pu_rp, pu_ci};
     SpmvPlan<T> pPu = plan_build<T>(pu_rp, n, tmp, s);
     D.pA = plan_build<T>(a_rp, m, tmp, s);
-    uint32_t* row_of = alloc<uint32_t>(std::max(Pu.nnz, A.nnz));
+    uint32_t* row_of = alloc<uint32_t>(std::max(pu_nnz, annz));
     plan_visit(Pup, pPu, RowOfFn{row_of}, s);
     // symmetrize_upper (solver.hpp:397)
     DevCsr<T> Pfull;
@@ -244,13 +374,13 @@ class Workspace {
     // transpose_csr (solver.hpp:398)
     plan_visit(D.A, D.pA, RowOfFn{row_of}, s);
     uint32_t* at_rp = alloc<uint32_t>(n + 1);
-    uint32_t* at_ci = alloc<uint32_t>(A.nnz);
-    permA = alloc<uint32_t>(A.nnz);
-    transpose_structure(a_ci, row_of, n, A.nnz, at_rp, at_ci, permA, tmp, s);
-    T* ato_v = alloc<T>(A.nnz);
-    gather_values(a_v, permA, A.nnz, ato_v, s);
-    D.Ao = DevCsr<T>{m, n, A.nnz, a_v, a_rp, a_ci};
-    D.ATo = DevCsr<T>{n, m, A.nnz, ato_v, at_rp, at_ci};
+    uint32_t* at_ci = alloc<uint32_t>(annz);
+    permA = alloc<uint32_t>(annz);
+    transpose_structure(a_ci, row_of, n, annz, at_rp, at_ci, permA, tmp, s);
+    T* ato_v = alloc<T>(annz);
+    gather_values(a_v, permA, annz, ato_v, s);
+    D.Ao = DevCsr<T>{m, n, annz, a_v, a_rp, a_ci};
+    D.ATo = DevCsr<T>{n, m, annz, ato_v, at_rp, at_ci};
     D.pAT = plan_build<T>(at_rp, n, tmp, s);
     D.pPo = D.pP;
     D.pAo = D.pA;
@@ -266,11 +396,11 @@ class Workspace {
     CK_LAUNCH();
     // ---- scaled copies
     D.P = DevCsr<T>{n, n, Pfull.nnz, alloc<T>(Pfull.nnz), Pfull.rp, Pfull.ci};
-    D.A = DevCsr<T>{m, n, A.nnz, alloc<T>(A.nnz), a_rp, a_ci};
-    D.AT = DevCsr<T>{n, m, A.nnz, alloc<T>(A.nnz), at_rp, at_ci};
+    D.A = DevCsr<T>{m, n, annz, alloc<T>(annz), a_rp, a_ci};
+    D.AT = DevCsr<T>{n, m, annz, alloc<T>(annz), at_rp, at_ci};
     CK(cudaMemcpyAsync(D.P.val, Pfull.val, sizeof(T) * Pfull.nnz, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(D.A.val, a_v, sizeof(T) * A.nnz, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(D.AT.val, ato_v, sizeof(T) * A.nnz, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(D.A.val, a_v, sizeof(T) * annz, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(D.AT.val, ato_v, sizeof(T) * annz, cudaMemcpyDeviceToDevice, s));
     D.q = vec(n, false);
     CK(cudaMemcpyAsync(D.q, D.q_o, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
     D.d = vec(n, false);
@@ -281,16 +411,77 @@ class Workspace {
     D.u = vec(m, false);
     fill(D.d, n, T(1));
     fill(D.e, m, T(1));
-    uint32_t passes = 0;
-    T deviation = T(0);
-    T c = T(1);
+    const T c = T(1);
     CK(cudaMemcpyAsync(ruiz_scal + 3, &c, sizeof(T), cudaMemcpyHostToDevice, s));
-    if (st.scaling_enabled) {
-      ruiz(st, passes, deviation);
-      c = read_scalar(ruiz_scal + 3);
-    }
-    // scaling.hpp:166-176: a_t re-derived from the scaled a; reciprocals; l, u
-    if (st.scaling_enabled) gather_values(D.A.val, permA, A.nnz, D.AT.val, s);
+    CK(cudaStreamSynchronize(s));
+  }
+
+  // modified Ruiz equilibration (scaling.hpp:92-187), bit-exact, one pass per
+  // ruiz_norms / ruiz_delta / ruiz_scale; ruiz_scal[4] = the pass deviation.
+  // Row blocks combine rz_atn (max) and the deviation (max) in between: both
+  // maxima are order-free, so the sharded scaling is bit-identical too.
+  void ruiz_prepare() {
+    const uint32_t n = D.n, m = D.m;
+    rz_dx = vec(n, false);
+    rz_dz = vec(m, false);
+    rz_pn = vec(n, false);
+    rz_atn = vec(n, false);
+    rz_an = vec(m, false);
+    // rows of P_full with entries, for the ordered mean (structure is fixed)
+    uint32_t* flags = alloc<uint32_t>(n + 1);
+    uint32_t* pos = alloc<uint32_t>(n + 1);
+    p_rows = alloc<uint32_t>(n + 1);
+    nonempty_flags_kernel<<<grid_for(n), kThreads, 0, s>>>(D.P.rp, n, flags);
+    CK_LAUNCH();
+    exclusive_scan_u32(flags, pos, n, tmp, s);
+    n_prows = scan_total(flags, pos, n, s);
+    compact_kernel<<<grid_for(n), kThreads, 0, s>>>(flags, pos, n, p_rows);
+    CK_LAUNCH();
+  }
+  void ruiz_norms() {
+    row_inf_norms(D.P, D.pP, rz_pn, s);
+    if (D.m == 0 || D.AT.nnz == 0)  // empty block: no column contributes
+      CK(cudaMemsetAsync(rz_atn, 0, sizeof(T) * D.n, s));
+    else
+      row_inf_norms(D.AT, D.pAT, rz_atn, s);
+    row_inf_norms(D.A, D.pA, rz_an, s);
+  }
+  void ruiz_delta() {
+    const uint32_t n = D.n, m = D.m;
+    k_ruiz_delta<T><<<red_grid<T>(std::max(n, m)), kThreads, 0, s>>>(
+        rz_pn, rz_atn, n, rz_an, m, rz_dx, rz_dz, D.d, D.e, D.q, D.red, &D.ctl->red_counter,
+        ruiz_scal + 4);
+    CK_LAUNCH();
+  }
+  void ruiz_scale() {
+    const uint32_t n = D.n;
+    plan_visit(D.P, D.pP, ScaleRowColFn<T>{D.P.val, D.P.ci, rz_dx, rz_dx}, s);
+    plan_visit(D.A, D.pA, ScaleRowColFn<T>{D.A.val, D.A.ci, rz_dz, rz_dx}, s);
+    plan_visit(D.AT, D.pAT, ScaleRowColFn<T>{D.AT.val, D.AT.ci, rz_dx, rz_dz}, s);
+    // cost scaling
+    T* mean = ruiz_scal + 0;
+    T* qinf = ruiz_scal + 1;
+    T* gamma = ruiz_scal + 2;
+    T* cc = ruiz_scal + 3;
+    row_inf_norms(D.P, D.pP, rz_pn, s);
+    ordered_mean_kernel<T><<<1, 256, 0, s>>>(rz_pn, p_rows, n_prows, n, mean);
+    CK_LAUNCH();
+    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q, n, D.red, &D.ctl->red_counter, qinf);
+    CK_LAUNCH();
+    k_ruiz_gamma<T><<<1, 1, 0, s>>>(mean, qinf, gamma, cc);
+    CK_LAUNCH();
+    k_scale_by<T><<<grid_for(D.P.nnz), kThreads, 0, s>>>(D.P.val, D.P.nnz, gamma);
+    k_scale_by<T><<<grid_for(n), kThreads, 0, s>>>(D.q, n, gamma);
+    CK_LAUNCH();
+  }
+
+  // scaling.hpp:166-176 (A^T re-derived from the scaled A, reciprocals, l, u),
+  // q_inf_scaled, diag(P)
+  void finish_scaling(uint32_t passes, T deviation) {
+    const uint32_t n = D.n, m = D.m;
+    equil_passes = passes;
+    equil_residual = deviation;
+    if (set.scaling_enabled) gather_values(D.A.val, permA, D.A.nnz, D.AT.val, s);
     {
       T *d = D.d, *e = D.e, *di = D.d_inv, *ei = D.e_inv, *lo = D.l_o, *uo = D.u_o, *ls = D.l,
         *us = D.u;
@@ -301,7 +492,7 @@ class Workspace {
         us[j] = e[j] * uo[j];
       }, s);
     }
-    if (!st.scaling_enabled) {  // identity_scaled_problem (scaling.hpp:190-205): l, u copied
+    if (!set.scaling_enabled) {  // identity_scaled_problem (scaling.hpp:190-205): l, u copied
       CK(cudaMemcpyAsync(D.l, D.l_o, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
       CK(cudaMemcpyAsync(D.u, D.u_o, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
     }
@@ -315,9 +506,11 @@ class Workspace {
     D.dinv = vec(n, false);
     extract_diag_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.P, D.diag_p);
     CK_LAUNCH();
-    diag_ata_kernel<T><<<grid_for(uint64_t(n) * 32), kThreads, 0, s>>>(D.AT, D.diag_ata);
-    CK_LAUNCH();
-    // ---- state and workspace vectors
+  }
+
+  // state and workspace vectors, the control block, the Jacobi diagonal
+  void finish_setup() {
+    const uint32_t n = D.n, m = D.m;
     D.x = vec(n); D.xt = vec(n); D.dx = vec(n); D.b = vec(n); D.r = vec(n); D.p = vec(n);
     D.kp = vec(n); D.best = vec(n); D.px = vec(n); D.aty = vec(n); D.rdual = vec(n);
     D.xo = vec(n); D.pxo = vec(n);
@@ -326,7 +519,11 @@ class Workspace {
     D.cert = vec(std::max(n, m));
     D.g2m = alloc<pair_t<T>>(m);
     D.g2n = alloc<pair_t<T>>(n);
-    const uint32_t cap = op.record_diagnostics ? st.max_admm_iter : 0u;
+    if (D.split) {
+      D.part = vec(2 * size_t(n));
+      D.shsc = vec(kShScal);
+    }
+    const uint32_t cap = opt.record_diagnostics ? set.max_admm_iter : 0u;
     D.calls = alloc<DiagRec<T>>(cap);
     D.checks = alloc<uint32_t>(cap);
     D.rhos = alloc<RhoRec<T>>(cap);
@@ -334,6 +531,7 @@ class Workspace {
     T hs[8];
     CK(cudaMemcpyAsync(hs, ruiz_scal, sizeof(T) * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    const qpcg_settings& st = set;
     std::memset(&hc, 0, sizeof(hc));
     hc.alpha = T(st.alpha);
     hc.sigma = T(st.sigma);
@@ -347,6 +545,7 @@ class Workspace {
     hc.check_interval = st.check_interval;
     hc.rho_interval = st.rho_update_interval;
     hc.pcg_cap = pcg_cap(n);
+    const T c = hs[3];
     hc.c = c;
     hc.c_inv = T(1) / c;
     hc.q_inf_orig = hs[5];
@@ -354,22 +553,10 @@ class Workspace {
     hc.rho = T(st.rho_bar_init);
     hc.status = QPCG_STATUS_MAX_ITER_REACHED;
     hc.diag_cap = cap;
-    equil_passes = passes;
-    equil_residual = deviation;
     push_ctl();
     k_precond<T><<<grid_for(n), kThreads, 0, s>>>(D, 1);
     CK_LAUNCH();
-    CK(cudaEventRecord(ev1, s));
-    CK(cudaEventSynchronize(ev1));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, ev0, ev1));
-    setup_seconds = ms * 1e-3;
-    setup_wall = now_s() - w0;
-    setup_launches = g_launches - l0;
   }
-
-  uint32_t equil_passes = 0;
-  T equil_residual = T(0);
 
   static uint32_t pcg_cap(uint32_t n) {  // solver.hpp:330-334, evaluated in T
     const uint32_t by_dim = (uint32_t)std::ceil(T(20) * std::sqrt(static_cast<T>(n)));
@@ -392,102 +579,6 @@ class Workspace {
     if (!(T(s.eps_pcg_min) > T(0))) bad("settings: eps_pcg_min must be positive");
     if (!(T(s.eps_equil) > T(0)) || s.equil_max_passes < 1)
       bad("settings: bad equilibration parameters");
-  }
-
-  void validate_problem(const HostCsr<T>& Pu, const HostCsr<T>& A, const uint32_t* pu_rp,
-                        const uint32_t* pu_ci, const T* pu_v, const uint32_t* a_rp,
-                        const uint32_t* a_ci, const T* a_v, bool p_square, bool a_cols_ok) {
-    const uint32_t n = Pu.rows, m = A.rows;
-    uint32_t ends[4];
-    CK(cudaMemcpyAsync(ends + 0, pu_rp, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(ends + 1, pu_rp + n, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(ends + 2, a_rp, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(ends + 3, a_rp + m, 4, cudaMemcpyDeviceToHost, s));
-    unsigned long long* key = alloc<unsigned long long>(1);
-    CK(cudaMemsetAsync(key, 0xff, 8, s));
-    CK(cudaStreamSynchronize(s));
-    if (ends[0] != 0 || ends[1] != Pu.nnz)
-      throw InvalidArgument("csr: row_ptr must start at 0 and end at nnz");
-    validate_csr_rows_kernel<<<grid_for(n), kThreads, 0, s>>>(pu_rp, pu_ci, n, Pu.cols, kValPRowPtr,
-                                                             p_square ? 1 : 0, key);
-    CK_LAUNCH();
-    unsigned long long k = 0;
-    CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if ((k >> 56) == kValPRowPtr) throw InvalidArgument(validation_message(k));
-    if (ends[2] != 0 || ends[3] != A.nnz)
-      throw InvalidArgument("csr: row_ptr must start at 0 and end at nnz");
-    validate_csr_rows_kernel<<<grid_for(m), kThreads, 0, s>>>(a_rp, a_ci, m, A.cols, kValARowPtr, 0,
-                                                             key);
-    CK_LAUNCH();
-    CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if ((k >> 56) == kValARowPtr) throw InvalidArgument(validation_message(k));
-    if (!p_square) throw InvalidArgument("problem: P must be square");
-    if (n == 0) throw InvalidArgument("problem: at least one variable required");
-    if ((k >> 56) == kValPBelow) throw InvalidArgument(validation_message(k));
-    if (!a_cols_ok) throw InvalidArgument("problem: A column count must equal n");
-    validate_values_kernel<T><<<grid_for(Pu.nnz), kThreads, 0, s>>>(pu_v, Pu.nnz, kValPFinite, key);
-    validate_values_kernel<T><<<grid_for(A.nnz), kThreads, 0, s>>>(a_v, A.nnz, kValAFinite, key);
-    validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.q_o, n, kValQFinite, key);
-    validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(D.l_o, D.u_o, m, key);
-    CK_LAUNCH();
-    CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (k != ~0ull) throw InvalidArgument(validation_message(k));
-  }
-
-  // modified Ruiz equilibration (scaling.hpp:92-187), bit-exact
-  void ruiz(const qpcg_settings& st, uint32_t& passes, T& deviation) {
-    const uint32_t n = D.n, m = D.m;
-    T* dx = vec(n, false);
-    T* dz = vec(m, false);
-    T* pn = vec(n, false);
-    T* atn = vec(n, false);
-    T* an = vec(m, false);
-    deviation = T(1);
-    passes = 0;
-    const T eps = T(st.eps_equil);
-    {  // rows of P_full with entries, for the ordered mean (structure is fixed)
-      uint32_t* flags = alloc<uint32_t>(n + 1);
-      uint32_t* pos = alloc<uint32_t>(n + 1);
-      p_rows = alloc<uint32_t>(n + 1);
-      nonempty_flags_kernel<<<grid_for(n), kThreads, 0, s>>>(D.P.rp, n, flags);
-      CK_LAUNCH();
-      exclusive_scan_u32(flags, pos, n, tmp, s);
-      n_prows = scan_total(flags, pos, n, s);
-      compact_kernel<<<grid_for(n), kThreads, 0, s>>>(flags, pos, n, p_rows);
-      CK_LAUNCH();
-    }
-    T* mean = ruiz_scal + 0;
-    T* qinf = ruiz_scal + 1;
-    T* gamma = ruiz_scal + 2;
-    T* cc = ruiz_scal + 3;
-    T* dev = ruiz_scal + 4;
-    while (passes < st.equil_max_passes && deviation > eps) {
-      ++passes;
-      row_inf_norms(D.P, D.pP, pn, s);
-      row_inf_norms(D.AT, D.pAT, atn, s);
-      row_inf_norms(D.A, D.pA, an, s);
-      k_ruiz_delta<T><<<red_grid<T>(std::max(n, m)), kThreads, 0, s>>>(
-          pn, atn, n, an, m, dx, dz, D.d, D.e, D.q, D.red, &D.ctl->red_counter, dev);
-      CK_LAUNCH();
-      plan_visit(D.P, D.pP, ScaleRowColFn<T>{D.P.val, D.P.ci, dx, dx}, s);
-      plan_visit(D.A, D.pA, ScaleRowColFn<T>{D.A.val, D.A.ci, dz, dx}, s);
-      plan_visit(D.AT, D.pAT, ScaleRowColFn<T>{D.AT.val, D.AT.ci, dx, dz}, s);
-      // cost scaling
-      row_inf_norms(D.P, D.pP, pn, s);
-      ordered_mean_kernel<T><<<1, 256, 0, s>>>(pn, p_rows, n_prows, n, mean);
-      CK_LAUNCH();
-      k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q, n, D.red, &D.ctl->red_counter, qinf);
-      CK_LAUNCH();
-      k_ruiz_gamma<T><<<1, 1, 0, s>>>(mean, qinf, gamma, cc);
-      CK_LAUNCH();
-      k_scale_by<T><<<grid_for(D.P.nnz), kThreads, 0, s>>>(D.P.val, D.P.nnz, gamma);
-      k_scale_by<T><<<grid_for(n), kThreads, 0, s>>>(D.q, n, gamma);
-      CK_LAUNCH();
-      deviation = read_scalar(dev);
-    }
   }
 
   // ------------------------------------------------------ enqueue helpers
@@ -652,12 +743,8 @@ class Workspace {
   }
 
   // ------------------------------------------------------------ solve
-  void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) {
-    CK(cudaSetDevice(device));
-    AllocScope scope(s);
-    const double w0 = now_s();
-    CK(cudaEventRecord(ev0, s));
-    // reset the per-solve state (solver.hpp:412, :430-443)
+  // reset the per-solve state (solver.hpp:412, :430-443)
+  void reset_solve_state() {
     pull_ctl();
     hc.iter = 0;
     hc.done = 0;
@@ -671,6 +758,48 @@ class Workspace {
     hc.n_inf = 0;
     hc.n_rho_branch = 0;
     push_ctl();
+  }
+  void raise_device_error() {
+    if (hc.error == kErrNotPD)
+      throw NotPositiveDefinite("pcg: encountered direction of nonpositive curvature");
+    if (hc.error == kErrInvalid) {
+      if (hc.n_rho > 0 && !(hc.rho > T(0))) throw InvalidArgument("kkt operator: rho must be positive");
+      throw InvalidArgument("pcg: warm start must be finite");
+    }
+  }
+  void fill_info(qpcg_info* info, double solve_s, double d2h, uint32_t n, uint32_t m) const {
+    const bool has_cert = hc.status == 1 || hc.status == 2;
+    std::memset(info, 0, sizeof(*info));
+    info->status = int32_t(hc.status);
+    info->iterations = hc.iter;
+    info->pcg_iterations_total = hc.pcg_total;
+    info->objective = double(hc.objective);
+    info->r_prim_inf = double(hc.rp_o);
+    info->r_dual_inf = double(hc.rd_o);
+    info->equil_passes = equil_passes;
+    info->rho_update_count = hc.rho_update_count;
+    info->equil_residual = double(equil_residual);
+    info->rho_final = double(hc.rho);
+    info->certificate_valid = has_cert;
+    info->n = n;
+    info->m = m;
+    info->setup_seconds = setup_seconds;
+    info->solve_seconds = solve_s;
+    info->h2d_seconds = h2d_seconds;
+    info->d2h_seconds = opt.input_memory == QPCG_MEM_HOST ? d2h : 0.0;
+    info->h2d_bytes = h2d_bytes;
+    info->d2h_bytes = opt.input_memory == QPCG_MEM_HOST
+                          ? sizeof(T) * (uint64_t(n) + 2ull * m) +
+                                (has_cert ? sizeof(T) * (hc.status == 1 ? m : n) : 0)
+                          : 0;
+  }
+
+  void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) {
+    CK(cudaSetDevice(device));
+    AllocScope scope(s);
+    const double w0 = now_s();
+    CK(cudaEventRecord(ev0, s));
+    reset_solve_state();
     uint64_t graph_build = 0;
     const uint64_t l0 = g_launches;
     // initial residuals and PCG tolerance (solver.hpp:436-441)
@@ -686,12 +815,7 @@ class Workspace {
       CK(cudaGraphLaunch(exec, s));
     }
     pull_ctl();
-    if (hc.error == kErrNotPD)
-      throw NotPositiveDefinite("pcg: encountered direction of nonpositive curvature");
-    if (hc.error == kErrInvalid) {
-      if (hc.n_rho > 0 && !(hc.rho > T(0))) throw InvalidArgument("kkt operator: rho must be positive");
-      throw InvalidArgument("pcg: warm start must be finite");
-    }
+    raise_device_error();
     if (!hc.residuals_current) enq_residuals_fresh(2);
     k_unscale<T><<<grid_for(std::max(D.n, D.m)), kThreads, 0, s>>>(D);
     CK_LAUNCH();
@@ -717,29 +841,7 @@ class Workspace {
     const double d2h = now_s() - td;
     have_solved = true;
     if (info) {
-      std::memset(info, 0, sizeof(*info));
-      info->status = int32_t(hc.status);
-      info->iterations = hc.iter;
-      info->pcg_iterations_total = hc.pcg_total;
-      info->objective = double(hc.objective);
-      info->r_prim_inf = double(hc.rp_o);
-      info->r_dual_inf = double(hc.rd_o);
-      info->equil_passes = equil_passes;
-      info->rho_update_count = hc.rho_update_count;
-      info->equil_residual = double(equil_residual);
-      info->rho_final = double(hc.rho);
-      info->certificate_valid = has_cert;
-      info->n = D.n;
-      info->m = D.m;
-      info->setup_seconds = setup_seconds;
-      info->solve_seconds = ms * 1e-3;
-      info->h2d_seconds = h2d_seconds;
-      info->d2h_seconds = opt.input_memory == QPCG_MEM_HOST ? d2h : 0.0;
-      info->h2d_bytes = h2d_bytes;
-      info->d2h_bytes = opt.input_memory == QPCG_MEM_HOST
-                            ? sizeof(T) * (uint64_t(D.n) + 2ull * D.m) +
-                                  (has_cert ? sizeof(T) * (hc.status == 1 ? D.m : D.n) : 0)
-                            : 0;
+      fill_info(info, ms * 1e-3, d2h, D.n, D.m);
       info->runtime_seconds = now_s() - w0;
       info->kernel_launches = launches + (have_counted_setup ? 0 : setup_launches);
     }
@@ -750,24 +852,36 @@ class Workspace {
   void warm_start(const T* x, const T* z, const T* y) {  // solver.hpp:413-428
     CK(cudaSetDevice(device));
     AllocScope scope(s);
+    if (warm_stage(x, z, y) != ~0ull) throw InvalidArgument("solve: warm start must be finite");
+    warm_apply();
+  }
+  // upload + finiteness key (~0 = all finite); the sharded path combines the
+  // keys of its row blocks before anyone throws
+  T *w_tx = nullptr, *w_tz = nullptr, *w_ty = nullptr;
+  unsigned long long warm_stage(const T* x, const T* z, const T* y) {
     const uint32_t n = D.n, m = D.m;
-    T* tx = vec(n, false);
-    T* tz = vec(m, false);
-    T* ty = vec(m, false);
-    upload(tx, x, sizeof(T) * n);
-    upload(tz, z, sizeof(T) * m);
-    upload(ty, y, sizeof(T) * m);
+    w_tx = vec(n, false);
+    w_tz = vec(m, false);
+    w_ty = vec(m, false);
+    upload(w_tx, x, sizeof(T) * n);
+    upload(w_tz, z, sizeof(T) * m);
+    upload(w_ty, y, sizeof(T) * m);
     unsigned long long* key = alloc<unsigned long long>(1);
     CK(cudaMemsetAsync(key, 0xff, 8, s));
-    validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(tx, n, 1, key);
-    validate_values_kernel<T><<<grid_for(m), kThreads, 0, s>>>(tz, m, 1, key);
-    validate_values_kernel<T><<<grid_for(m), kThreads, 0, s>>>(ty, m, 1, key);
+    validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(w_tx, n, 1, key);
+    validate_values_kernel<T><<<grid_for(m), kThreads, 0, s>>>(w_tz, m, 1, key);
+    validate_values_kernel<T><<<grid_for(m), kThreads, 0, s>>>(w_ty, m, 1, key);
+    CK_LAUNCH();
     unsigned long long k;
     CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (k != ~0ull) throw InvalidArgument("solve: warm start must be finite");
+    return k;
+  }
+  void warm_apply() {
+    const uint32_t n = D.n, m = D.m;
     const T c = hc.c;
     T *X = D.x, *XT = D.xt, *Z = D.z, *Y = D.y, *di = D.d_inv, *e = D.e, *ei = D.e_inv;
+    const T *tx = w_tx, *tz = w_tz, *ty = w_ty;
     for_n(n, [=] __device__(uint32_t i) {
       const T v = di[i] * tx[i];
       X[i] = v;
@@ -900,6 +1014,11 @@ class Workspace {
   void update_vectors(const T* q, const T* l, const T* u) {
     CK(cudaSetDevice(device));
     AllocScope scope(s);
+    const unsigned long long k = vectors_stage(q, l, u);
+    if (k != ~0ull) throw InvalidArgument(validation_message(k));
+    vectors_apply();
+  }
+  unsigned long long vectors_stage(const T* q, const T* l, const T* u) {
     const uint32_t n = D.n, m = D.m;
     if (q) upload(D.q_o, q, sizeof(T) * n);
     if (l) upload(D.l_o, l, sizeof(T) * m);
@@ -907,11 +1026,15 @@ class Workspace {
     unsigned long long* key = alloc<unsigned long long>(1);
     CK(cudaMemsetAsync(key, 0xff, 8, s));
     validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.q_o, n, kValQFinite, key);
-    validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(D.l_o, D.u_o, m, key);
+    validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(D.l_o, D.u_o, m, key, row0);
+    CK_LAUNCH();
     unsigned long long k;
     CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (k != ~0ull) throw InvalidArgument(validation_message(k));
+    return k;
+  }
+  void vectors_apply() {
+    const uint32_t n = D.n, m = D.m;
     const T c = hc.c;
     T *qs = D.q, *qo = D.q_o, *d = D.d, *e = D.e, *ls = D.l, *us = D.u, *lo = D.l_o, *uo = D.u_o;
     for_n(n, [=] __device__(uint32_t i) { qs[i] = c * (d[i] * qo[i]); }, s);
@@ -931,6 +1054,8 @@ class Workspace {
 
 }  // namespace qpcg_b200
 
+#include "shard.cuh"
+
 // =====================================================================
 // C-ABI
 // =====================================================================
@@ -940,6 +1065,8 @@ struct qpcg_workspace {
   int precision = 64;
   std::unique_ptr<Workspace<double>> w64;
   std::unique_ptr<Workspace<float>> w32;
+  std::unique_ptr<Sharded<double>> s64;  // row-sharded (options.virtual_shards / nccl)
+  std::unique_ptr<Sharded<float>> s32;
   std::string err;
 };
 
@@ -965,6 +1092,9 @@ int guarded(qpcg_workspace* ws, F&& f) {
   } catch (const CudaError& e) {
     *msg = e.what();
     return QPCG_ERR_CUDA;
+  } catch (const NcclError& e) {
+    *msg = e.what();
+    return QPCG_ERR_NCCL;
   } catch (const std::exception& e) {
     *msg = e.what();
     return QPCG_ERR_RUNTIME;
@@ -982,6 +1112,14 @@ template <>
 std::unique_ptr<Workspace<double>>& slot<double>(qpcg_workspace* ws) { return ws->w64; }
 template <>
 std::unique_ptr<Workspace<float>>& slot<float>(qpcg_workspace* ws) { return ws->w32; }
+template <typename T>
+std::unique_ptr<Sharded<T>>& sslot(qpcg_workspace* ws);
+template <>
+std::unique_ptr<Sharded<double>>& sslot<double>(qpcg_workspace* ws) { return ws->s64; }
+template <>
+std::unique_ptr<Sharded<float>>& sslot<float>(qpcg_workspace* ws) { return ws->s32; }
+
+bool is_sharded(const qpcg_options& o) { return o.virtual_shards > 1 || o.nccl_id != nullptr; }
 
 template <typename T, typename CsrT>
 int setup_impl(qpcg_workspace** out, const CsrT* p, const T* q, const CsrT* a, const T* l,
@@ -1000,8 +1138,13 @@ int setup_impl(qpcg_workspace** out, const CsrT* p, const T* q, const CsrT* a, c
   qpcg_default_options(&op);
   if (o) op = *o;
   const int rc = guarded(ws, [&] {
-    slot<T>(ws).reset(new Workspace<T>());
-    slot<T>(ws)->setup(host_csr<T>(p), q, host_csr<T>(a), l, u, st, op);
+    if (is_sharded(op)) {
+      sslot<T>(ws).reset(new Sharded<T>());
+      sslot<T>(ws)->setup(host_csr<T>(p), q, host_csr<T>(a), l, u, st, op);
+    } else {
+      slot<T>(ws).reset(new Workspace<T>());
+      slot<T>(ws)->setup(host_csr<T>(p), q, host_csr<T>(a), l, u, st, op);
+    }
   });
   if (rc != QPCG_OK) {
     g_last_error = ws->err;
@@ -1018,6 +1161,19 @@ Workspace<T>* get(qpcg_workspace* ws) {
   if (ws == nullptr || !slot<T>(ws)) throw InvalidArgument("workspace: wrong precision or null");
   return slot<T>(ws).get();
 }
+// f(engine) on the workspace's single-device or sharded engine
+template <typename T, typename F>
+void run(qpcg_workspace* ws, F&& f) {
+  if (ws != nullptr && sslot<T>(ws)) return f(*sslot<T>(ws));
+  f(*get<T>(ws));
+}
+// the block whose control block and diagnostics speak for the solve
+template <typename T>
+Workspace<T>* primary(const qpcg_workspace* w) {
+  auto* ws = const_cast<qpcg_workspace*>(w);
+  if (sslot<T>(ws)) return &sslot<T>(ws)->w0();
+  return slot<T>(ws).get();
+}
 
 template <typename T, typename CsrT>
 int solve_problem_impl(const CsrT* p, const T* q, const CsrT* a, const T* l, const T* u,
@@ -1028,8 +1184,9 @@ int solve_problem_impl(const CsrT* p, const T* q, const CsrT* a, const T* l, con
   qpcg_workspace* ws = nullptr;
   int rc = setup_impl<T>(&ws, p, q, a, l, u, s, o);
   if (rc == QPCG_OK && wx != nullptr)
-    rc = guarded(ws, [&] { get<T>(ws)->warm_start(wx, wz, wy); });
-  if (rc == QPCG_OK) rc = guarded(ws, [&] { get<T>(ws)->solve(info, x, z, y, cert); });
+    rc = guarded(ws, [&] { run<T>(ws, [&](auto& w) { w.warm_start(wx, wz, wy); }); });
+  if (rc == QPCG_OK)
+    rc = guarded(ws, [&] { run<T>(ws, [&](auto& w) { w.solve(info, x, z, y, cert); }); });
   if (rc == QPCG_OK && info) info->runtime_seconds = now_s() - t0;  // solver.hpp:392 -> :537
   if (rc != QPCG_OK && msg && msg_len) {
     const std::string& e = ws ? ws->err : g_last_error;
@@ -1134,30 +1291,30 @@ int qpcg_f32_setup(qpcg_workspace** ws, const qpcg_csr_f32* p, const float* q,
   return setup_impl<float>(ws, p, q, a, l, u, s, o);
 }
 int qpcg_f64_warm_start(qpcg_workspace* ws, const double* x, const double* z, const double* y) {
-  return guarded(ws, [&] { get<double>(ws)->warm_start(x, z, y); });
+  return guarded(ws, [&] { run<double>(ws, [&](auto& w) { w.warm_start(x, z, y); }); });
 }
 int qpcg_f32_warm_start(qpcg_workspace* ws, const float* x, const float* z, const float* y) {
-  return guarded(ws, [&] { get<float>(ws)->warm_start(x, z, y); });
+  return guarded(ws, [&] { run<float>(ws, [&](auto& w) { w.warm_start(x, z, y); }); });
 }
 int qpcg_f64_update_rho(qpcg_workspace* ws, double rho) {
-  return guarded(ws, [&] { get<double>(ws)->update_rho(rho); });
+  return guarded(ws, [&] { run<double>(ws, [&](auto& w) { w.update_rho(rho); }); });
 }
 int qpcg_f32_update_rho(qpcg_workspace* ws, double rho) {
-  return guarded(ws, [&] { get<float>(ws)->update_rho(float(rho)); });
+  return guarded(ws, [&] { run<float>(ws, [&](auto& w) { w.update_rho(float(rho)); }); });
 }
 int qpcg_f64_update_vectors(qpcg_workspace* ws, const double* q, const double* l, const double* u) {
-  return guarded(ws, [&] { get<double>(ws)->update_vectors(q, l, u); });
+  return guarded(ws, [&] { run<double>(ws, [&](auto& w) { w.update_vectors(q, l, u); }); });
 }
 int qpcg_f32_update_vectors(qpcg_workspace* ws, const float* q, const float* l, const float* u) {
-  return guarded(ws, [&] { get<float>(ws)->update_vectors(q, l, u); });
+  return guarded(ws, [&] { run<float>(ws, [&](auto& w) { w.update_vectors(q, l, u); }); });
 }
 int qpcg_f64_solve(qpcg_workspace* ws, qpcg_info* info, double* x, double* z, double* y,
                    double* cert) {
-  return guarded(ws, [&] { get<double>(ws)->solve(info, x, z, y, cert); });
+  return guarded(ws, [&] { run<double>(ws, [&](auto& w) { w.solve(info, x, z, y, cert); }); });
 }
 int qpcg_f32_solve(qpcg_workspace* ws, qpcg_info* info, float* x, float* z, float* y,
                    float* cert) {
-  return guarded(ws, [&] { get<float>(ws)->solve(info, x, z, y, cert); });
+  return guarded(ws, [&] { run<float>(ws, [&](auto& w) { w.solve(info, x, z, y, cert); }); });
 }
 int qpcg_f64_solve_problem(const qpcg_csr_f64* p, const double* q, const qpcg_csr_f64* a,
                            const double* l, const double* u, const qpcg_settings* s,
@@ -1176,25 +1333,43 @@ int qpcg_f32_solve_problem(const qpcg_csr_f32* p, const float* q, const qpcg_csr
                                    msg_len);
 }
 void qpcg_cleanup(qpcg_workspace* ws) { delete ws; }
+
+int qpcg_shard_cuts(const uint32_t* row_ptr, uint32_t rows, uint32_t nnz, uint32_t blocks,
+                    uint32_t* cuts) {
+  if (row_ptr == nullptr || cuts == nullptr || blocks == 0) return 0;
+  return shard_cuts(row_ptr, rows, nnz, blocks, cuts) ? 1 : 0;
+}
+
+int qpcg_nccl_unique_id(void* out) {
+  return guarded(nullptr, [&] {
+    if (out == nullptr) throw InvalidArgument("nccl: null id buffer");
+    ncclUniqueId id;
+    nccl_check(nccl_api().GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == QPCG_NCCL_ID_BYTES, "ncclUniqueId size");
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
 const char* qpcg_last_error(const qpcg_workspace* ws) {
   return ws ? ws->err.c_str() : g_last_error.c_str();
 }
 
 uint32_t qpcg_get_pcg_calls(const qpcg_workspace* ws, qpcg_pcg_call* out, uint32_t cap) {
-  auto* w = const_cast<qpcg_workspace*>(ws);
-  if (!w) return 0;
-  return w->w64 ? calls_of(w->w64.get(), out, cap) : w->w32 ? calls_of(w->w32.get(), out, cap) : 0;
+  if (!ws) return 0;
+  if (Workspace<double>* w = primary<double>(ws)) return calls_of(w, out, cap);
+  if (Workspace<float>* w = primary<float>(ws)) return calls_of(w, out, cap);
+  return 0;
 }
 uint32_t qpcg_get_rho_updates(const qpcg_workspace* ws, qpcg_rho_update* out, uint32_t cap) {
-  auto* w = const_cast<qpcg_workspace*>(ws);
-  if (!w) return 0;
-  return w->w64 ? rhos_of(w->w64.get(), out, cap) : w->w32 ? rhos_of(w->w32.get(), out, cap) : 0;
+  if (!ws) return 0;
+  if (Workspace<double>* w = primary<double>(ws)) return rhos_of(w, out, cap);
+  if (Workspace<float>* w = primary<float>(ws)) return rhos_of(w, out, cap);
+  return 0;
 }
 uint32_t qpcg_get_check_iterations(const qpcg_workspace* ws, uint32_t* out, uint32_t cap) {
-  auto* w = const_cast<qpcg_workspace*>(ws);
-  if (!w) return 0;
-  return w->w64 ? checks_of(w->w64.get(), out, cap)
-                : w->w32 ? checks_of(w->w32.get(), out, cap) : 0;
+  if (!ws) return 0;
+  if (Workspace<double>* w = primary<double>(ws)) return checks_of(w, out, cap);
+  if (Workspace<float>* w = primary<float>(ws)) return checks_of(w, out, cap);
+  return 0;
 }
 
 int qpcg_debug_dims(const qpcg_workspace* ws, uint64_t* dims) {

@@ -91,30 +91,32 @@ __device__ __forceinline__ void val_report(unsigned long long* key, uint32_t cat
 
 // sparse.hpp:110-123 per-row checks; pos 0 = nondecreasing, 2j+1 = bound of
 // j-th entry, 2j+2 = ordering of j-th entry
+// (off: global index of element 0 — a row block of A reports global rows, so
+// the minimum over blocks is the unsharded first error)
 __global__ void validate_csr_rows_kernel(const uint32_t* rp, const uint32_t* ci, uint32_t rows,
                                          uint32_t cols, uint32_t cat, int check_upper,
-                                         unsigned long long* key) {
+                                         unsigned long long* key, uint32_t off = 0) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
     const uint32_t b = rp[r], e = rp[r + 1];
     if (e < b) {
-      val_report(key, cat, r, 0);
+      val_report(key, cat, r + off, 0);
       continue;
     }
     for (uint32_t k = b; k < e; ++k) {
       const uint32_t j = k - b;
       if (ci[k] >= cols) {
-        val_report(key, cat, r, 2 * j + 1);
+        val_report(key, cat, r + off, 2 * j + 1);
         break;
       }
       if (k > b && ci[k] <= ci[k - 1]) {
-        val_report(key, cat, r, 2 * j + 2);
+        val_report(key, cat, r + off, 2 * j + 2);
         break;
       }
     }
     if (check_upper) {
       for (uint32_t k = b; k < e; ++k)
         if (ci[k] < r) {
-          val_report(key, kValPBelow, r, k - b);
+          val_report(key, kValPBelow, r + off, k - b);
           break;
         }
     }
@@ -123,22 +125,23 @@ __global__ void validate_csr_rows_kernel(const uint32_t* rp, const uint32_t* ci,
 
 template <typename T>
 __global__ void validate_values_kernel(const T* v, uint32_t n, uint32_t cat,
-                                       unsigned long long* key) {
+                                       unsigned long long* key, uint32_t off = 0) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    if (!isfinite(v[i])) val_report(key, cat, i, 0);
+    if (!isfinite(v[i])) val_report(key, cat, i + off, 0);
 }
 
 // problem.hpp:86-91 per bound: NaN (pos 0), inf-side (pos 1), l > u (pos 2)
 template <typename T>
-__global__ void validate_bounds_kernel(const T* l, const T* u, uint32_t m, unsigned long long* key) {
+__global__ void validate_bounds_kernel(const T* l, const T* u, uint32_t m, unsigned long long* key,
+                                       uint32_t off = 0) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     const T li = l[i], ui = u[i];
     if (isnan(li) || isnan(ui))
-      val_report(key, kValBounds, i, 0);
+      val_report(key, kValBounds, i + off, 0);
     else if (li == (T)INFINITY || ui == -(T)INFINITY)
-      val_report(key, kValBounds, i, 1);
+      val_report(key, kValBounds, i + off, 1);
     else if (li > ui)
-      val_report(key, kValBounds, i, 2);
+      val_report(key, kValBounds, i + off, 2);
   }
 }
 
@@ -298,13 +301,15 @@ void row_inf_norms(const DevCsr<T>& M, const SpmvPlan<T>& P, T* out, cudaStream_
 }
 
 // diag_ata: warp per A^T row, sequential sum of squares in stored order.
+// init (nullable): running sums carried in from the row blocks above (the
+// sharded chain); out may alias init.
 template <typename T>
-__global__ void diag_ata_kernel(DevCsr<T> AT, T* out) {
+__global__ void diag_ata_kernel(DevCsr<T> AT, T* out, const T* init) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < AT.rows; r += nwarps) {
     const uint32_t b = AT.rp[r], e = AT.rp[r + 1];
-    T s = T(0);
+    T s = init ? init[r] : T(0);
     for (uint32_t k0 = b; k0 < e; k0 += 32) {
       const uint32_t k = k0 + lane;
       const T v = k < e ? AT.val[k] : T(0);

@@ -1,0 +1,435 @@
+// shard.cuh — the row-sharded solve: A cut into G
+// contiguous nnz-balanced row blocks, each block a Workspace<T> holding A_g,
+// its own transpose A_g^T (n x m_g), the replicated P and n-vectors, and the
+// m_g-slices of every m-vector.  Per K-apply the only exchange is the sum of
+// the A_g^T partial n-vectors; scalar decisions are taken from combined
+// values, identical on every block, so the loop stays in lockstep without
+// further communication.
+//
+// Exchanges per ADMM step (all through ShardComm):
+//   rhs:   allreduce(2n)   [A^T (rho z - y), A^T (rho z~)]
+//   PCG:   allreduce(n)    per iteration [A^T t]
+//   check: allreduce(n) [A^T y] + allreduce_max(14 scalars)
+//   rho:   allreduce_max(1) [|z|_inf]
+//   infeasibility (rare): allreduce(3), allreduce(n), allreduce(1)
+// Setup: allreduce_max(n) + allreduce_max(1) per Ruiz pass (maxima: the
+// scaled problem stays bit-identical to the unsharded one) and a chain across
+// blocks for diag(A^T A) (a sequential sum in the reference; chaining keeps
+// it bit-exact), so the Jacobi preconditioner is bit-identical as well.
+//
+// The loop is host-driven: one control-block read per PCG iteration decides
+// the next step on every block.
+#pragma once
+
+#include "comm.cuh"
+
+namespace qpcg_b200 {
+
+template <typename T>
+class Sharded {
+ public:
+  ShardComm comm;
+  std::vector<std::unique_ptr<Workspace<T>>> sh;
+  std::vector<uint32_t> cuts;      // [G + 1] global row cuts
+  std::vector<uint32_t> rank_off;  // [R + 1] first row of every rank's blocks
+  cudaStream_t s = nullptr;
+  bool own_stream = true;
+  int device = 0;
+  uint32_t n = 0, m = 0;
+  bool balanced = true;
+  qpcg_options opt{};
+  double setup_seconds = 0;
+  uint64_t setup_launches = 0;
+  bool have_counted_setup = false;
+  T* full_m = nullptr;  // gather buffer [m]
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  ~Sharded() {
+    sh.clear();  // blocks free their buffers on the shared stream
+    if (full_m) {
+      AllocScope scope(s);
+      dfree(full_m);
+      cudaStreamSynchronize(s);
+    }
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (s && own_stream) cudaStreamDestroy(s);
+  }
+
+  Workspace<T>& w0() { return *sh[0]; }
+  template <typename F>
+  void each(F&& f) {
+    for (auto& w : sh) f(*w);
+  }
+  template <typename U, typename F>
+  std::vector<U*> bufs(F&& f) {
+    std::vector<U*> v;
+    for (auto& w : sh) v.push_back(f(*w));
+    return v;
+  }
+  void allreduce_part(size_t count) {
+    comm.allreduce(bufs<T>([](Workspace<T>& w) { return w.D.part; }), count, false);
+  }
+  void allreduce_scal(size_t count, bool max) {
+    comm.allreduce(bufs<T>([](Workspace<T>& w) { return w.D.shsc; }), count, max);
+  }
+  // min of a per-block host key over every block of every rank
+  unsigned long long agree_min(const std::vector<unsigned long long>& keys) {
+    unsigned long long k = ~0ull;
+    for (auto v : keys) k = std::min(k, v);
+    if (comm.comm) {
+      unsigned long long* d = w0().template alloc<unsigned long long>(1);
+      CK(cudaMemcpyAsync(d, &k, 8, cudaMemcpyHostToDevice, s));
+      comm.allreduce_min_u64(d);
+      CK(cudaMemcpyAsync(&k, d, 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    return k;
+  }
+
+  // ------------------------------------------------------------- setup
+  void setup(const HostCsr<T>& Pu, const T* q, const HostCsr<T>& A, const T* l, const T* u,
+             const qpcg_settings& st, const qpcg_options& op) {
+    const double w0s = now_s();
+    const uint64_t l0 = g_launches;
+    opt = op;
+    Workspace<T>::validate_settings(st);
+    device = op.device;
+    if (device < 0) CK(cudaGetDevice(&device));
+    CK(cudaSetDevice(device));
+    if (op.stream != nullptr) {
+      s = static_cast<cudaStream_t>(op.stream);
+      own_stream = false;
+    } else {
+      CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    }
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaEventRecord(ev0, s));
+    comm.s = s;
+    comm.local = op.virtual_shards > 1 ? op.virtual_shards : 1;
+    if (comm.local > kMaxLocalShards) throw InvalidArgument("options: at most 16 virtual shards");
+    if (op.nccl_id != nullptr) {
+      if (op.nccl_ranks < 1 || op.nccl_rank < 0 || op.nccl_rank >= op.nccl_ranks)
+        throw InvalidArgument("options: bad nccl rank / ranks");
+      comm.init_nccl(op.nccl_id, op.nccl_rank, op.nccl_ranks);
+    }
+    const uint32_t L = comm.local, R = comm.nranks, G = L * R;
+    n = Pu.rows;
+    m = A.rows;
+    // ---- nnz-balanced cuts from the (host copy of) row_ptr
+    std::vector<uint32_t> hrp;
+    const uint32_t* rp = A.row_ptr;
+    if (op.input_memory != QPCG_MEM_HOST) {
+      hrp.resize(size_t(m) + 1);
+      CK(cudaMemcpyAsync(hrp.data(), A.row_ptr, 4 * (size_t(m) + 1), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      rp = hrp.data();
+    }
+    cuts.assign(G + 1, 0);
+    balanced = shard_cuts(rp, m, A.nnz, G, cuts.data());
+    rank_off.assign(R + 1, 0);
+    for (uint32_t r = 0; r <= R; ++r) rank_off[r] = cuts[r * L];
+    // ---- per-block upload and validation
+    std::vector<unsigned long long> kp, ka, kv;
+    for (uint32_t li = 0; li < L; ++li) {
+      const int g = comm.global_index(li);
+      sh.emplace_back(new Workspace<T>());
+      Workspace<T>& w = *sh.back();
+      w.D.split = 1;
+      w.D.sh_index = g;
+      w.D.sh_count = G;
+      w.begin(st, op, s);
+      AllocScope scope(s);
+      if (balanced)
+        w.load(Pu, q, A, l, u, cuts[g], cuts[g + 1], true);
+      else if (g == 0)  // invalid row_ptr: block 0 sees A exactly as given
+        w.load(Pu, q, A, l, u, 0, m, false);
+      else
+        w.load(Pu, q, A, l, u, m, m, true);
+      const typename Workspace<T>::ValKeys v = w.validate_keys();
+      // P's row_ptr ends are identical on every block; A's are block-local
+      // (and only block 0 can see a bad one): fold both into the stage keys
+      // (0 = "row_ptr must start at 0 and end at nnz", ahead of any key)
+      kp.push_back((v.ends[0] != 0 || v.ends[1] != w.pu_nnz) ? 0ull : v.k[0]);
+      ka.push_back((v.ends[2] != 0 || v.ends[3] != w.D.A.nnz) ? 0ull : v.k[1]);
+      kv.push_back(v.k[2]);
+    }
+    {
+      typename Workspace<T>::ValKeys v{};
+      v.k[0] = agree_min(kp);
+      v.k[1] = agree_min(ka);
+      v.k[2] = agree_min(kv);
+      if (v.k[0] == 0) throw InvalidArgument("csr: row_ptr must start at 0 and end at nnz");
+      if ((v.k[0] >> 56) == kValPRowPtr) throw InvalidArgument(validation_message(v.k[0]));
+      if (v.k[1] == 0) throw InvalidArgument("csr: row_ptr must start at 0 and end at nnz");
+      // the rest of the reference order (problem.hpp:46-92) as raise_first
+      Workspace<T>& w = w0();
+      if ((v.k[1] >> 56) == kValARowPtr) throw InvalidArgument(validation_message(v.k[1]));
+      if (!w.p_square) throw InvalidArgument("problem: P must be square");
+      if (n == 0) throw InvalidArgument("problem: at least one variable required");
+      if ((v.k[0] >> 56) == kValPBelow) throw InvalidArgument(validation_message(v.k[0]));
+      if (!w.a_cols_ok) throw InvalidArgument("problem: A column count must equal n");
+      if (v.k[2] != ~0ull) throw InvalidArgument(validation_message(v.k[2]));
+    }
+    AllocScope scope(s);
+    each([](Workspace<T>& w) { w.build_structures(); });
+    // ---- Ruiz with the two maxima combined across blocks
+    uint32_t passes = 0;
+    T deviation = T(0);
+    if (st.scaling_enabled) {
+      each([](Workspace<T>& w) { w.ruiz_prepare(); });
+      deviation = T(1);
+      while (passes < st.equil_max_passes && deviation > T(st.eps_equil)) {
+        ++passes;
+        each([](Workspace<T>& w) { w.ruiz_norms(); });
+        comm.allreduce(bufs<T>([](Workspace<T>& w) { return w.rz_atn; }), n, true);
+        each([](Workspace<T>& w) { w.ruiz_delta(); });
+        comm.allreduce(bufs<T>([](Workspace<T>& w) { return w.ruiz_scal + 4; }), 1, true);
+        each([](Workspace<T>& w) { w.ruiz_scale(); });
+        deviation = w0().read_scalar(w0().ruiz_scal + 4);
+      }
+    }
+    each([&](Workspace<T>& w) { w.finish_scaling(passes, deviation); });
+    // ---- diag(A^T A): one sequential chain through the blocks in row order
+    T* acc = w0().D.diag_ata;
+    comm.chain(acc, n, [&] {
+      for (uint32_t li = 0; li < L; ++li) {
+        const bool first = comm.rank == 0 && li == 0;
+        diag_ata_kernel<T><<<grid_for(uint64_t(n) * 32), kThreads, 0, s>>>(sh[li]->D.AT, acc,
+                                                                            first ? nullptr : acc);
+        CK_LAUNCH();
+      }
+    });
+    for (uint32_t li = 1; li < L; ++li)
+      CK(cudaMemcpyAsync(sh[li]->D.diag_ata, acc, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+    each([](Workspace<T>& w) { w.finish_setup(); });
+    CK(dmalloc(&full_m, sizeof(T) * (size_t(m) + 1)));
+    CK(cudaEventRecord(ev1, s));
+    CK(cudaEventSynchronize(ev1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    setup_seconds = ms * 1e-3;
+    each([&](Workspace<T>& w) {
+      w.setup_seconds = setup_seconds;
+      w.setup_wall = now_s() - w0s;
+    });
+    setup_launches = g_launches - l0;
+  }
+
+  // ------------------------------------------------------ loop pieces
+  void enq_rhs() {
+    each([](Workspace<T>& w) {
+      k_pack_rhs<T><<<grid_for(w.D.m), kThreads, 0, w.s>>>(w.D);
+      CK_LAUNCH();
+      launch_spmv<T, 2, SumOp>(w.D.AT, w.D.pAT, GatherRhs<T>{w.D.g2m},
+                               EpiPart<T, 2>{w.D.part, w.D.ctl, 0}, w.s);
+    });
+    allreduce_part(2 * size_t(n));
+    each([](Workspace<T>& w) {
+      k_rhs_finish<T><<<grid_for(w.D.n), kThreads, 0, w.s>>>(w.D);
+      CK_LAUNCH();
+      w.enq_pcg_init(Handles{});
+    });
+  }
+  void enq_pcg_iter() {
+    each([](Workspace<T>& w) {
+      launch_spmv<T, 1, SumOp>(w.D.A, w.D.pA, GatherVec<T>{w.D.p}, EpiAp<T>{w.D.t, w.D.ctl, T(0)}, w.s);
+      launch_spmv<T, 1, SumOp>(w.D.AT, w.D.pAT, GatherVec<T>{w.D.t},
+                               EpiPart<T, 1>{w.D.part, w.D.ctl, 1}, w.s);
+    });
+    allreduce_part(n);
+    each([](Workspace<T>& w) {
+      k_pcg_dot<T><<<red_grid<T>(w.D.n), kThreads, 0, w.s>>>(w.D);
+      CK_LAUNCH();
+      k_pcg_update<T><<<red_grid<T>(w.D.n), kThreads, 0, w.s>>>(w.D, Handles{});
+      CK_LAUNCH();
+      k_pcg_pupdate<T><<<grid_for(w.D.n), kThreads, 0, w.s>>>(w.D);
+      CK_LAUNCH();
+    });
+  }
+  void enq_check(int mode) {
+    each([](Workspace<T>& w) {
+      launch_spmv<T, 1, SumOp>(w.D.AT, w.D.pAT, GatherVec<T>{w.D.y},
+                               EpiPart<T, 1>{w.D.part, w.D.ctl, 0}, w.s);
+    });
+    allreduce_part(n);
+    each([&](Workspace<T>& w) {
+      k_dual_finish<T><<<grid_for(w.D.n), kThreads, 0, w.s>>>(w.D);
+      CK_LAUNCH();
+      k_residuals<T><<<red_grid<T>(std::max(w.D.n, w.D.m)), kThreads, 0, w.s>>>(w.D, mode, Handles{});
+      CK_LAUNCH();
+    });
+    allreduce_scal(14, true);
+    each([&](Workspace<T>& w) {
+      k_residuals_decide<T><<<1, 32, 0, w.s>>>(w.D, mode, Handles{});
+      CK_LAUNCH();
+    });
+  }
+  void enq_residuals_fresh(int mode) {
+    each([](Workspace<T>& w) {
+      launch_spmv<T, 1, SumOp>(w.D.A, w.D.pA, GatherVec<T>{w.D.x}, EpiStore<T>{w.D.ax}, w.s);
+    });
+    enq_check(mode);
+  }
+  void enq_infeas() {
+    each([](Workspace<T>& w) {
+      k_infeas_vec<T><<<red_grid<T>(std::max(w.D.n, w.D.m)), kThreads, 0, w.s>>>(w.D);
+      CK_LAUNCH();
+    });
+    allreduce_scal(3, false);
+    each([](Workspace<T>& w) {
+      Dev<T>& D = w.D;
+      k_infeas_vec_decide<T><<<1, 32, 0, w.s>>>(D);
+      CK_LAUNCH();
+      launch_spmv<T, 1, SumOp>(D.ATo, D.pATo, GatherCertY<T>{D.e, D.dy, D.ctl, T(0), T(0)},
+                               EpiPart<T, 1>{D.part, D.ctl, 2}, w.s);
+    });
+    allreduce_part(n);
+    each([](Workspace<T>& w) {
+      Dev<T>& D = w.D;
+      k_atv_norm<T><<<red_grid<T>(D.n), kThreads, 0, w.s>>>(D);
+      CK_LAUNCH();
+      launch_spmv<T, 1, SumOp>(D.Po, D.pPo, GatherCertX<T>{D.d, D.dx, D.ctl, T(0)},
+                               EpiNormMax<T>{&D.ctl->pv_inf_bits, &D.ctl->need_dinf}, w.s);
+      k_infeas_mid<T><<<1, 1, 0, w.s>>>(D);
+      CK_LAUNCH();
+      launch_spmv<T, 1, SumOp>(
+          D.Ao, D.pAo, GatherCertX<T>{D.d, D.dx, D.ctl, T(0)},
+          EpiDualRows<T>{D.l_o, D.u_o, &D.ctl->dinf_bad, &D.ctl->need_dinf, T(0), D.ctl}, w.s);
+      k_flag_to_scal<T><<<1, 1, 0, w.s>>>(D);
+      CK_LAUNCH();
+    });
+    allreduce_scal(1, false);
+    each([](Workspace<T>& w) {
+      k_infeas<T><<<1, 1, 0, w.s>>>(w.D);
+      CK_LAUNCH();
+    });
+  }
+  void enq_rho() {
+    each([](Workspace<T>& w) {
+      w.enq_rho_flag(Handles{});
+      k_rho<T><<<red_grid<T>(w.D.m), kThreads, 0, w.s>>>(w.D);
+      CK_LAUNCH();
+    });
+    allreduce_scal(1, true);
+    each([](Workspace<T>& w) {
+      k_rho_decide<T><<<1, 32, 0, w.s>>>(w.D);
+      CK_LAUNCH();
+      k_precond<T><<<grid_for(w.D.n), kThreads, 0, w.s>>>(w.D, 0);
+      CK_LAUNCH();
+    });
+  }
+
+  // ------------------------------------------------------------ solve
+  void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) {
+    CK(cudaSetDevice(device));
+    AllocScope scope(s);
+    const double w0s = now_s();
+    CK(cudaEventRecord(ev0, s));
+    each([](Workspace<T>& w) { w.reset_solve_state(); });
+    const uint64_t l0 = g_launches;
+    Workspace<T>& W = w0();
+    enq_residuals_fresh(1);  // solver.hpp:436-441
+    for (;;) {
+      W.pull_ctl();
+      if (W.hc.done || W.hc.error || W.hc.iter >= W.hc.max_iter) break;
+      enq_rhs();
+      W.pull_ctl();
+      while (W.hc.pcg_active && !W.hc.error) {
+        enq_pcg_iter();
+        W.pull_ctl();
+      }
+      each([](Workspace<T>& w) { w.enq_post_pcg(Handles{}); });
+      W.pull_ctl();
+      if (W.hc.is_check && !W.hc.error) {
+        enq_check(0);
+        W.pull_ctl();
+        if (W.hc.inf_branch) enq_infeas();
+      }
+      enq_rho();
+    }
+    W.pull_ctl();
+    W.raise_device_error();
+    if (!W.hc.residuals_current) enq_residuals_fresh(2);
+    each([](Workspace<T>& w) {
+      Dev<T>& D = w.D;
+      k_unscale<T><<<grid_for(std::max(D.n, D.m)), kThreads, 0, w.s>>>(D);
+      CK_LAUNCH();
+    });
+    W.pull_ctl();
+    const bool infeasible = W.hc.status == 1 || W.hc.status == 2;
+    if (!infeasible)  // P is replicated: block 0 alone forms the objective
+      launch_spmv<T, 1, SumOp>(W.D.Po, W.D.pPo, GatherVec<T>{W.D.xo}, EpiStore<T>{W.D.pxo}, s);
+    k_objective<T><<<red_grid<T>(n), kThreads, 0, s>>>(W.D);
+    CK_LAUNCH();
+    CK(cudaEventRecord(ev1, s));
+    W.pull_ctl();
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    // m-side outputs: every block's slice at its global rows, then across ranks
+    const double td0 = now_s();
+    gather_m([](Workspace<T>& w) { return w.D.zo; }, z);
+    gather_m([](Workspace<T>& w) { return w.D.yo; }, y);
+    W.download(x, W.D.xo, sizeof(T) * n);
+    if (W.hc.status == 1)
+      gather_m([](Workspace<T>& w) { return w.D.cert; }, cert);
+    else if (W.hc.status == 2)
+      W.download(cert, W.D.cert, sizeof(T) * n);
+    CK(cudaStreamSynchronize(s));
+    const double d2h = now_s() - td0;
+    if (info) {
+      W.fill_info(info, ms * 1e-3, d2h, n, m);
+      info->setup_seconds = setup_seconds;
+      info->runtime_seconds = now_s() - w0s;
+      uint64_t h2d = 0;
+      double h2ds = 0;
+      each([&](Workspace<T>& w) {
+        h2d += w.h2d_bytes;
+        h2ds += w.h2d_seconds;
+      });
+      info->h2d_bytes = h2d;
+      info->h2d_seconds = h2ds;
+      info->kernel_launches = (g_launches - l0) + (have_counted_setup ? 0 : setup_launches);
+    }
+    have_counted_setup = true;
+  }
+
+  // download (host or device destination) an m-vector assembled from the blocks
+  template <typename F>
+  void gather_m(F&& src, T* dst) {
+    if (dst == nullptr || m == 0) return;
+    each([&](Workspace<T>& w) {
+      if (w.D.m)
+        CK(cudaMemcpyAsync(full_m + w.row0, src(w), sizeof(T) * w.D.m, cudaMemcpyDeviceToDevice, s));
+    });
+    comm.allgather_blocks(full_m, rank_off);
+    w0().download(dst, full_m, sizeof(T) * m);
+  }
+
+  // --------------------------------------------------- OSQP-style updates
+  void warm_start(const T* x, const T* z, const T* y) {
+    CK(cudaSetDevice(device));
+    AllocScope scope(s);
+    std::vector<unsigned long long> keys;
+    each([&](Workspace<T>& w) { keys.push_back(w.warm_stage(x, z + w.row0, y + w.row0)); });
+    if (agree_min(keys) != ~0ull) throw InvalidArgument("solve: warm start must be finite");
+    each([](Workspace<T>& w) { w.warm_apply(); });
+  }
+  void update_rho(T rho) {
+    each([&](Workspace<T>& w) { w.update_rho(rho); });
+  }
+  void update_vectors(const T* q, const T* l, const T* u) {
+    CK(cudaSetDevice(device));
+    AllocScope scope(s);
+    std::vector<unsigned long long> keys;
+    each([&](Workspace<T>& w) {
+      keys.push_back(w.vectors_stage(q, l ? l + w.row0 : nullptr, u ? u + w.row0 : nullptr));
+    });
+    const unsigned long long k = agree_min(keys);
+    if (k != ~0ull) throw InvalidArgument(validation_message(k));
+    each([](Workspace<T>& w) { w.vectors_apply(); });
+  }
+};
+
+}  // namespace qpcg_b200

@@ -52,6 +52,8 @@ def load_library() -> C.CDLL:
     lib.qpcg_get_rho_updates.restype = C.c_uint32
     lib.qpcg_get_check_iterations.argtypes = [vp, vp, C.c_uint32]
     lib.qpcg_get_check_iterations.restype = C.c_uint32
+    lib.qpcg_shard_cuts.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_uint32, vp]
+    lib.qpcg_nccl_unique_id.argtypes = [vp]
     _lib = lib
     return lib
 
@@ -75,27 +77,57 @@ def _pre(dtype) -> str:
 
 
 def make_options(device: int = -1, mode: str = "graph", record_diagnostics: bool = False,
-                 device_memory: bool = False) -> _abi.Options:
+                 device_memory: bool = False, shards: int = 1,
+                 nccl: tuple | None = None) -> _abi.Options:
+    """shards: row blocks of A held on this device (virtual shards);
+    nccl: (rank, ranks, id_bytes) to join the row-sharded NCCL group
+    (id_bytes from nccl_unique_id() on rank 0)."""
     o = _abi.Options()
     o.device = device
     o.input_memory = _abi.MEM_DEVICE if device_memory else _abi.MEM_HOST
     o.mode = _abi.MODE_EAGER if mode == "eager" else _abi.MODE_GRAPH
     o.record_diagnostics = 1 if record_diagnostics else 0
-    o.virtual_shards = 1
+    o.virtual_shards = max(1, int(shards))
+    if nccl is not None:
+        rank, ranks, uid = nccl
+        buf = C.create_string_buffer(bytes(uid), _abi.NCCL_ID_BYTES)
+        o.nccl_rank, o.nccl_ranks = int(rank), int(ranks)
+        o.nccl_id = C.cast(buf, C.c_void_p)
+        o._keep_id = buf  # the id must outlive the setup call
     return o
+
+
+def shard_cuts(row_ptr: np.ndarray, nnz: int, blocks: int) -> tuple[np.ndarray, bool]:
+    """nnz-balanced contiguous row cuts (qpcg_shard_cuts; host-only, no GPU)."""
+    rp = np.ascontiguousarray(row_ptr, np.uint32)
+    cuts = np.zeros(blocks + 1, np.uint32)
+    ok = load_library().qpcg_shard_cuts(_abi.ptr(rp), len(rp) - 1, int(nnz), int(blocks),
+                                        _abi.ptr(cuts))
+    return cuts, bool(ok)
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (rank 0 creates it and shares it with the group)."""
+    lib = load_library()
+    buf = C.create_string_buffer(_abi.NCCL_ID_BYTES)
+    rc = lib.qpcg_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if rc != _abi.QPCG_OK:
+        _raise(rc, lib.qpcg_last_error(None).decode())
+    return buf.raw
 
 
 class Workspace:
     """OSQP-style workspace: setup once, then solve / warm_start / update_*."""
 
     def __init__(self, problem: QpProblem, settings: Settings | None = None, device: int = -1,
-                 mode: str = "graph", record_diagnostics: bool = False):
+                 mode: str = "graph", record_diagnostics: bool = False, shards: int = 1,
+                 nccl: tuple | None = None):
         self.lib = load_library()
         self.problem = problem
         self.dtype = problem.dtype
         self.pre = _pre(self.dtype)
         self.settings = settings or Settings()
-        self._opts = make_options(device, mode, record_diagnostics)
+        self._opts = make_options(device, mode, record_diagnostics, shards=shards, nccl=nccl)
         self._s = self.settings.to_c()
         self._pv, self._av = problem.p_upper.view(), problem.a.view()
         self.ws = C.c_void_p()
@@ -171,10 +203,13 @@ def fetch_diagnostics(lib, ws, diag: SolveDiagnostics):
 
 
 def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | None = None,
-          diag: SolveDiagnostics | None = None, device: int = -1, mode: str = "graph"):
-    """Drop-in for qpcg::solve (solver.hpp:386-541) on the B200 engine."""
+          diag: SolveDiagnostics | None = None, device: int = -1, mode: str = "graph",
+          shards: int = 1, nccl: tuple | None = None):
+    """Drop-in for qpcg::solve (solver.hpp:386-541) on the B200 engine.
+    shards > 1 / nccl: the row-sharded engine."""
     if diag is not None:
-        with Workspace(p, settings, device, mode, record_diagnostics=True) as ws:
+        with Workspace(p, settings, device, mode, record_diagnostics=True, shards=shards,
+                       nccl=nccl) as ws:
             if initial is not None:
                 ws.warm_start(initial.x, initial.z, initial.y)
             return ws.solve(diag)
@@ -183,7 +218,7 @@ def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | N
     n, m = p.n, p.m
     dt = p.dtype
     s = (settings or Settings()).to_c()
-    o = make_options(device, mode)
+    o = make_options(device, mode, shards=shards, nccl=nccl)
     x, z, y = np.zeros(n, dt), np.zeros(m, dt), np.zeros(m, dt)
     cert = np.zeros(max(n, m), dt)
     info = _abi.Info()

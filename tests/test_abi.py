@@ -45,7 +45,8 @@ int main(void) {
          sizeof(qpcg_rho_update), sizeof(qpcg_csr_f64));
   P(qpcg_settings, lambda_pcg); P(qpcg_settings, equil_max_passes);
   P(qpcg_info, setup_seconds); P(qpcg_info, kernel_launches); P(qpcg_info, rho_final);
-  P(qpcg_options, stream); P(qpcg_pcg_call, converged);
+  P(qpcg_options, stream); P(qpcg_options, nccl_id); P(qpcg_options, nccl_ranks);
+  P(qpcg_pcg_call, converged);
   return 0;
 }'''
     with tempfile.TemporaryDirectory() as d:
@@ -66,6 +67,8 @@ int main(void) {
     assert int(out["qpcg_info.kernel_launches"]) == _abi.Info.kernel_launches.offset
     assert int(out["qpcg_info.rho_final"]) == _abi.Info.rho_final.offset
     assert int(out["qpcg_options.stream"]) == _abi.Options.stream.offset
+    assert int(out["qpcg_options.nccl_id"]) == _abi.Options.nccl_id.offset
+    assert int(out["qpcg_options.nccl_ranks"]) == _abi.Options.nccl_ranks.offset
     assert int(out["qpcg_pcg_call.converged"]) == _abi.PcgCall.converged.offset
 
 
