@@ -23,8 +23,12 @@ RNG and recipes; fp64; settings {"lambda_pcg": 1e-3} (0.01, the survey's choice,
               the solve time is extrapolated with the solve's iteration counts.
 
 --impl reference runs only the reference CPU arm (rank 0), same metric/config.
-Multi-GPU (torchrun): each rank solves an independent instance ("replicas",
-weak scaling) until the row-sharded path lands; value = max over ranks.
+Multi-GPU (torchrun, N > 1): the ROW-SHARDED engine — every
+rank holds an nnz-balanced block of A's rows (+ its own A_g^T), the A^T
+partials are summed with NCCL once per operator apply; one instance solved by
+all N GPUs ("strong" scaling), value = max over ranks of the device-timed
+solve.  --replicas instead solves an independent instance per rank ("weak").
+--shards K (N = 1) runs the sharded engine with K row blocks on one GPU.
 """
 from __future__ import annotations
 
@@ -73,6 +77,9 @@ def parse():
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="graph", choices=["graph", "eager"])
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent instance per rank instead of the row-sharded solve")
+    ap.add_argument("--shards", type=int, default=1, help="row blocks per GPU (virtual shards)")
     return ap.parse_args()
 
 
@@ -150,7 +157,7 @@ def _views(arrs, n, m, dev):
 
 
 class Engine:
-    def __init__(self, problem, settings, device, stream_ptr, dtype, mode):
+    def __init__(self, problem, settings, device, stream_ptr, dtype, mode, shards=1, nccl=None):
         import torch
         from paper_1912_04263_b200 import _abi, solver
         self.lib = solver.load_library()
@@ -181,8 +188,12 @@ class Engine:
             o.input_memory = _abi.MEM_DEVICE if memkind == "device" else _abi.MEM_HOST
             o.mode = _abi.MODE_EAGER if mode == "eager" else _abi.MODE_GRAPH
             o.record_diagnostics = 0
-            o.virtual_shards = 1
+            o.virtual_shards = shards
             o.stream = C.c_void_p(stream_ptr)
+            if nccl is not None:  # (rank, ranks, id): the row-sharded NCCL group
+                self._id = C.create_string_buffer(bytes(nccl[2]), _abi.NCCL_ID_BYTES)
+                o.nccl_rank, o.nccl_ranks = nccl[0], nccl[1]
+                o.nccl_id = C.cast(self._id, C.c_void_p)
             self.opts[memkind] = o
         self._abi = _abi
         self.msg = C.create_string_buffer(512)
@@ -354,17 +365,24 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    from paper_1912_04263_b200 import generators
+    from paper_1912_04263_b200 import generators, solver
     from paper_1912_04263_b200.problem import Settings
     dtype = np.float64 if args.dtype == "f64" else np.float32
+    sharded = world > 1 and not args.replicas
+    nccl = None
+    if sharded:  # one NCCL group for the engine, id shared over torch.distributed
+        obj = [solver.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl = (rank, world, obj[0])
     tg = time.time()
-    problem = generators.config(args.config, seed=rank)
+    problem = generators.config(args.config, seed=0 if sharded else rank)
     gen_s = time.time() - tg
     log(f"generated config {args.config}: n={problem.n} m={problem.m} nnz(A)={problem.a.nnz} in {gen_s:.1f}s")
     settings = Settings(lambda_pcg=args.lambda_pcg)
     stream = torch.cuda.Stream(device=local)
     with torch.cuda.stream(stream):
-        eng = Engine(problem, settings, local, stream.cuda_stream, dtype, args.mode)
+        eng = Engine(problem, settings, local, stream.cuda_stream, dtype, args.mode,
+                     shards=args.shards, nccl=nccl)
         for i in range(args.warmup):
             t = time.time()
             info = eng.solve("device")
@@ -418,10 +436,11 @@ def main():
     at_ms, pcg_ms = kt[1], kt[2]
     achieved = kt[4] / (at_ms * 1e-3) / 1e9
     loop_s = last.solve_seconds
-    roofline = {"bound": "hbm", "kernel": "spmv A^T pass of the PCG operator (Kp = P p + sigma p + A^T t)",
+    roofline = {"bound": "hbm", "kernel": "spmv A^T pass of the PCG operator (Kp = P p + sigma p + A^T t)"
+                + (" on rank 0's row block" if sharded or args.shards > 1 else ""),
                 "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "peak_source": pk["source"],
-                "traffic": ncu_traffic(args.config),
+                "traffic": None if (sharded or args.shards > 1) else ncu_traffic(args.config),
                 "algorithmic_bytes_per_launch": kt[4], "launch_ms": at_ms,
                 "a_pass": {"ms": kt[0], "bytes": kt[3], "achieved": kt[3] / (kt[0] * 1e-3) / 1e9},
                 "pcg_iteration": {"ms": pcg_ms, "bytes": kt[5],
@@ -430,12 +449,15 @@ def main():
                 "frac_of_nominal_8TBs": achieved / 8000.0}
     line = {"metric": METRIC, "value": ms * 1e-3, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": False, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic (reference RNG + recipes, SURVEY.md §8(d))",
             "config": {"workload": WORKLOADS[args.config], "config_id": args.config,
                        "n": problem.n, "m": problem.m, "nnz_P_upper": problem.p_upper.nnz,
                        "nnz_A": problem.a.nnz, "settings": {"lambda_pcg": args.lambda_pcg},
-                       "parallelism": "single" if world == 1 else f"replicas{world}",
+                       "parallelism": (f"rowshard{world}" if sharded else f"replicas{world}")
+                                      if world > 1 else
+                                      ("single" if args.shards <= 1 else f"virtual-rowshard{args.shards}"),
                        "l2": "inputs larger than L2 (A and A^T streams ~%.1f GB per PCG iteration)"
                              % (kt[5] / 1e9),
                        "mode": args.mode},

@@ -1412,11 +1412,14 @@ int qpcg_debug_operator(qpcg_workspace* ws, const void* x, void* kx, void* dinv)
 }
 
 int qpcg_bench_kernels(qpcg_workspace* ws, uint32_t reps, double* out) {
+  // (sharded workspaces: the kernels of this process's first row block)
   return guarded(ws, [&] {
-    if (ws && ws->w64)
-      ws->w64->bench_kernels(reps, out);
+    if (Workspace<double>* w = ws ? primary<double>(ws) : nullptr)
+      w->bench_kernels(reps, out);
+    else if (Workspace<float>* w = ws ? primary<float>(ws) : nullptr)
+      w->bench_kernels(reps, out);
     else
-      get<float>(ws)->bench_kernels(reps, out);
+      throw InvalidArgument("workspace: null");
   });
 }
 
