@@ -142,19 +142,30 @@ template <typename T>
 __host__ __device__ __forceinline__ T smin(T a, T b) { return (b < a) ? b : a; }
 
 // streaming loads: bypass L1 allocation for the matrix streams
+// (QPCG_LDMODE 1: + 256-byte L2 prefetch hint; 2: ld.global.cs)
+#ifndef QPCG_LDMODE
+#define QPCG_LDMODE 1
+#endif
+#if QPCG_LDMODE == 1
+#define QPCG_LD_Q "ld.global.nc.L1::no_allocate.L2::256B"
+#elif QPCG_LDMODE == 2
+#define QPCG_LD_Q "ld.global.cs"
+#else
+#define QPCG_LD_Q "ld.global.nc.L1::no_allocate"
+#endif
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm volatile(QPCG_LD_Q ".f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ float ld_stream(const float* p) {
   float v;
-  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  asm volatile(QPCG_LD_Q ".f32 %0, [%1];" : "=f"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile(QPCG_LD_Q ".u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 

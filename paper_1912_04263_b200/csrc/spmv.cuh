@@ -26,6 +26,8 @@
 
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace qpcg_b200 {
@@ -88,7 +90,10 @@ struct GatherNone {
 };
 
 // --------------------------------------------------------------- kernel
-template <typename T, int NCOL, class Op, class Gather, class Epi, int U = 4>
+#ifndef QPCG_SPMV_U
+#define QPCG_SPMV_U 8
+#endif
+template <typename T, int NCOL, class Op, class Gather, class Epi, int U = QPCG_SPMV_U>
 __global__ void __launch_bounds__(kThreads) spmv_kernel(DevCsr<T> M, SpmvPlan<T> P, Gather gather,
                                                        Epi epi) {
   // functors load their device-resident scalars (rho, flags) once per thread;
@@ -123,12 +128,24 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(DevCsr<T> M, SpmvPlan<T>
         for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v[u], Op::kNeedsGather ? g[j] : T(0));
       }
     }
-    for (; k < end; k += 32u) {
-      const T v = ld_stream(val + k);
-      T g[NCOL];
-      if (Op::kNeedsGather) gather(ld_stream(ci + k), g);
+    if (k < end) {  // the < 32U remaining entries: one predicated step, all loads in flight
+      uint32_t c[U];
+      T v[U];
 #pragma unroll
-      for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v, Op::kNeedsGather ? g[j] : T(0));
+      for (int u = 0; u < U; ++u) {
+        const bool ok = k + 32u * u < end;
+        v[u] = ok ? ld_stream(val + k + 32u * u) : T(0);
+        if (Op::kNeedsGather) c[u] = ok ? ld_stream(ci + k + 32u * u) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (k + 32u * u < end) {
+          T g[NCOL];
+          if (Op::kNeedsGather) gather(c[u], g);
+#pragma unroll
+          for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v[u], Op::kNeedsGather ? g[j] : T(0));
+        }
+      }
     }
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) acc[j] = Op::warp(acc[j]);
@@ -205,7 +222,7 @@ __global__ void plan_emit_kernel(const uint32_t* __restrict__ rp, uint32_t rows,
                                  const uint32_t* nch, const uint32_t* item_off,
                                  const uint32_t* lr_idx, const uint32_t* pbase,
                                  uint32_t* short_rows, WorkItem* items, uint32_t* item_len,
-                                 uint2* lrinfo) {
+                                 uint2* lrinfo, int by_chunk) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
     if (is_short[r]) {
       short_rows[short_pos[r]] = r;
@@ -221,7 +238,12 @@ __global__ void plan_emit_kernel(const uint32_t* __restrict__ rp, uint32_t rows,
       w.end = min(e, w.beg + kChunk);
       w.lr = lr;
       items[item_off[r] + q] = w;
-      item_len[item_off[r] + q] = kChunk - (w.end - w.beg);  // sort key: longest first
+      // sort key.  by_chunk: the q-th chunks of all rows first, in row order,
+      // then the (q+1)-th ...: chunk q of a row with sorted columns covers
+      // about the same column window in every row of similar density, so the
+      // warps resident on an SM gather from one window (L1 reuse).  Else:
+      // longest first (balanced tail).
+      item_len[item_off[r] + q] = by_chunk ? q : kChunk - (w.end - w.beg);
     }
   }
 }
@@ -291,6 +313,8 @@ void plan_free(SpmvPlan<T>& P) {
 template <typename T>
 SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaStream_t s) {
   SpmvPlan<T> P;
+  const char* ord = std::getenv("QPCG_ITEM_ORDER");
+  const int by_chunk = !(ord && ord[0] == 'l');  // "len": longest first
   if (rows == 0) return P;
   uint32_t *is_short, *nch, *is_multi, *multi_nch, *short_pos, *item_off, *lr_idx, *pbase;
   const size_t bytes = sizeof(uint32_t) * rows;
@@ -329,18 +353,19 @@ SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaSt
   CK(dmalloc(&order_out, sizeof(uint32_t) * ni));
   plan_emit_kernel<<<grid_for(rows), kThreads, 0, s>>>(d_rp, rows, is_short, short_pos, nch,
                                                       item_off, lr_idx, pbase, P.short_rows,
-                                                      items_tmp, keys, P.lrinfo);
+                                                      items_tmp, keys, P.lrinfo, by_chunk);
   CK_LAUNCH();
   if (P.n_items > 0) {
     // stable sort of items by length (longest first) for a balanced tail
     iota_kernel<<<grid_for(P.n_items), kThreads, 0, s>>>(order, P.n_items);
     CK_LAUNCH();
     size_t b = 0;
+    const int kbits = by_chunk ? 20 : 12;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, b, keys, keys_out, order, order_out, P.n_items, 0,
-                                       12, s));
+                                       kbits, s));
     tmp.ensure(b);
     CK(cub::DeviceRadixSort::SortPairs(tmp.ptr, b, keys, keys_out, order, order_out, P.n_items, 0,
-                                       12, s));
+                                       kbits, s));
     plan_gather_items_kernel<<<grid_for(P.n_items), kThreads, 0, s>>>(items_tmp, order_out,
                                                                      P.n_items, P.items);
     CK_LAUNCH();

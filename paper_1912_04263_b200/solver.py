@@ -20,7 +20,8 @@ from . import _abi
 from .problem import (NotPositiveDefiniteError, QpProblem, Settings, SolveDiagnostics,
                       WarmStart, outcome_from_c)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqpcg_b200.so")
+LIB_PATH = os.environ.get("QPCG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                      "libqpcg_b200.so")
 
 _lib = None
 
