@@ -18,6 +18,7 @@
 // ADMM step (the reference streams 4 A-sized matrices + P per step).
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -354,6 +355,11 @@ class Workspace {
     if (v.k[2] != ~0ull) throw InvalidArgument(validation_message(v.k[2]));
   }
 
+  static bool compress_indices() {  // QPCG_COMPRESS=0: uint32 column streams
+    const char* e = std::getenv("QPCG_COMPRESS");
+    return !(e && e[0] == '0');
+  }
+
   // symmetrize_upper, transpose_csr, plans, the original and scaled copies
   void build_structures() {
     const uint32_t n = D.n, m = D.m, annz = D.A.nnz;
@@ -382,6 +388,10 @@ class Workspace {
     D.Ao = DevCsr<T>{m, n, annz, a_v, a_rp, a_ci};
     D.ATo = DevCsr<T>{n, m, annz, ato_v, at_rp, at_ci};
     D.pAT = plan_build<T>(at_rp, n, tmp, s);
+    if (compress_indices()) {  // 16-bit column offsets for the A / A^T streams
+      plan_compress(D.pA, a_ci, annz, n, tmp, s);
+      plan_compress(D.pAT, at_ci, annz, m, tmp, s);
+    }
     D.pPo = D.pP;
     D.pAo = D.pA;
     D.pATo = D.pAT;

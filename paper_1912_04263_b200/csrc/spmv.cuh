@@ -45,8 +45,23 @@ struct SpmvPlan {
   uint2* lrinfo = nullptr;      // [n_long] {partial base, item count}
   T* partials = nullptr;        // [n_partials * kMaxCols]
   uint32_t* counters = nullptr; // [n_long], zero between launches
+  // Compressed column indices of the work items (plan_compress).  An item is
+  // read by its warp 32 consecutive entries of one row at a time (strictly
+  // increasing columns); chunk j of item it has id c0[it] + j and
+  //   cbase[id] = first column,  col[k] = cbase[id] + off16[k]   (span < 2^16)
+  //   cbase[id] = kWide | w,     col    = wide[32 w + lane]        (otherwise)
+  // so the streams carry 2 index bytes per entry instead of 4.  off16 is
+  // indexed by entry position; short rows keep the uint32 ci.
+  uint16_t* off16 = nullptr;
+  uint32_t* cbase = nullptr;
+  uint32_t* c0 = nullptr;
+  uint32_t* wide = nullptr;
+  uint32_t n_chunks = 0, n_wide = 0;
   uint32_t grid() const { return nb_items + nb_short; }
 };
+
+constexpr uint32_t kWide = 0x80000000u;
+constexpr uint32_t kLongItemMean = 256;  // mean entries per item to compress / unroll 8
 
 constexpr int kMaxCols = 3;
 
@@ -89,11 +104,87 @@ struct GatherNone {
   }
 };
 
+__device__ __forceinline__ uint16_t ld_stream(const uint16_t* p) {
+  unsigned short v;
+  asm volatile(QPCG_LD_Q ".u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+
+// One warp, one work item: lanes stride the item 32 entries at a time
+// (coalesced), U strides in flight; the last < 32U entries in one predicated
+// step.  CMP: columns from the compressed index (SpmvPlan::off16).
+template <typename T, int NCOL, class Op, class Gather, int U, bool CMP>
+__device__ __forceinline__ void item_loop(const DevCsr<T>& M, const SpmvPlan<T>& P,
+                                          const Gather& gather, const WorkItem& item, uint32_t c0,
+                                          uint32_t lane, T (&acc)[NCOL]) {
+  const T* __restrict__ val = M.val;
+  const uint32_t* __restrict__ ci = M.ci;
+  uint32_t k = item.beg + lane;
+  const uint32_t end = item.end;
+  uint32_t ch = c0;  // chunk id of the entries at k (CMP)
+  // column of stride u: plain load, or base (shuffled from lane u) + offset
+  auto load_col = [&](uint32_t kk, uint32_t bl, int u, bool ok, uint32_t& c, uint16_t& o,
+                      uint32_t& b) {
+    if (!CMP) {
+      c = ok ? ld_stream(ci + kk) : 0u;
+    } else {
+      b = __shfl_sync(0xffffffffu, bl, u);
+      o = ok ? ld_stream(P.off16 + kk) : (uint16_t)0;
+    }
+  };
+  auto col_of = [&](uint32_t c, uint16_t o, uint32_t b) -> uint32_t {
+    if (!CMP) return c;
+    return (b & kWide) ? __ldg(P.wide + 32u * (b & ~kWide) + lane) : b + o;
+  };
+  for (; k + 32u * (U - 1) < end; k += 32u * U, ch += U) {
+    uint32_t c[U], b[U];
+    uint16_t o[U];
+    T v[U];
+    const uint32_t bl = (CMP && lane < (uint32_t)U) ? __ldg(P.cbase + ch + lane) : 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      v[u] = ld_stream(val + k + 32u * u);
+      if (Op::kNeedsGather) load_col(k + 32u * u, bl, u, true, c[u], o[u], b[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      T g[NCOL];
+      if (Op::kNeedsGather) gather(col_of(c[u], o[u], b[u]), g);
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v[u], Op::kNeedsGather ? g[j] : T(0));
+    }
+  }
+  const uint32_t kf = k - lane;  // first entry of the remaining strides
+  if (kf < end) {  // the < 32U remaining entries: one predicated step, all loads in flight
+    uint32_t c[U], b[U];
+    uint16_t o[U];
+    T v[U];
+    const uint32_t nch = (end - kf + 31u) / 32u;
+    const uint32_t bl = (CMP && lane < nch) ? __ldg(P.cbase + ch + lane) : 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = k + 32u * u < end;
+      v[u] = ok ? ld_stream(val + k + 32u * u) : T(0);
+      if (Op::kNeedsGather) load_col(k + 32u * u, bl, u, ok, c[u], o[u], b[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (k + 32u * u < end) {
+        T g[NCOL];
+        if (Op::kNeedsGather) gather(col_of(c[u], o[u], b[u]), g);
+#pragma unroll
+        for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v[u], Op::kNeedsGather ? g[j] : T(0));
+      }
+    }
+  }
+}
+
 // --------------------------------------------------------------- kernel
-#ifndef QPCG_SPMV_U
-#define QPCG_SPMV_U 8
-#endif
-template <typename T, int NCOL, class Op, class Gather, class Epi, int U = QPCG_SPMV_U>
+// Two builds of the kernel (registers are per kernel, so they are separate
+// kernels rather than branches): U = 8 strides in flight with the compressed
+// index for plans of long items (the latency-bound streams of A / A^T), and
+// U = 4 with uint32 columns for plans of short items, where occupancy wins.
+template <typename T, int NCOL, class Op, class Gather, class Epi, int U, bool CMP>
 __global__ void __launch_bounds__(kThreads) spmv_kernel(DevCsr<T> M, SpmvPlan<T> P, Gather gather,
                                                        Epi epi) {
   // functors load their device-resident scalars (rho, flags) once per thread;
@@ -110,43 +201,8 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(DevCsr<T> M, SpmvPlan<T>
     T acc[NCOL];
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
-    uint32_t k = item.beg + lane;
-    const uint32_t end = item.end;
-    for (; k + 32u * (U - 1) < end; k += 32u * U) {
-      uint32_t c[U];
-      T v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        v[u] = ld_stream(val + k + 32u * u);
-        if (Op::kNeedsGather) c[u] = ld_stream(ci + k + 32u * u);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        T g[NCOL];
-        if (Op::kNeedsGather) gather(c[u], g);
-#pragma unroll
-        for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v[u], Op::kNeedsGather ? g[j] : T(0));
-      }
-    }
-    if (k < end) {  // the < 32U remaining entries: one predicated step, all loads in flight
-      uint32_t c[U];
-      T v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool ok = k + 32u * u < end;
-        v[u] = ok ? ld_stream(val + k + 32u * u) : T(0);
-        if (Op::kNeedsGather) c[u] = ok ? ld_stream(ci + k + 32u * u) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (k + 32u * u < end) {
-          T g[NCOL];
-          if (Op::kNeedsGather) gather(c[u], g);
-#pragma unroll
-          for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v[u], Op::kNeedsGather ? g[j] : T(0));
-        }
-      }
-    }
+    item_loop<T, NCOL, Op, Gather, U, CMP && Op::kNeedsGather>(M, P, gather, item,
+                                                                CMP ? P.c0[it] : 0u, lane, acc);
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) acc[j] = Op::warp(acc[j]);
     if (lane != 0) return;
@@ -198,7 +254,10 @@ template <typename T, int NCOL, class Op, class Gather, class Epi>
 void launch_spmv(const DevCsr<T>& M, const SpmvPlan<T>& P, const Gather& g, const Epi& e,
                  cudaStream_t s) {
   if (P.grid() == 0) return;
-  spmv_kernel<T, NCOL, Op, Gather, Epi><<<P.grid(), kThreads, 0, s>>>(M, P, g, e);
+  if (P.off16 != nullptr)
+    spmv_kernel<T, NCOL, Op, Gather, Epi, 8, true><<<P.grid(), kThreads, 0, s>>>(M, P, g, e);
+  else
+    spmv_kernel<T, NCOL, Op, Gather, Epi, 4, false><<<P.grid(), kThreads, 0, s>>>(M, P, g, e);
   CK_LAUNCH();
 }
 
@@ -306,7 +365,87 @@ void plan_free(SpmvPlan<T>& P) {
   dfree(P.lrinfo);
   dfree(P.partials);
   dfree(P.counters);
+  dfree(P.off16);
+  dfree(P.cbase);
+  dfree(P.c0);
+  dfree(P.wide);
   P = SpmvPlan<T>{};
+}
+
+__global__ void chunk_count_kernel(const WorkItem* items, uint32_t n, uint32_t* nch) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    nch[i] = ceil_div(items[i].end - items[i].beg, 32u);
+}
+
+// warp per item: classify every 32-entry chunk, write offsets / wide columns.
+// fill == 0 only counts the wide chunks (sizing pass).
+__global__ void compress_kernel(const uint32_t* __restrict__ ci, const WorkItem* items, uint32_t n,
+                                const uint32_t* c0, uint16_t* off16, uint32_t* cbase,
+                                uint32_t* wide, uint32_t* n_wide, int fill) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n; it += nw) {
+    const WorkItem w = items[it];
+    uint32_t ch = fill ? c0[it] : 0u;
+    for (uint32_t k0 = w.beg; k0 < w.end; k0 += 32u, ++ch) {
+      const uint32_t cnt = min(32u, w.end - k0);
+      const uint32_t k = k0 + lane;
+      const uint32_t c = lane < cnt ? ci[k] : 0u;
+      const uint32_t first = __shfl_sync(0xffffffffu, c, 0);
+      const uint32_t last = __shfl_sync(0xffffffffu, c, cnt - 1);
+      if (last - first < 65536u) {
+        if (fill) {
+          if (lane < cnt) off16[k] = (uint16_t)(c - first);
+          if (lane == 0) cbase[ch] = first;
+        }
+        continue;
+      }
+      uint32_t slot = 0;
+      if (lane == 0) slot = atomicAdd(n_wide, 1u);
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      if (fill) {
+        wide[32u * slot + lane] = c;
+        if (lane == 0) cbase[ch] = kWide | slot;
+      }
+    }
+  }
+}
+
+// Build the compressed index of P's work items over the structure `ci`.
+// Columns must stay below 2^31 (the wide flag) or the plan stays uncompressed.
+template <typename T>
+void plan_compress(SpmvPlan<T>& P, const uint32_t* ci, uint32_t nnz, uint32_t cols, CubTemp& tmp,
+                   cudaStream_t s) {
+  if (P.n_items == 0 || cols >= kWide) return;
+  // only plans of long items: short items keep the high-occupancy kernel
+  if (uint64_t(nnz) < uint64_t(kLongItemMean) * P.n_items) return;
+  uint32_t* nch;
+  CK(dmalloc(&nch, sizeof(uint32_t) * P.n_items));
+  CK(dmalloc(&P.c0, sizeof(uint32_t) * P.n_items));
+  chunk_count_kernel<<<grid_for(P.n_items), kThreads, 0, s>>>(P.items, P.n_items, nch);
+  CK_LAUNCH();
+  exclusive_scan_u32(nch, P.c0, P.n_items, tmp, s);
+  P.n_chunks = scan_total(nch, P.c0, P.n_items, s);
+  CK(dfree(nch));
+  uint32_t* cnt;
+  CK(dmalloc(&cnt, sizeof(uint32_t)));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), s));
+  const uint32_t g = grid_for(uint64_t(P.n_items) * 32);
+  compress_kernel<<<g, kThreads, 0, s>>>(ci, P.items, P.n_items, P.c0, nullptr, nullptr, nullptr,
+                                          cnt, 0);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(&P.n_wide, cnt, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // (+32: the per-stride base load of a warp may read up to U - 1 ids past
+  // the item's last chunk)
+  CK(dmalloc(&P.off16, sizeof(uint16_t) * (size_t(nnz) + 1)));
+  CK(dmalloc(&P.cbase, sizeof(uint32_t) * (size_t(P.n_chunks) + 32)));
+  CK(dmalloc(&P.wide, sizeof(uint32_t) * 32 * (size_t(P.n_wide) + 1)));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), s));
+  compress_kernel<<<g, kThreads, 0, s>>>(ci, P.items, P.n_items, P.c0, P.off16, P.cbase, P.wide,
+                                          cnt, 1);
+  CK_LAUNCH();
+  CK(dfree(cnt));
 }
 
 // Build the plan for a CSR structure whose row_ptr lives on the device.
