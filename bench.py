@@ -225,7 +225,7 @@ class Engine:
         if rc != 0:
             raise RuntimeError(self.lib.qpcg_last_error(None).decode())
         try:
-            out = np.zeros(6)
+            out = np.zeros(9)
             self.lib.qpcg_bench_kernels.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
             rc = self.lib.qpcg_bench_kernels(ws, reps, out.ctypes.data)
             if rc != 0:
@@ -446,6 +446,13 @@ def main():
                 "pcg_iteration": {"ms": pcg_ms, "bytes": kt[5],
                                   "achieved": kt[5] / (pcg_ms * 1e-3) / 1e9,
                                   "frac": kt[5] / (pcg_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
+                # the engine streams 16-bit compressed column offsets: the bytes
+                # of the formats actually read (achieved/frac above use SURVEY
+                # §8(d)'s 4-byte-index formula, i.e. effective bandwidth)
+                "format_bytes": {"a_pass": kt[6], "at_pass": kt[7], "pcg_iteration": kt[8],
+                                 "at_pass_achieved": kt[7] / (at_ms * 1e-3) / 1e9,
+                                 "at_pass_frac": kt[7] / (at_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                                 "pcg_iteration_frac": kt[8] / (pcg_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
                 "frac_of_nominal_8TBs": achieved / 8000.0}
     line = {"metric": METRIC, "value": ms * 1e-3, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

@@ -41,7 +41,10 @@ int qpcg_debug_operator(qpcg_workspace* ws, const void* x, void* kx, void* diag_
 /* Times `reps` launches each of the PCG-iteration kernels on the workspace's
  * stream with CUDA events.  out[0] ms per A pass (t = rho A p), out[1] ms per
  * A^T pass (Kp = P p + sigma p + A^T t), out[2] ms per whole PCG iteration
- * (5 kernels), out[3..5] algorithmic bytes of each. */
+ * (5 kernels), out[3..5] algorithmic bytes of each (4-byte
+ * column indices), out[6..8] the same with the bytes of the matrix formats
+ * actually streamed (16-bit compressed column offsets where used).
+ * out must hold 9 doubles. */
 int qpcg_bench_kernels(qpcg_workspace* ws, uint32_t reps, double* out);
 
 #ifdef __cplusplus

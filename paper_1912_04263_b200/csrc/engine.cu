@@ -1018,6 +1018,12 @@ class Workspace {
     out[3] = mb(D.A) + S * n + S * m;                    // read A, p; write t
     out[4] = mb(D.AT) + mb(D.P) + S * m + 2 * S * n;     // read A^T, P, t, p; write Kp
     out[5] = mb(D.A) + mb(D.AT) + mb(D.P) + S * (2 * m + 11 * n);
+    // the same with the bytes of the formats actually streamed (compressed
+    // column offsets where the plan has them)
+    const double fa = plan_stream_bytes(D.A, D.pA), fat = plan_stream_bytes(D.AT, D.pAT);
+    out[6] = fa + S * n + S * m;
+    out[7] = fat + mb(D.P) + S * m + 2 * S * n;
+    out[8] = fa + fat + mb(D.P) + S * (2 * m + 11 * n);
   }
 
   // Not in the reference: rescale with the existing D, E, c.

@@ -358,6 +358,15 @@ inline uint32_t scan_total(const uint32_t* in, const uint32_t* ex, uint32_t n, c
   return a + b;
 }
 
+// bytes one SumOp pass streams from the matrix in the plan's format (values,
+// column indices or compressed offsets + chunk bases + chunk ids, row_ptr)
+template <typename T>
+double plan_stream_bytes(const DevCsr<T>& M, const SpmvPlan<T>& P) {
+  const double idx = P.off16 ? 2.0 * M.nnz + 4.0 * P.n_chunks + 4.0 * P.n_items + 128.0 * P.n_wide
+                             : 4.0 * M.nnz;
+  return double(sizeof(T)) * M.nnz + idx + 4.0 * (double(M.rows) + 1);
+}
+
 template <typename T>
 void plan_free(SpmvPlan<T>& P) {
   dfree(P.items);

@@ -34,7 +34,7 @@ for cfg in cfgs:
     eps_d = s.eps_abs + s.eps_rel * max(nm["px"], nm["aty"], nm["q"])
     lib = solver.load_library()
     with solver.Workspace(p, s, device=0) as ws:
-        out = np.zeros(6)
+        out = np.zeros(9)
         lib.qpcg_bench_kernels.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
         lib.qpcg_bench_kernels(ws.ws, 10, out.ctypes.data)
     rec = dict(config=cfg, n=p.n, m=p.m, nnz_A=int(p.a.nnz), nnz_P_upper=int(p.p_upper.nnz),

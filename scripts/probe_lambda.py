@@ -17,7 +17,7 @@ for lam in lams:
           f"pcg[:12]={its[:12]} zero_pcg={sum(1 for i in its if i == 0)}", flush=True)
 lib = solver.load_library()
 with solver.Workspace(p, Settings(lambda_pcg=lams[0]), device=0) as ws:
-    out = np.zeros(6)
+    out = np.zeros(9)
     lib.qpcg_bench_kernels.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
     lib.qpcg_bench_kernels(ws.ws, 20, out.ctypes.data)
 print(f"[{cfg}] kernels: A {out[0]:.4f} ms ({out[3]/out[0]/1e6:.0f} GB/s), A^T {out[1]:.4f} ms ({out[4]/out[1]/1e6:.0f} GB/s), "
