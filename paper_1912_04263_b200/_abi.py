@@ -24,6 +24,7 @@ MEM_HOST = 0
 MEM_DEVICE = 1
 MODE_GRAPH = 0
 MODE_EAGER = 1
+MODE_PERSISTENT = 2
 
 u32p = C.POINTER(C.c_uint32)
 

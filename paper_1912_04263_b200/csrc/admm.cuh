@@ -221,28 +221,31 @@ __device__ __forceinline__ T prow_dot(const DevCsr<T>& P, uint32_t r, const T* x
 // The two gathered columns are packed by k_pack_rhs into one interleaved
 // array so each nnz costs a single 16-byte gather (one L2 sector) instead of
 // three scattered 8-byte ones.
-template <typename T>
+template <typename T, bool NC = true>
 struct GatherRhs {
   const pair_t<T>* g2;
   __device__ __forceinline__ void init() {}
   __device__ __forceinline__ void operator()(uint32_t c, T (&g)[2]) const {
-    const pair_t<T> v = __ldg(g2 + c);
+    const pair_t<T> v = ldv<NC>(g2 + c);
     g[0] = v.x;
     g[1] = v.y;
   }
 };
 // {rho z - y, rho z~} (solver.hpp:351; linsys.hpp:84-85 with A x~ = z~)
 template <typename T>
-__global__ void k_pack_rhs(Dev<T> D) {
-  const Ctl<T>* C = D.ctl;
-  if (C->error) return;
-  const T rho = C->rho;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.m; i += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void pack_rhs_elems(const Dev<T>& D, uint32_t t0, uint32_t stride) {
+  const T rho = D.ctl->rho;
+  for (uint32_t i = t0; i < D.m; i += stride) {
     pair_t<T> v;
     v.x = rho * D.z[i] - D.y[i];
     v.y = rho * D.zt[i];
     D.g2m[i] = v;
   }
+}
+template <typename T>
+__global__ void k_pack_rhs(Dev<T> D) {
+  if (D.ctl->error) return;
+  pack_rhs_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 template <typename T>
 __device__ __forceinline__ void rhs_row(const Dev<T>& D, T sigma, uint32_t r, T s0, T s1) {
@@ -299,12 +302,12 @@ struct EpiKp {
 // z~ = A x~ with the whole m-side ADMM update fused (solver.hpp:360-378);
 // col1 (check iterations only) = A x_new with x_new formed on the fly exactly
 // as solver.hpp:366-367 forms it, feeding compute_residuals' A x (:196).
-template <typename T>
+template <typename T, bool NC = true>
 struct GatherAdmm {  // {x~, x_new} packed by k_pcg_fin
   const pair_t<T>* g2;
   __device__ __forceinline__ void init() {}
   __device__ __forceinline__ void operator()(uint32_t c, T (&g)[2]) const {
-    const pair_t<T> v = __ldg(g2 + c);
+    const pair_t<T> v = ldv<NC>(g2 + c);
     g[0] = v.x;
     g[1] = v.y;
   }
@@ -360,7 +363,7 @@ struct EpiDual {
 
 // certificate vectors formed on the fly (certificate_vectors, solver.hpp:318-325,
 // then normalised: check_primal/dual_infeasible :240-243, :275-278)
-template <typename T>
+template <typename T, bool NC = true>
 struct GatherCertY {  // v_i = ((e_i dy_i) c_inv) * (1/|dy|)
   const T *e, *dy;
   const Ctl<T>* ctl;
@@ -370,17 +373,17 @@ struct GatherCertY {  // v_i = ((e_i dy_i) c_inv) * (1/|dy|)
     s = T(1) / ctl->dy_norm;
   }
   __device__ __forceinline__ void operator()(uint32_t c, T (&g)[1]) const {
-    g[0] = ((__ldg(e + c) * __ldg(dy + c)) * c_inv) * s;
+    g[0] = ((__ldg(e + c) * ldv<NC>(dy + c)) * c_inv) * s;
   }
 };
-template <typename T>
+template <typename T, bool NC = true>
 struct GatherCertX {  // v_i = (d_i dx_i) * (1/|dx|)
   const T *d, *dx;
   const Ctl<T>* ctl;
   T s;
   __device__ __forceinline__ void init() { s = T(1) / ctl->dx_norm; }
   __device__ __forceinline__ void operator()(uint32_t c, T (&g)[1]) const {
-    g[0] = (__ldg(d + c) * __ldg(dx + c)) * s;
+    g[0] = (__ldg(d + c) * ldv<NC>(dx + c)) * s;
   }
 };
 template <typename T>
@@ -478,16 +481,20 @@ __global__ void k_flag_to_scal(Dev<T> D) {
 
 // =====================================================================
 // vector kernels
+//
+// Each kernel is an element body (grid-strided from t0 by stride) plus, for
+// the reductions, a decision taken by one thread from the reduced totals.
+// The stand-alone kernels below wrap them with grid_reduce; the persistent
+// loop (persist.cuh) calls the same bodies and decisions between grid
+// barriers, so both drivers execute the identical arithmetic.
 // =====================================================================
 
 // PCG initialisation (linsys.hpp:203-233) after the fused rhs/r0 pass.
+// v: max|b|, max|r|, r.y, #nonfinite(x~)
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_pcg_init(Dev<T> D, Handles H) {
-  Ctl<T>* C = D.ctl;
-  if (C->error) return;
-  const uint32_t n = D.n;
-  T v[4] = {T(0), T(0), T(0), T(0)};  // max|b|, max|r|, r.y, #nonfinite(x~)
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void pcg_init_elems(const Dev<T>& D, uint32_t t0, uint32_t stride,
+                                               T (&v)[4]) {
+  for (uint32_t i = t0; i < D.n; i += stride) {
     const T ri = D.r[i];
     const T yi = D.dinv[i] * ri;
     D.p[i] = -yi;
@@ -498,9 +505,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(Dev<T> D, Handles H) {
     v[2] += ri * yi;
     if (!isfinite(xi)) v[3] += T(1);
   }
-  T tot[4];
-  if (!grid_reduce<T, 4>(v, 0x3u, D.red, &C->red_counter, tot)) return;
-  if (threadIdx.x != 0) return;
+}
+template <typename T>
+__device__ void pcg_init_decide(Ctl<T>* C, const T (&tot)[4], Handles H) {
   C->k = 0;
   C->improved = 0;
   C->pcg_exit = kPcgConverged;
@@ -522,27 +529,35 @@ __global__ void __launch_bounds__(kThreads) k_pcg_init(Dev<T> D, Handles H) {
   C->pcg_active = active;
   set_cond(H.pcg, active);
 }
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_pcg_init(Dev<T> D, Handles H) {
+  Ctl<T>* C = D.ctl;
+  if (C->error) return;
+  T v[4] = {T(0), T(0), T(0), T(0)};
+  pcg_init_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, v);
+  T tot[4];
+  if (!grid_reduce<T, 4>(v, 0x3u, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  pcg_init_decide(C, tot, H);
+}
 
 // curvature p.Kp and step length (linsys.hpp:246-253)
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_pcg_dot(Dev<T> D) {
-  Ctl<T>* C = D.ctl;
-  if (!C->pcg_active || C->error) return;
-  T v[1] = {T(0)};
+__device__ __forceinline__ void pcg_dot_elems(const Dev<T>& D, uint32_t t0, uint32_t stride,
+                                              T (&v)[1]) {
   if (D.split) {  // Kp = (P p + sigma p) + sum_g A_g^T t_g  (EpiKp semantics)
-    const T sigma = C->sigma;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+    const T sigma = D.ctl->sigma;
+    for (uint32_t i = t0; i < D.n; i += stride) {
       const T kp = kp_row(D, sigma, i, D.part[i]);
       D.kp[i] = kp;
       v[0] += D.p[i] * kp;
     }
   } else {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
-      v[0] += D.p[i] * D.kp[i];
+    for (uint32_t i = t0; i < D.n; i += stride) v[0] += D.p[i] * D.kp[i];
   }
-  T tot[1];
-  if (!grid_reduce<T, 1>(v, 0x0u, D.red, &C->red_counter, tot)) return;
-  if (threadIdx.x != 0) return;
+}
+template <typename T>
+__device__ void pcg_dot_decide(Ctl<T>* C, const T (&tot)[1]) {
   C->curv = tot[0];
   if (tot[0] <= T(0)) {
     C->error = kErrNotPD;  // NotPositiveDefiniteError (linsys.hpp:247-250)
@@ -552,18 +567,24 @@ __global__ void __launch_bounds__(kThreads) k_pcg_dot(Dev<T> D) {
     C->alpha_cg = C->rm / tot[0];
   }
 }
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_pcg_dot(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (!C->pcg_active || C->error) return;
+  T v[1] = {T(0)};
+  pcg_dot_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, v);
+  T tot[1];
+  if (!grid_reduce<T, 1>(v, 0x0u, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  pcg_dot_decide(C, tot);
+}
 
 // x += a p; r += a Kp; y = M^-1 r; r.y; |r|  (linsys.hpp:254-263)
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_pcg_update(Dev<T> D, Handles H) {
-  Ctl<T>* C = D.ctl;
-  if (!C->pcg_active || C->error) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.pcg, 0);
-    return;
-  }
-  const T a = C->alpha_cg;
-  T v[2] = {T(0), T(0)};  // r.y, max|r|
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void pcg_update_elems(const Dev<T>& D, uint32_t t0, uint32_t stride,
+                                                 T (&v)[2]) {
+  const T a = D.ctl->alpha_cg;
+  for (uint32_t i = t0; i < D.n; i += stride) {
     D.xt[i] += a * D.p[i];
     const T ri = D.r[i] + a * D.kp[i];
     D.r[i] = ri;
@@ -571,9 +592,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(Dev<T> D, Handles H) {
     v[0] += ri * yi;
     v[1] = smax(v[1], tabs(ri));
   }
-  T tot[2];
-  if (!grid_reduce<T, 2>(v, 0x2u, D.red, &C->red_counter, tot)) return;
-  if (threadIdx.x != 0) return;
+}
+template <typename T>
+__device__ void pcg_update_decide(Ctl<T>* C, const T (&tot)[2], Handles H) {
   const T rm_next = tot[0];
   C->beta = rm_next / C->rm;
   C->rm = rm_next;
@@ -593,33 +614,49 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(Dev<T> D, Handles H) {
   C->pcg_active = active;
   set_cond(H.pcg, active);
 }
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_pcg_update(Dev<T> D, Handles H) {
+  Ctl<T>* C = D.ctl;
+  if (!C->pcg_active || C->error) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.pcg, 0);
+    return;
+  }
+  T v[2] = {T(0), T(0)};
+  pcg_update_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, v);
+  T tot[2];
+  if (!grid_reduce<T, 2>(v, 0x2u, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  pcg_update_decide(C, tot, H);
+}
 
 // p = -y + beta p; best-iterate copy (linsys.hpp:259, 264-267)
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_pcg_pupdate(Dev<T> D) {
+__device__ __forceinline__ void pcg_pupdate_elems(const Dev<T>& D, uint32_t t0, uint32_t stride) {
   const Ctl<T>* C = D.ctl;
-  if (C->error) return;
-  if (C->k == 0) return;  // nothing to do before the first update
+  if (C->error || C->k == 0) return;  // nothing to do before the first update
   const T beta = C->beta;
   const bool imp = C->improved;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+  for (uint32_t i = t0; i < D.n; i += stride) {
     const T yi = D.dinv[i] * D.r[i];
     D.p[i] = -yi + beta * D.p[i];
     if (imp) D.best[i] = D.xt[i];
   }
+}
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_pcg_pupdate(Dev<T> D) {
+  pcg_pupdate_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 // PCG exit: x~ = 0 (b == 0) or best iterate (cap); PcgCall record.
 // also packs {x~, x_new} for the z~ pass; x_new = alpha x~ + (1 - alpha) x is
 // formed exactly as solver.hpp:366-367 (only needed on check iterations).
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_pcg_fin(Dev<T> D) {
-  Ctl<T>* C = D.ctl;
-  if (C->error) return;
+__device__ __forceinline__ void pcg_fin_elems(const Dev<T>& D, uint32_t t0, uint32_t stride) {
+  const Ctl<T>* C = D.ctl;
   const uint32_t ex = C->pcg_exit;
   const bool two = ((C->iter + 1) % C->check_interval) == 0;
   const T alpha = C->alpha, oma = T(1) - alpha;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
+  for (uint32_t i = t0; i < D.n; i += stride) {
     T xt = D.xt[i];
     if (ex != kPcgConverged) {
       xt = ex == kPcgZeroRhs ? T(0) : D.best[i];
@@ -630,24 +667,51 @@ __global__ void __launch_bounds__(kThreads) k_pcg_fin(Dev<T> D) {
     v.y = two ? alpha * xt + oma * D.x[i] : T(0);
     D.g2n[i] = v;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    C->pcg_total += C->k;
-    if (C->n_calls < C->diag_cap) {
-      DiagRec<T> rec;
-      rec.admm_iter = C->iter + 1;
-      rec.iterations = C->k;
-      rec.eps = C->pcg_eps;
-      rec.rp = C->last_rp;
-      rec.rd = C->last_rd;
-      rec.converged = ex != kPcgCap;
-      rec.pad = 0;
-      D.calls[C->n_calls] = rec;
-    }
-    C->n_calls += 1;
+}
+template <typename T>
+__device__ void pcg_fin_book(const Dev<T>& D, bool record) {
+  Ctl<T>* C = D.ctl;
+  C->pcg_total += C->k;
+  if (record && C->n_calls < C->diag_cap) {
+    DiagRec<T> rec;
+    rec.admm_iter = C->iter + 1;
+    rec.iterations = C->k;
+    rec.eps = C->pcg_eps;
+    rec.rp = C->last_rp;
+    rec.rd = C->last_rd;
+    rec.converged = C->pcg_exit != kPcgCap;
+    rec.pad = 0;
+    D.calls[C->n_calls] = rec;
   }
+  C->n_calls += 1;
+}
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_pcg_fin(Dev<T> D) {
+  if (D.ctl->error) return;
+  pcg_fin_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+  if (blockIdx.x == 0 && threadIdx.x == 0) pcg_fin_book(D, true);
 }
 
 // n-side relaxation (solver.hpp:366-368, 377) and the iteration counter.
+template <typename T>
+__device__ __forceinline__ void xupdate_elems(const Dev<T>& D, uint32_t t0, uint32_t stride) {
+  const T alpha = D.ctl->alpha, oma = T(1) - alpha;
+  for (uint32_t i = t0; i < D.n; i += stride) {
+    const T xp = D.x[i];
+    const T xn = alpha * D.xt[i] + oma * xp;
+    D.x[i] = xn;
+    D.dx[i] = xn - xp;
+  }
+}
+template <typename T>
+__device__ void xupdate_book(Ctl<T>* C, Handles H) {
+  const uint32_t it = C->iter + 1;
+  C->iter = it;
+  C->residuals_current = 0;
+  const uint32_t chk = (it % C->check_interval) == 0;
+  C->is_check = chk;
+  set_cond(H.chk, chk);
+}
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_xupdate(Dev<T> D, Handles H) {
   Ctl<T>* C = D.ctl;
@@ -655,27 +719,16 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(Dev<T> D, Handles H) {
     if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.chk, 0);
     return;
   }
-  const T alpha = C->alpha, oma = T(1) - alpha;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
-    const T xp = D.x[i];
-    const T xn = alpha * D.xt[i] + oma * xp;
-    D.x[i] = xn;
-    D.dx[i] = xn - xp;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint32_t it = C->iter + 1;
-    C->iter = it;
-    C->residuals_current = 0;
-    const uint32_t chk = (it % C->check_interval) == 0;
-    C->is_check = chk;
-    set_cond(H.chk, chk);
-  }
+  xupdate_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+  if (blockIdx.x == 0 && threadIdx.x == 0) xupdate_book(C, H);
 }
 
 // Residual bookkeeping, adaptive eps and the termination test from the 14
 // reduced norms (solver.hpp:205-206, 222-230, 468-476; linsys.hpp:170-179).
+// record: write the check-iteration diagnostics (one writer).
 template <typename T>
-__device__ void residuals_decide(Dev<T> D, const T (&tot)[14], int mode, Handles H) {
+__device__ void residuals_decide(Dev<T> D, const T (&tot)[14], int mode, Handles H,
+                                 bool record = true) {
   Ctl<T>* C = D.ctl;
   const T c_inv = C->c_inv;
   C->rp_s = tot[0];
@@ -702,7 +755,7 @@ __device__ void residuals_decide(Dev<T> D, const T (&tot)[14], int mode, Handles
     C->last_rd = C->rd_s;
   }
   if (mode == 0) {
-    if (C->n_checks < C->diag_cap) D.checks[C->n_checks] = C->iter;
+    if (record && C->n_checks < C->diag_cap) D.checks[C->n_checks] = C->iter;
     C->n_checks += 1;
     // check_optimal (solver.hpp:222-230) on unscaled norms
     const T eps_prim = C->eps_abs + C->eps_rel * smax(C->ax_o, C->z_o);
@@ -727,22 +780,13 @@ __device__ void residuals_decide(Dev<T> D, const T (&tot)[14], int mode, Handles
 
 // Residual norms (solver.hpp:205-206, 468-475) + termination (:476-495 start).
 // mode 0: loop check; mode 1: initial residuals (eps only); mode 2: final.
+// v: 0 rp_s 1 ax_s 2 z_s 3 rp_o 4 ax_o 5 z_o 6 dy_norm | 7 rd_s 8 px_s 9 aty_s
+//    10 rd_o' 11 px_o' 12 aty_o' 13 dx_norm  (all maxima)
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Handles H) {
-  Ctl<T>* C = D.ctl;
-  if (C->error) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.inf, 0);
-    return;
-  }
-  const uint32_t n = D.n, m = D.m;
-  const T c_inv = C->c_inv;
-  // 0 rp_s 1 ax_s 2 z_s 3 rp_o 4 ax_o 5 z_o 6 dy_norm | 7 rd_s 8 px_s 9 aty_s
-  // 10 rd_o' 11 px_o' 12 aty_o' 13 dx_norm
-  T v[14];
-#pragma unroll
-  for (int q = 0; q < 14; ++q) v[q] = T(0);
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+__device__ __forceinline__ void residuals_elems(const Dev<T>& D, uint32_t t0, uint32_t stride,
+                                                T (&v)[14]) {
+  const T c_inv = D.ctl->c_inv;
+  for (uint32_t i = t0; i < D.m; i += stride) {
     const T ax = D.ax[i], z = D.z[i], ei = D.e_inv[i];
     const T rp = ax - z;
     v[0] = smax(v[0], tabs(rp));
@@ -753,7 +797,7 @@ __global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Hand
     v[5] = smax(v[5], tabs(z * ei));
     v[6] = smax(v[6], tabs((D.e[i] * D.dy[i]) * c_inv));
   }
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  for (uint32_t i = t0; i < D.n; i += stride) {
     const T rd = D.rdual[i], px = D.px[i], aty = D.aty[i], di = D.d_inv[i];
     v[7] = smax(v[7], tabs(rd));
     v[8] = smax(v[8], tabs(px));
@@ -763,6 +807,18 @@ __global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Hand
     v[12] = smax(v[12], tabs(aty * di));
     v[13] = smax(v[13], tabs(D.d[i] * D.dx[i]));
   }
+}
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Handles H) {
+  Ctl<T>* C = D.ctl;
+  if (C->error) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.inf, 0);
+    return;
+  }
+  T v[14];
+#pragma unroll
+  for (int q = 0; q < 14; ++q) v[q] = T(0);
+  residuals_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, v);
   T tot[14];
   if (!grid_reduce<T, 14>(v, 0x3fffu, D.red, &C->red_counter, tot)) return;
   if (threadIdx.x != 0) return;
@@ -789,25 +845,16 @@ __global__ void k_residuals_decide(Dev<T> D, int mode, Handles H) {
 // the reference, far fewer matrix streams on ordinary (feasible) solves.
 // Stage 1: the vector parts — support sum and infinite-bound tests of the
 // primal certificate (:248-263), q'v of the dual one (:281).
+// v: support (sum), bad (max; a count across row blocks), q'v (sum)
 template <typename T>
-__device__ void infeas_vec_decide(Ctl<T>* C, const T (&tot)[3]) {
-  C->support = tot[0];
-  C->qv = tot[2];
-  if (C->need_pinf && !(tot[1] == T(0) && tot[0] < C->eps_pinf)) C->need_pinf = 0;
-  if (C->need_dinf && !(tot[2] < C->eps_dinf)) C->need_dinf = 0;
-}
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_infeas_vec(Dev<T> D) {
-  Ctl<T>* C = D.ctl;
-  if (C->error || !C->inf_branch) return;
-  const uint32_t n = D.n, m = D.m;
+__device__ __forceinline__ void infeas_vec_elems(const Dev<T>& D, uint32_t t0, uint32_t stride,
+                                                 T (&v)[3]) {
+  const Ctl<T>* C = D.ctl;
   const T c_inv = C->c_inv, eps_p = C->eps_pinf;
   const T sy = C->need_pinf ? T(1) / C->dy_norm : T(0);
   const T sx = C->need_dinf ? T(1) / C->dx_norm : T(0);
-  T v[3] = {T(0), T(0), T(0)};  // support, bad (max), q'v
-  const uint32_t stride = gridDim.x * blockDim.x;
   if (C->need_pinf) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    for (uint32_t i = t0; i < D.m; i += stride) {
       const T vi = ((D.e[i] * D.dy[i]) * c_inv) * sy;
       const T neg = smin(vi, T(0)), pos = smax(vi, T(0));
       const T li = D.l_o[i], ui = D.u_o[i];
@@ -825,9 +872,22 @@ __global__ void __launch_bounds__(kThreads) k_infeas_vec(Dev<T> D) {
   }
   // (n-vectors are replicated across row blocks: block 0 alone sums q'v)
   if (C->need_dinf && (!D.split || D.sh_index == 0)) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-      v[2] += D.q_o[i] * ((D.d[i] * D.dx[i]) * sx);
+    for (uint32_t i = t0; i < D.n; i += stride) v[2] += D.q_o[i] * ((D.d[i] * D.dx[i]) * sx);
   }
+}
+template <typename T>
+__device__ void infeas_vec_decide(Ctl<T>* C, const T (&tot)[3]) {
+  C->support = tot[0];
+  C->qv = tot[2];
+  if (C->need_pinf && !(tot[1] == T(0) && tot[0] < C->eps_pinf)) C->need_pinf = 0;
+  if (C->need_dinf && !(tot[2] < C->eps_dinf)) C->need_dinf = 0;
+}
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_infeas_vec(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (C->error || !C->inf_branch) return;
+  T v[3] = {T(0), T(0), T(0)};
+  infeas_vec_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, v);
   T tot[3];
   if (!grid_reduce<T, 3>(v, 0x2u, D.red, &C->red_counter, tot)) return;
   if (threadIdx.x != 0) return;
@@ -850,19 +910,21 @@ __global__ void k_infeas_vec_decide(Dev<T> D) {
 
 // Stage 2 (after the P_orig pass): |P v| <= eps (:280)
 template <typename T>
+__device__ void infeas_mid_decide(Ctl<T>* C) {
+  if (C->need_dinf && bits_to_value(C->pv_inf_bits, T(0)) > C->eps_dinf) C->need_dinf = 0;
+}
+template <typename T>
 __global__ void k_infeas_mid(Dev<T> D) {
   Ctl<T>* C = D.ctl;
   if (C->error || !C->inf_branch) return;
-  if (C->need_dinf && bits_to_value(C->pv_inf_bits, T(0)) > C->eps_dinf) C->need_dinf = 0;
+  infeas_mid_decide(C);
 }
 
 // Stage 3: decision after the A_orig^T (primal) and A_orig (dual) passes
 template <typename T>
-__global__ void k_infeas(Dev<T> D) {
-  Ctl<T>* C = D.ctl;
-  if (C->error || !C->inf_branch) return;
+__device__ void infeas_decide(Ctl<T>* C, bool dual_rows_bad) {
   const bool primal = C->need_pinf && !(bits_to_value(C->atv_inf_bits, T(0)) > C->eps_pinf);
-  const bool dual = C->need_dinf && (D.split ? D.shsc[0] == T(0) : C->dinf_bad == 0);
+  const bool dual = C->need_dinf && !dual_rows_bad;
   if (primal) {
     C->status = 1;
     C->done = 1;
@@ -871,46 +933,30 @@ __global__ void k_infeas(Dev<T> D) {
     C->done = 1;
   }
 }
+template <typename T>
+__global__ void k_infeas(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (C->error || !C->inf_branch) return;
+  infeas_decide(C, D.split ? D.shsc[0] != T(0) : C->dinf_bad != 0);
+}
 
 // decides the rho branch (solver.hpp:498)
 template <typename T>
-__global__ void k_rho_flag(Dev<T> D, Handles H) {
-  Ctl<T>* C = D.ctl;
+__device__ void rho_flag_book(Ctl<T>* C, Handles H) {
   const uint32_t f = !C->error && !C->done && (C->iter % C->rho_interval) == 0;
   C->rho_branch = f;
   C->n_rho_branch += f;
   set_cond(H.rho, f);
 }
-
 template <typename T>
-__device__ void rho_decide(Dev<T> D, T z_inf);
-
-// adapt_rho (solver.hpp:302-314) from the last residuals and the current |z|
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_rho(Dev<T> D) {
-  Ctl<T>* C = D.ctl;
-  if (!C->rho_branch) return;
-  T v[1] = {T(0)};
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.m; i += gridDim.x * blockDim.x)
-    v[0] = smax(v[0], tabs(D.z[i]));
-  T tot[1];
-  if (!grid_reduce<T, 1>(v, 0x1u, D.red, &C->red_counter, tot)) return;
-  if (threadIdx.x != 0) return;
-  if (D.split) {  // this block's max |z|, combined by a max
-    D.shsc[0] = tot[0];
-    return;
-  }
-  rho_decide(D, tot[0]);
+__global__ void k_rho_flag(Dev<T> D, Handles H) {
+  rho_flag_book(D.ctl, H);
 }
 
+// adapt_rho (solver.hpp:302-314) from the last residuals and the current |z|.
+// record: write the rho-update diagnostics (one writer).
 template <typename T>
-__global__ void k_rho_decide(Dev<T> D) {
-  if (threadIdx.x != 0 || !D.ctl->rho_branch) return;
-  rho_decide(D, D.shsc[0]);
-}
-
-template <typename T>
-__device__ void rho_decide(Dev<T> D, T z_inf) {
+__device__ void rho_decide(Dev<T> D, T z_inf, bool record = true) {
   Ctl<T>* C = D.ctl;
   const T fl = T(1e-10);
   const T rel_prim = C->last_rp / smax(smax(C->ax_s, z_inf), fl);
@@ -926,7 +972,7 @@ __device__ void rho_decide(Dev<T> D, T z_inf) {
     if (next < T(1e-6)) next = T(1e-6);
     else if (T(1e6) < next) next = T(1e6);
   }
-  if (C->n_rho < C->diag_cap) {
+  if (record && C->n_rho < C->diag_cap) {
     RhoRec<T> rr;
     rr.admm_iter = C->iter;
     rr.pad = 0;
@@ -943,25 +989,57 @@ __device__ void rho_decide(Dev<T> D, T z_inf) {
   C->rho = next;
   C->rho_update_count += 1;
 }
+template <typename T>
+__device__ __forceinline__ void rho_elems(const Dev<T>& D, uint32_t t0, uint32_t stride, T (&v)[1]) {
+  for (uint32_t i = t0; i < D.m; i += stride) v[0] = smax(v[0], tabs(D.z[i]));
+}
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_rho(Dev<T> D) {
+  Ctl<T>* C = D.ctl;
+  if (!C->rho_branch) return;
+  T v[1] = {T(0)};
+  rho_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, v);
+  T tot[1];
+  if (!grid_reduce<T, 1>(v, 0x1u, D.red, &C->red_counter, tot)) return;
+  if (threadIdx.x != 0) return;
+  if (D.split) {  // this block's max |z|, combined by a max
+    D.shsc[0] = tot[0];
+    return;
+  }
+  rho_decide(D, tot[0]);
+}
+template <typename T>
+__global__ void k_rho_decide(Dev<T> D) {
+  if (threadIdx.x != 0 || !D.ctl->rho_branch) return;
+  rho_decide(D, D.shsc[0]);
+}
 
 // Jacobi diagonal (linsys.hpp:142-146): (diag_p + sigma) + rho diag_ata
+template <typename T>
+__device__ __forceinline__ void precond_elems(const Dev<T>& D, uint32_t t0, uint32_t stride) {
+  const T sigma = D.ctl->sigma, rho = D.ctl->rho;
+  for (uint32_t i = t0; i < D.n; i += stride) {
+    const T dm = D.diag_p[i] + sigma + rho * D.diag_ata[i];
+    D.dinv[i] = T(1) / dm;
+  }
+}
 template <typename T>
 __global__ void k_precond(Dev<T> D, int force) {
   const Ctl<T>* C = D.ctl;
   if (!force && !C->rho_branch) return;
   if (C->error) return;
-  const T sigma = C->sigma, rho = C->rho;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x) {
-    const T dm = D.diag_p[i] + sigma + rho * D.diag_ata[i];
-    D.dinv[i] = T(1) / dm;
-  }
+  precond_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 // loop condition (solver.hpp:444)
 template <typename T>
+__device__ __forceinline__ uint32_t admm_go(const Ctl<T>* C) {
+  return !C->done && !C->error && C->iter < C->max_iter;
+}
+template <typename T>
 __global__ void k_admm_cond(Dev<T> D, Handles H) {
   Ctl<T>* C = D.ctl;
-  const uint32_t go = !C->done && !C->error && C->iter < C->max_iter;
+  const uint32_t go = admm_go(C);
   C->admm_continue = go;
   set_cond(H.admm, go);
 }

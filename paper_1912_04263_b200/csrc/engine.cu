@@ -28,6 +28,7 @@
 #include "../../include/qpcg_b200_ops.h"
 #include "admm.cuh"
 #include "comm.cuh"
+#include "persist.cuh"
 #include "setup.cuh"
 
 namespace qpcg_b200 {
@@ -727,6 +728,36 @@ class Workspace {
     CK(cudaGraphInstantiate(&exec, graph, 0));
   }
 
+  // ------------------------------------------------- persistent loop
+  // The small-problem path (persist.cuh): the whole loop in one cooperative
+  // kernel.  Chosen automatically in graph mode while A fits the L2 budget.
+  T* persist_part = nullptr;
+  static uint64_t persist_max_nnz() {
+    const char* e = std::getenv("QPCG_PERSIST_MAX_NNZ");
+    return e ? std::strtoull(e, nullptr, 10) : 2000000ull;
+  }
+  bool use_persistent() const {
+    if (D.split) return false;
+    if (opt.mode == QPCG_MODE_PERSISTENT) return true;
+    return opt.mode == QPCG_MODE_GRAPH && uint64_t(D.A.nnz) + D.P.nnz <= persist_max_nnz();
+  }
+  void run_persistent() {
+    if (!persist_part) persist_part = alloc<T>(2 * kMaxQ * kMaxVirtual);
+    static int max_grid = 0;  // co-resident blocks (same device model for every workspace)
+    if (max_grid == 0) {
+      int per_sm = 0, sms = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_admm_persistent<T>, kThreads, 0));
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      max_grid = std::max(1, per_sm) * sms;
+    }
+    const int grid = max_grid;  // measured: more co-resident blocks is faster at every size
+    PersistBufs<T> B{persist_part, D.ctl};
+    void* args[] = {(void*)&D, (void*)&B};
+    CK(cudaLaunchCooperativeKernel((const void*)k_admm_persistent<T>, dim3(grid), dim3(kThreads), args,
+                                   0, s));
+    CK_LAUNCH();
+  }
+
   // ------------------------------------------------------- eager loop
   void run_eager() {
     Handles H{};
@@ -816,6 +847,8 @@ class Workspace {
     enq_residuals_fresh(1);
     if (opt.mode == QPCG_MODE_EAGER) {
       run_eager();
+    } else if (use_persistent()) {
+      run_persistent();
     } else {
       if (!exec) {
         const uint64_t b0 = g_launches;
@@ -843,7 +876,7 @@ class Workspace {
     download(y, D.yo, sizeof(T) * D.m);
     const bool has_cert = hc.status == 1 || hc.status == 2;
     uint64_t launches = g_launches - l0 - graph_build;
-    if (opt.mode != QPCG_MODE_EAGER)  // kernels executed inside the graph
+    if (opt.mode != QPCG_MODE_EAGER && !use_persistent())  // kernels executed inside the graph
       launches += 8ull * hc.iter + 5ull * hc.pcg_total + 2ull * hc.n_checks + 6ull * hc.n_inf +
                   2ull * hc.n_rho_branch;
     if (has_cert) download(cert, D.cert, sizeof(T) * (hc.status == 1 ? D.m : D.n));

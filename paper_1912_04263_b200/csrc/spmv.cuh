@@ -89,11 +89,19 @@ struct MaxAbsOp {
 };
 
 // gather helpers
-template <typename T>
+// gathered loads: read-only path (NC) in the stand-alone kernels; plain
+// (coherent) loads inside the persistent loop, where the gathered vectors are
+// rewritten between grid barriers of the same kernel
+template <bool NC, typename V>
+__device__ __forceinline__ V ldv(const V* p) {
+  if constexpr (NC) return __ldg(p);
+  else return *p;
+}
+template <typename T, bool NC = true>
 struct GatherVec {  // x[c]
   const T* __restrict__ x;
   __device__ __forceinline__ void init() {}
-  __device__ __forceinline__ void operator()(uint32_t c, T (&g)[1]) const { g[0] = __ldg(x + c); }
+  __device__ __forceinline__ void operator()(uint32_t c, T (&g)[1]) const { g[0] = ldv<NC>(x + c); }
 };
 template <typename T, int N>
 struct GatherNone {
@@ -180,6 +188,66 @@ __device__ __forceinline__ void item_loop(const DevCsr<T>& M, const SpmvPlan<T>&
 }
 
 // --------------------------------------------------------------- kernel
+// One work item (one warp; lane 0 runs the epilogue).  Multi-item rows
+// publish a partial; the last item to arrive combines them in item order
+// (deterministic).
+template <typename T, int NCOL, class Op, class Gather, class Epi, int U, bool CMP>
+__device__ __forceinline__ void spmv_item(const DevCsr<T>& M, const SpmvPlan<T>& P,
+                                          const Gather& gather, const Epi& epi, uint32_t it,
+                                          uint32_t lane) {
+  const WorkItem item = P.items[it];
+  T acc[NCOL];
+#pragma unroll
+  for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
+  item_loop<T, NCOL, Op, Gather, U, CMP && Op::kNeedsGather>(M, P, gather, item,
+                                                              CMP ? P.c0[it] : 0u, lane, acc);
+#pragma unroll
+  for (int j = 0; j < NCOL; ++j) acc[j] = Op::warp(acc[j]);
+  if (lane != 0) return;
+  if (item.lr == 0xffffffffu) {
+    epi(item.row, acc);
+    return;
+  }
+  const uint2 info = P.lrinfo[item.lr];
+  const uint32_t chunk = (item.beg - M.rp[item.row]) / kChunk;
+  T* part = P.partials + (size_t)(info.x + chunk) * kMaxCols;
+#pragma unroll
+  for (int j = 0; j < NCOL; ++j) part[j] = acc[j];
+  __threadfence();
+  const uint32_t prev = atomicAdd(P.counters + item.lr, 1u);
+  if (prev != info.y - 1) return;
+  __threadfence();
+  T tot[NCOL];
+#pragma unroll
+  for (int j = 0; j < NCOL; ++j) tot[j] = T(0);
+  for (uint32_t q = 0; q < info.y; ++q) {
+    const T* pp = P.partials + (size_t)(info.x + q) * kMaxCols;
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) tot[j] = Op::join(tot[j], __ldcg(pp + j));
+  }
+  P.counters[item.lr] = 0u;
+  epi(item.row, tot);
+}
+
+// One short row (<= kShortRowMax nnz), one thread, left to right: bit-exact.
+template <typename T, int NCOL, class Op, class Gather, class Epi>
+__device__ __forceinline__ void spmv_short(const DevCsr<T>& M, const SpmvPlan<T>& P,
+                                           const Gather& gather, const Epi& epi, uint32_t idx) {
+  const uint32_t r = P.short_rows[idx];
+  const uint32_t b = __ldg(M.rp + r), e = __ldg(M.rp + r + 1);
+  T acc[NCOL];
+#pragma unroll
+  for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
+  for (uint32_t k = b; k < e; ++k) {
+    const T v = ld_stream(M.val + k);
+    T g[NCOL];
+    if (Op::kNeedsGather) gather(ld_stream(M.ci + k), g);
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v, Op::kNeedsGather ? g[j] : T(0));
+  }
+  epi(r, acc);
+}
+
 // Two builds of the kernel (registers are per kernel, so they are separate
 // kernels rather than branches): U = 8 strides in flight with the compressed
 // index for plans of long items (the latency-bound streams of A / A^T), and
@@ -191,62 +259,12 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(DevCsr<T> M, SpmvPlan<T>
   // an inactive epilogue (e.g. a skipped certificate pass) exits immediately
   if (!epi.init()) return;
   gather.init();
-  const T* __restrict__ val = M.val;
-  const uint32_t* __restrict__ ci = M.ci;
   if (blockIdx.x < P.nb_items) {
-    const uint32_t lane = threadIdx.x & 31;
     const uint32_t it = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    if (it >= P.n_items) return;
-    const WorkItem item = P.items[it];
-    T acc[NCOL];
-#pragma unroll
-    for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
-    item_loop<T, NCOL, Op, Gather, U, CMP && Op::kNeedsGather>(M, P, gather, item,
-                                                                CMP ? P.c0[it] : 0u, lane, acc);
-#pragma unroll
-    for (int j = 0; j < NCOL; ++j) acc[j] = Op::warp(acc[j]);
-    if (lane != 0) return;
-    if (item.lr == 0xffffffffu) {
-      epi(item.row, acc);
-      return;
-    }
-    // multi-item row: publish the partial, the last item to finish combines
-    // all partials in item order (deterministic).
-    const uint2 info = P.lrinfo[item.lr];
-    const uint32_t chunk = (item.beg - M.rp[item.row]) / kChunk;
-    T* part = P.partials + (size_t)(info.x + chunk) * kMaxCols;
-#pragma unroll
-    for (int j = 0; j < NCOL; ++j) part[j] = acc[j];
-    __threadfence();
-    const uint32_t prev = atomicAdd(P.counters + item.lr, 1u);
-    if (prev != info.y - 1) return;
-    __threadfence();
-    T tot[NCOL];
-#pragma unroll
-    for (int j = 0; j < NCOL; ++j) tot[j] = T(0);
-    for (uint32_t q = 0; q < info.y; ++q) {
-      const T* pp = P.partials + (size_t)(info.x + q) * kMaxCols;
-#pragma unroll
-      for (int j = 0; j < NCOL; ++j) tot[j] = Op::join(tot[j], __ldcg(pp + j));
-    }
-    P.counters[item.lr] = 0u;
-    epi(item.row, tot);
+    if (it < P.n_items) spmv_item<T, NCOL, Op, Gather, Epi, U, CMP>(M, P, gather, epi, it, threadIdx.x & 31);
   } else {
     const uint32_t idx = (blockIdx.x - P.nb_items) * kThreads + threadIdx.x;
-    if (idx >= P.n_short) return;
-    const uint32_t r = P.short_rows[idx];
-    const uint32_t b = __ldg(M.rp + r), e = __ldg(M.rp + r + 1);
-    T acc[NCOL];
-#pragma unroll
-    for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
-    for (uint32_t k = b; k < e; ++k) {
-      const T v = ld_stream(val + k);
-      T g[NCOL];
-      if (Op::kNeedsGather) gather(ld_stream(ci + k), g);
-#pragma unroll
-      for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v, Op::kNeedsGather ? g[j] : T(0));
-    }
-    epi(r, acc);
+    if (idx < P.n_short) spmv_short<T, NCOL, Op, Gather, Epi>(M, P, gather, epi, idx);
   }
 }
 

@@ -86,7 +86,7 @@ def make_options(device: int = -1, mode: str = "graph", record_diagnostics: bool
     o = _abi.Options()
     o.device = device
     o.input_memory = _abi.MEM_DEVICE if device_memory else _abi.MEM_HOST
-    o.mode = _abi.MODE_EAGER if mode == "eager" else _abi.MODE_GRAPH
+    o.mode = {"eager": _abi.MODE_EAGER, "persistent": _abi.MODE_PERSISTENT}.get(mode, _abi.MODE_GRAPH)
     o.record_diagnostics = 1 if record_diagnostics else 0
     o.virtual_shards = max(1, int(shards))
     if nccl is not None:
