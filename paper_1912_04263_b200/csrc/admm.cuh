@@ -312,7 +312,10 @@ struct GatherAdmm {  // {x~, x_new} packed by k_pcg_fin
     g[1] = v.y;
   }
 };
-template <typename T>
+// NCOL 2 on check iterations (col 1 = A x_new for the residuals), NCOL 1 (x~
+// only, an 8-byte gather) otherwise.  Both builds are launched; each returns
+// at init() unless it is the one this iteration needs (gate: the pass's NCOL).
+template <typename T, int NCOL = 2>
 struct EpiAdmm {
   Dev<T> D;
   T alpha, one_m_alpha, rho;
@@ -322,9 +325,9 @@ struct EpiAdmm {
     one_m_alpha = T(1) - alpha;
     rho = D.ctl->rho;
     two = ((D.ctl->iter + 1) % D.ctl->check_interval) == 0;
-    return D.ctl->error == 0;
+    return D.ctl->error == 0 && two == (NCOL == 2);
   }
-  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[2]) const {
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[NCOL]) const {
     const T zt = s[0];
     const T zp = D.z[r], yp = D.y[r];
     const T w = alpha * zt + one_m_alpha * zp + yp / rho;
@@ -334,7 +337,7 @@ struct EpiAdmm {
     D.z[r] = zn;
     D.y[r] = yn;
     D.dy[r] = yn - yp;
-    if (two) D.ax[r] = s[1];
+    if constexpr (NCOL == 2) D.ax[r] = s[1];
   }
 };
 

@@ -119,6 +119,12 @@ class Workspace {
   bool have_counted_setup = false;
 
   ~Workspace() {
+    if (s_side) {
+      cudaStreamSynchronize(s_side);
+      cudaStreamDestroy(s_side);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     {
@@ -464,26 +470,41 @@ class Workspace {
         ruiz_scal + 4);
     CK_LAUNCH();
   }
+  // The cost scaling (the sequential mean of P's row norms, |q|, gamma, P and
+  // q *= gamma) only depends on P and q: it runs on a side stream while the
+  // main stream scales A and A^T (the mean is a latency-bound dependent chain).
+  cudaStream_t s_side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void ruiz_scale() {
     const uint32_t n = D.n;
+    if (!s_side) {
+      CK(cudaStreamCreateWithFlags(&s_side, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
     plan_visit(D.P, D.pP, ScaleRowColFn<T>{D.P.val, D.P.ci, rz_dx, rz_dx}, s);
-    plan_visit(D.A, D.pA, ScaleRowColFn<T>{D.A.val, D.A.ci, rz_dz, rz_dx}, s);
-    plan_visit(D.AT, D.pAT, ScaleRowColFn<T>{D.AT.val, D.AT.ci, rz_dx, rz_dz}, s);
-    // cost scaling
+    row_inf_norms(D.P, D.pP, rz_pn, s);
+    CK(cudaEventRecord(ev_fork, s));
+    CK(cudaStreamWaitEvent(s_side, ev_fork, 0));
+    // cost scaling (scaling.hpp:156-162), side stream
     T* mean = ruiz_scal + 0;
     T* qinf = ruiz_scal + 1;
     T* gamma = ruiz_scal + 2;
     T* cc = ruiz_scal + 3;
-    row_inf_norms(D.P, D.pP, rz_pn, s);
-    ordered_mean_kernel<T><<<1, 256, 0, s>>>(rz_pn, p_rows, n_prows, n, mean);
+    ordered_mean_kernel<T><<<1, 256, 0, s_side>>>(rz_pn, p_rows, n_prows, n, mean);
     CK_LAUNCH();
-    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q, n, D.red, &D.ctl->red_counter, qinf);
+    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s_side>>>(D.q, n, D.red, &D.ctl->red_counter, qinf);
     CK_LAUNCH();
-    k_ruiz_gamma<T><<<1, 1, 0, s>>>(mean, qinf, gamma, cc);
+    k_ruiz_gamma<T><<<1, 1, 0, s_side>>>(mean, qinf, gamma, cc);
     CK_LAUNCH();
-    k_scale_by<T><<<grid_for(D.P.nnz), kThreads, 0, s>>>(D.P.val, D.P.nnz, gamma);
-    k_scale_by<T><<<grid_for(n), kThreads, 0, s>>>(D.q, n, gamma);
+    k_scale_by<T><<<grid_for(D.P.nnz), kThreads, 0, s_side>>>(D.P.val, D.P.nnz, gamma);
+    k_scale_by<T><<<grid_for(n), kThreads, 0, s_side>>>(D.q, n, gamma);
     CK_LAUNCH();
+    CK(cudaEventRecord(ev_join, s_side));
+    // main stream meanwhile: A rows (dz) then cols (dx); A^T rows (dx) then cols (dz)
+    plan_visit(D.A, D.pA, ScaleRowColFn<T>{D.A.val, D.A.ci, rz_dz, rz_dx}, s);
+    plan_visit(D.AT, D.pAT, ScaleRowColFn<T>{D.AT.val, D.AT.ci, rz_dx, rz_dz}, s);
+    CK(cudaStreamWaitEvent(s, ev_join, 0));
   }
 
   // scaling.hpp:166-176 (A^T re-derived from the scaled A, reciprocals, l, u),
@@ -615,8 +636,10 @@ class Workspace {
   void enq_post_pcg(const Handles& H) {
     k_pcg_fin<T><<<grid_for(D.n), kThreads, 0, s>>>(D);
     CK_LAUNCH();
-    launch_spmv<T, 2, SumOp>(D.A, D.pA, GatherAdmm<T>{D.g2n}, EpiAdmm<T>{D, T(0), T(0), T(0), false},
-                             s);
+    launch_spmv<T, 2, SumOp>(D.A, D.pA, GatherAdmm<T>{D.g2n},
+                             EpiAdmm<T, 2>{D, T(0), T(0), T(0), false}, s);
+    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.xt},
+                             EpiAdmm<T, 1>{D, T(0), T(0), T(0), false}, s);
     k_xupdate<T><<<grid_for(D.n), kThreads, 0, s>>>(D, H);
     CK_LAUNCH();
   }
@@ -877,7 +900,7 @@ class Workspace {
     const bool has_cert = hc.status == 1 || hc.status == 2;
     uint64_t launches = g_launches - l0 - graph_build;
     if (opt.mode != QPCG_MODE_EAGER && !use_persistent())  // kernels executed inside the graph
-      launches += 8ull * hc.iter + 5ull * hc.pcg_total + 2ull * hc.n_checks + 6ull * hc.n_inf +
+      launches += 9ull * hc.iter + 5ull * hc.pcg_total + 2ull * hc.n_checks + 6ull * hc.n_inf +
                   2ull * hc.n_rho_branch;
     if (has_cert) download(cert, D.cert, sizeof(T) * (hc.status == 1 ? D.m : D.n));
     CK(cudaStreamSynchronize(s));

@@ -151,7 +151,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
     }
     grid.sync();
     spmv_phase<T, 2, SumOp>(D.A, D.pA, GatherAdmm<T, false>{D.g2n},
-                            EpiAdmm<T>{D, T(0), T(0), T(0), false});
+                            EpiAdmm<T, 2>{D, T(0), T(0), T(0), false});
+    spmv_phase<T, 1, SumOp>(D.A, D.pA, GatherVec<T, false>{D.xt},
+                            EpiAdmm<T, 1>{D, T(0), T(0), T(0), false});
     grid.sync();
     if (!C->error) {
       xupdate_elems(D, t0, stride);
