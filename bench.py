@@ -80,6 +80,10 @@ def parse():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent instance per rank instead of the row-sharded solve")
     ap.add_argument("--shards", type=int, default=1, help="row blocks per GPU (virtual shards)")
+    ap.add_argument("--sweep", default="",
+                    help="CLASSES:SCALES[:INSTANCES] (e.g. lasso,svm:1,3,5:10): instead of the "
+                         "headline line, print the bench/runner.hpp CSV sweep solved by the engine "
+                         "with the reference CPU solver's columns beside it")
     return ap.parse_args()
 
 
@@ -351,8 +355,27 @@ def run_reference(args, rank: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def run_sweep(args) -> None:
+    """runner.hpp-schema CSV: the engine's row + the reference's (oracle/_ref,
+    1 core, the cpu_baseline leg) status / iterations / runtime + speed-up."""
+    from oracle import oracle as O  # reference columns only
+    from paper_1912_04263_b200 import generators, runner
+    from paper_1912_04263_b200.problem import Settings
+    parts = args.sweep.split(":")
+    classes = generators.CLASSES if parts[0] == "all" else parts[0].split(",")
+    scales = [int(v) for v in parts[1].split(",")]
+    k = int(parts[2]) if len(parts) > 2 else 10
+    s = Settings(lambda_pcg=args.lambda_pcg)
+    mine = runner.run_benchmark(classes, scales, s, k, solve_fn=runner.b200_solve(0, args.mode))
+    ref = runner.run_benchmark(classes, scales, s, k, solve_fn=lambda p, st: O.ref_solve(p, st))
+    runner.write_csv(mine, sys.stdout, compare=ref)
+
+
 def main():
     args = parse()
+    if args.sweep:
+        run_sweep(args)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

@@ -24,10 +24,12 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "qpcg/bench/generators.hpp"
+#include "qpcg/bench/runner.hpp"
 #include "qpcg/linsys.hpp"
 #include "qpcg/scaling.hpp"
 #include "qpcg/solver.hpp"
@@ -618,6 +620,34 @@ int qref_time_components_f64(const qpcg_csr_f64* p, const double* q,
     out[7] = (now_s() - t) / reps;
     out[8] = now_s() - t0;
   });
+}
+
+// ---- bench/runner.hpp sweep (the reference's own CSV, runtime included) -----
+// Writes run_benchmark + write_csv into out (NUL-terminated, truncated to
+// cap); returns the full length or -1 on error.
+int64_t qref_run_benchmark_csv(const int* classes, uint32_t n_classes, const uint32_t* scales,
+                               uint32_t n_scales, uint32_t instances, uint64_t base_seed,
+                               uint32_t threads, const qpcg_settings* s, char* out, size_t cap) {
+  try {
+    qb::SweepOptions o;
+    for (uint32_t i = 0; i < n_classes; ++i) o.classes.push_back(static_cast<qb::ProblemClass>(classes[i]));
+    for (uint32_t i = 0; i < n_scales; ++i) o.scales.push_back(scales[i]);
+    o.instances_per_size = instances;
+    o.base_seed = base_seed;
+    o.threads = threads;
+    std::ostringstream os;
+    qb::write_csv(os, qb::run_benchmark<double>(o, to_settings<double>(s)));
+    const std::string csv = os.str();
+    if (out && cap) {
+      const size_t k = std::min(cap - 1, csv.size());
+      std::memcpy(out, csv.data(), k);
+      out[k] = 0;
+    }
+    return int64_t(csv.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
 }
 
 }  // extern "C"
