@@ -366,6 +366,7 @@ def run_sweep(args) -> None:
     scales = [int(v) for v in parts[1].split(",")]
     k = int(parts[2]) if len(parts) > 2 else 10
     s = Settings(lambda_pcg=args.lambda_pcg)
+    runner.b200_solve(0, args.mode)(generators.generate(classes[0], scales[0], 0), s)  # context warm-up
     mine = runner.run_benchmark(classes, scales, s, k, solve_fn=runner.b200_solve(0, args.mode))
     ref = runner.run_benchmark(classes, scales, s, k, solve_fn=lambda p, st: O.ref_solve(p, st))
     runner.write_csv(mine, sys.stdout, compare=ref)
