@@ -153,10 +153,13 @@ typedef struct {
 #define QPCG_MODE_GRAPH 0 /* device-resident control flow: CUDA graph with
                              conditional while/if nodes (default) */
 #define QPCG_MODE_EAGER 1 /* host-driven loop with a sync per decision (debug) */
-#define QPCG_MODE_PERSISTENT 2 /* the whole loop in one cooperative kernel; GRAPH
-                                  picks it by itself while nnz(A) + nnz(P) <=
-                                  2e6 (env QPCG_PERSIST_MAX_NNZ).  All three
-                                  modes give bitwise-identical results. */
+#define QPCG_MODE_PERSISTENT 2 /* the whole loop in one kernel: one thread-block
+                                  cluster (hardware barriers) while nnz(A) +
+                                  nnz(P) <= 15e3 (env QPCG_CLUSTER_MAX_NNZ),
+                                  else a cooperative grid.  GRAPH picks it by
+                                  itself while nnz(A) + nnz(P) <= 2e6 (env
+                                  QPCG_PERSIST_MAX_NNZ).  All modes give
+                                  bitwise-identical results. */
 
 /* Row sharding.  A is cut into G = virtual_shards x
  * nccl_ranks contiguous nnz-balanced row blocks (qpcg_shard_cuts); every

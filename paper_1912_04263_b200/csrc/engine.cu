@@ -764,20 +764,68 @@ class Workspace {
     if (opt.mode == QPCG_MODE_PERSISTENT) return true;
     return opt.mode == QPCG_MODE_GRAPH && uint64_t(D.A.nnz) + D.P.nnz <= persist_max_nnz();
   }
+  static uint64_t cluster_max_nnz() {
+    const char* e = std::getenv("QPCG_CLUSTER_MAX_NNZ");
+    return e ? std::strtoull(e, nullptr, 10) : 15000ull;
+  }
   void run_persistent() {
     if (!persist_part) persist_part = alloc<T>(2 * kMaxQ * kMaxVirtual);
+    PersistBufs<T> B{persist_part, D.ctl};
+    void* args[] = {(void*)&D, (void*)&B};
+    const uint64_t work = uint64_t(D.A.nnz) + D.P.nnz;
+    static int cluster = -1;  // largest cluster the kernel can run as (same device model)
+    if (cluster < 0) {
+      cluster = 0;
+      auto* kc = k_admm_persistent<T, ClusterSync>;
+      if (cudaFuncSetAttribute(kc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+        for (int c : {16, 8}) {
+          cudaLaunchConfig_t cfg = {};
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = c;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          cfg.gridDim = dim3(c);
+          cfg.blockDim = dim3(kThreads);
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          int nc = 0;
+          if (cudaOccupancyMaxActiveClusters(&nc, kc, &cfg) == cudaSuccess && nc > 0) {
+            cluster = c;
+            break;
+          }
+        }
+      }
+      cudaGetLastError();
+    }
+    if (cluster > 0 && work <= cluster_max_nnz()) {
+      // tiny problem: one cluster, hardware barriers
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(cluster);
+      cfg.blockDim = dim3(kThreads);
+      cfg.stream = s;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelExC(&cfg, (const void*)k_admm_persistent<T, ClusterSync>, args));
+      CK_LAUNCH();
+      return;
+    }
     static int max_grid = 0;  // co-resident blocks (same device model for every workspace)
     if (max_grid == 0) {
       int per_sm = 0, sms = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_admm_persistent<T>, kThreads, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_admm_persistent<T, GridSync>,
+                                                       kThreads, 0));
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
       max_grid = std::max(1, per_sm) * sms;
     }
     const int grid = max_grid;  // measured: more co-resident blocks is faster at every size
-    PersistBufs<T> B{persist_part, D.ctl};
-    void* args[] = {(void*)&D, (void*)&B};
-    CK(cudaLaunchCooperativeKernel((const void*)k_admm_persistent<T>, dim3(grid), dim3(kThreads), args,
-                                   0, s));
+    CK(cudaLaunchCooperativeKernel((const void*)k_admm_persistent<T, GridSync>, dim3(grid),
+                                   dim3(kThreads), args, 0, s));
     CK_LAUNCH();
   }
 

@@ -38,11 +38,23 @@ struct PersistBufs {
 };
 constexpr uint32_t kMaxVirtual = 2 * kNumSMs;  // red_grid() never exceeds kRedBlocks
 
+// The barrier between phases: the whole grid (cooperative launch, one or two
+// blocks per SM) or one thread-block cluster (up to 16 SMs, hardware barrier:
+// the tiny-problem variant, where barrier latency is the whole cost).
+struct GridSync {
+  cgp::grid_group g;
+  __device__ GridSync() : g(cgp::this_grid()) {}
+  __device__ __forceinline__ void sync() { g.sync(); }
+};
+struct ClusterSync {
+  __device__ __forceinline__ void sync() { cgp::this_cluster().sync(); }
+};
+
 // Reduction with the stand-alone kernels' geometry: virtual block vb of
 // Gv = red_grid(len) covers threads vb*kThreads + tid with stride Gv*kThreads.
-template <typename T, int NQ, typename F>
+template <typename T, int NQ, typename F, class Sync>
 __device__ __forceinline__ void preduce(F&& elems, uint32_t len, uint32_t max_mask, T* part,
-                                        cgp::grid_group& grid, T (&tot)[NQ]) {
+                                        Sync& grid, T (&tot)[NQ]) {
   __shared__ T sm[33];
   const uint32_t Gv = red_grid<T>(len);
   for (uint32_t vb = blockIdx.x; vb < Gv; vb += gridDim.x) {
@@ -90,9 +102,9 @@ __device__ __forceinline__ void spmv_phase(const DevCsr<T>& M, const SpmvPlan<T>
     spmv_short<T, NCOL, Op, Gather, Epi>(M, P, gather, epi, idx);
 }
 
-template <typename T>
+template <typename T, class Sync>
 __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, PersistBufs<T> B) {
-  cgp::grid_group grid = cgp::this_grid();
+  Sync grid;
   __shared__ Ctl<T> sctl;
   if (threadIdx.x == 0) sctl = *Dg.ctl;
   __syncthreads();
