@@ -22,8 +22,12 @@ ENGINE_SO = os.path.join(HERE, "libqpcg_b200.so")
 GEN_SO = os.path.join(HERE, "libqpcg_gen.so")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
-              "--extended-lambda", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+              "--extended-lambda", "-std=c++17", "-Xcompiler", "-fPIC",
               f"-I{os.path.join(ROOT, 'include')}"]
+# the C-ABI and one translation unit per precision (explicit instantiations of
+# Workspace<T> / Sharded<T>), compiled in parallel, linked into one .so
+ENGINE_TUS = ["engine.cu", "engine_f64.cu", "engine_f32.cu"]
+OBJ_DIR = os.path.join(HERE, "build")
 
 
 def _stale(target: str, deps: list[str]) -> bool:
@@ -35,11 +39,23 @@ def _stale(target: str, deps: list[str]) -> bool:
 
 def build_engine(force: bool = False) -> str:
     deps = glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
-        [os.path.join(ROOT, "include", "qpcg_b200.h")]
-    if force or _stale(ENGINE_SO, deps):
-        cmd = [NVCC, *NVCC_FLAGS, "-o", ENGINE_SO, os.path.join(CSRC, "engine.cu")]
+        [os.path.join(ROOT, "include", "qpcg_b200.h"), os.path.join(ROOT, "include", "qpcg_b200_ops.h")]
+    if not (force or _stale(ENGINE_SO, deps)):
+        return ENGINE_SO
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    objs, procs = [], []
+    for tu in ENGINE_TUS:
+        obj = os.path.join(OBJ_DIR, tu.replace(".cu", ".o"))
+        cmd = [NVCC, *NVCC_FLAGS, "-c", "-o", obj, os.path.join(CSRC, tu)]
         print(" ".join(cmd), flush=True)
-        subprocess.check_call(cmd)
+        procs.append(subprocess.Popen(cmd))
+        objs.append(obj)
+    rcs = [p.wait() for p in procs]
+    if any(rcs):
+        raise subprocess.CalledProcessError(max(rcs), "nvcc")
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", ENGINE_SO, *objs]
+    print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
     return ENGINE_SO
 
 

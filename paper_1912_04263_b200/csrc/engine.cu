@@ -1,1178 +1,7 @@
-// engine.cu — the B200 ADMM/PCG workspace and the C-ABI (include/qpcg_b200.h).
-//
-// Drop-in for qpcg::solve (solver.hpp:386-541).  One workspace = one device,
-// one stream, all buffers; calls on distinct workspaces are re-entrant.
-//
-// Per ADMM step (SURVEY.md §7 hard part 4b):
-//   A^T pass  [rhs = A^T(rho z - y) + (sigma x - q) ; r0 = K x~ - rhs]   2 cols
-//   k_pcg_init
-//   while PCG: A pass [t = rho A p] ; A^T pass [Kp = P p + sigma p + A^T t] ;
-//              k_pcg_dot ; k_pcg_update ; k_pcg_pupdate
-//   k_pcg_fin
-//   A pass    [z~ = A x~, m-side relax/project/dual update ; A x_new]    2 cols
-//   k_xupdate
-//   if check: A^T pass [A^T y, P x, r_dual] ; k_residuals
-//             if not optimal: A_o^T, P_o, A_o passes ; k_infeas
-//   if rho:   k_rho ; k_precond
-// The matrix streams are A and A^T once per PCG iteration plus once each per
-// ADMM step (the reference streams 4 A-sized matrices + P per step).
-#include <chrono>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <memory>
-#include <string>
-#include <vector>
-
-#include "../../include/qpcg_b200.h"
-#include "../../include/qpcg_b200_ops.h"
-#include "admm.cuh"
-#include "comm.cuh"
-#include "persist.cuh"
-#include "setup.cuh"
-
-namespace qpcg_b200 {
-
-template <typename T>
-struct HostCsr {
-  uint32_t rows, cols, nnz;
-  const T* values;
-  const uint32_t* row_ptr;
-  const uint32_t* col_indices;
-};
-
-static double now_s() {
-  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
-
-// ------------------------------------------------------------ setup kernels
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_ruiz_delta(const T* pn, const T* atn, uint32_t n,
-                                                        const T* an, uint32_t m, T* dx, T* dz,
-                                                        T* d, T* e, T* q, T* part,
-                                                        uint32_t* counter, T* dev_out) {
-  // scaling.hpp:125-138: delta = 1/sqrt(col norm) (1 for empty), D *= dx, E *= dz,
-  // q *= dx; deviation = |1 - delta|_inf (:163-165)
-  T v[1] = {T(0)};
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const T cn = smax(pn[i], atn[i]);
-    const T di = cn > T(0) ? T(1) / t_sqrt(cn) : T(1);
-    dx[i] = di;
-    d[i] *= di;
-    q[i] *= di;
-    v[0] = smax(v[0], tabs(T(1) - di));
-  }
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
-    const T a = an[j];
-    const T dj = a > T(0) ? T(1) / t_sqrt(a) : T(1);
-    dz[j] = dj;
-    e[j] *= dj;
-    v[0] = smax(v[0], tabs(T(1) - dj));
-  }
-  T tot[1];
-  if (!grid_reduce<T, 1>(v, 0x1u, part, counter, tot)) return;
-  if (threadIdx.x == 0) *dev_out = tot[0];
-}
-
-// gamma = 1/max(mean, |q|_inf) (1 if 0); c *= gamma  (scaling.hpp:159-162)
-template <typename T>
-__global__ void k_ruiz_gamma(const T* mean, const T* qinf, T* gamma, T* c) {
-  const T denom = smax(*mean, *qinf);
-  const T g = denom > T(0) ? T(1) / denom : T(1);
-  *gamma = g;
-  *c *= g;
-}
-
-template <typename T>
-__global__ void k_scale_by(T* v, uint32_t n, const T* g) {
-  const T s = *g;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    v[i] *= s;
-}
-
-// =====================================================================
-template <typename T>
-class Workspace {
- public:
-  int device = 0;
-  cudaStream_t s = nullptr;
-  CubTemp tmp;
-  Dev<T> D{};
-  Ctl<T> hc{};
-  qpcg_settings set{};
-  qpcg_options opt{};
-  std::vector<void*> allocs;
-  uint32_t* permA = nullptr;  // transpose permutation of A
-  uint32_t* p_rows = nullptr;  // rows of P_full with entries (ordered mean)
-  uint32_t n_prows = 0;
-  T* ruiz_scal = nullptr;      // [mean, qinf, gamma, c, dev]
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  double setup_seconds = 0, h2d_seconds = 0, setup_wall = 0;
-  uint64_t h2d_bytes = 0;
-  std::string err;
-  bool have_solved = false;
-  bool own_stream = true;
-  uint64_t setup_launches = 0;
-  bool have_counted_setup = false;
-
-  ~Workspace() {
-    if (s_side) {
-      cudaStreamSynchronize(s_side);
-      cudaStreamDestroy(s_side);
-    }
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
-    {
-      AllocScope scope(s);
-      for (void* p : allocs) dfree(p);
-      for (SpmvPlan<T>* p : {&D.pP, &D.pA, &D.pAT}) plan_free(*p);
-      if (tmp.ptr) dfree(tmp.ptr);
-      tmp.ptr = nullptr;
-      tmp.bytes = 0;
-      if (s) cudaStreamSynchronize(s);
-    }
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
-    if (s && own_stream) cudaStreamDestroy(s);
-  }
-
-  template <typename U>
-  U* alloc(size_t count) {
-    void* p = nullptr;
-    CK(dmalloc(&p, sizeof(U) * (count ? count : 1)));
-    allocs.push_back(p);
-    return static_cast<U*>(p);
-  }
-  T* vec(size_t count, bool zero = true) {
-    T* p = alloc<T>(count);
-    if (zero) CK(cudaMemsetAsync(p, 0, sizeof(T) * (count ? count : 1), s));
-    return p;
-  }
-  void upload(void* dst, const void* src, size_t bytes) {
-    if (bytes == 0) return;
-    const bool host = opt.input_memory == QPCG_MEM_HOST;
-    CK(cudaMemcpyAsync(dst, src, bytes, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
-    if (host) h2d_bytes += bytes;
-  }
-  void download(void* dst, const void* src, size_t bytes) {
-    if (bytes == 0 || dst == nullptr) return;
-    const bool host = opt.input_memory == QPCG_MEM_HOST;
-    CK(cudaMemcpyAsync(dst, src, bytes, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
-  }
-  void fill(T* p, uint32_t n, T v) {
-    for_n(n, [=] __device__(uint32_t i) { p[i] = v; }, s);
-  }
-  T read_scalar(const T* p) {
-    T v;
-    CK(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    return v;
-  }
-  void pull_ctl() {
-    CK(cudaMemcpyAsync(&hc, D.ctl, sizeof(Ctl<T>), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-  }
-  void push_ctl() { CK(cudaMemcpyAsync(D.ctl, &hc, sizeof(Ctl<T>), cudaMemcpyHostToDevice, s)); }
-
-  // ------------------------------------------------------------- setup
-  // The single-device setup; the sharded path (shard.cuh) runs the same
-  // phases per row block with its collectives in between.
-  void setup(const HostCsr<T>& Pu, const T* q, const HostCsr<T>& A, const T* l, const T* u,
-             const qpcg_settings& st, const qpcg_options& op) {
-    const double w0 = now_s();
-    const uint64_t l0 = g_launches;
-    begin(st, op, nullptr);
-    AllocScope scope(s);
-    CK(cudaEventRecord(ev0, s));
-    load(Pu, q, A, l, u, 0, A.rows, false);
-    ValKeys k = validate_keys();
-    raise_first(k);
-    build_structures();
-    uint32_t passes = 0;
-    T deviation = T(0);
-    if (set.scaling_enabled) {
-      ruiz_prepare();
-      deviation = T(1);
-      while (passes < set.equil_max_passes && deviation > T(set.eps_equil)) {
-        ++passes;
-        ruiz_norms();
-        ruiz_delta();
-        ruiz_scale();
-        deviation = read_scalar(ruiz_scal + 4);
-      }
-    }
-    finish_scaling(passes, deviation);
-    diag_ata_kernel<T><<<grid_for(uint64_t(D.n) * 32), kThreads, 0, s>>>(D.AT, D.diag_ata, nullptr);
-    CK_LAUNCH();
-    finish_setup();
-    CK(cudaEventRecord(ev1, s));
-    CK(cudaEventSynchronize(ev1));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, ev0, ev1));
-    setup_seconds = ms * 1e-3;
-    setup_wall = now_s() - w0;
-    setup_launches = g_launches - l0;
-  }
-
-  uint32_t equil_passes = 0;
-  T equil_residual = T(0);
-
-  // setup-phase state
-  uint32_t *pu_rp = nullptr, *pu_ci = nullptr, *a_rp = nullptr, *a_ci = nullptr;
-  T *pu_v = nullptr, *a_v = nullptr;
-  uint32_t pu_nnz = 0, pu_cols = 0, a_cols = 0;
-  uint32_t row0 = 0;  // first global row of this block of A (sharded path)
-  uint32_t nnz0 = 0;  // first global entry of this block
-  bool p_square = true, a_cols_ok = true;
-  T *rz_dx = nullptr, *rz_dz = nullptr, *rz_pn = nullptr, *rz_atn = nullptr, *rz_an = nullptr;
-
-  // settings, device, stream, pool, events
-  void begin(const qpcg_settings& st, const qpcg_options& op, cudaStream_t shared) {
-    set = st;
-    opt = op;
-    validate_settings(st);
-    device = op.device;
-    if (device < 0) CK(cudaGetDevice(&device));
-    CK(cudaSetDevice(device));
-    if (shared != nullptr) {
-      s = shared;
-      own_stream = false;
-    } else if (op.stream != nullptr) {
-      s = static_cast<cudaStream_t>(op.stream);
-      own_stream = false;
-    } else {
-      CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    }
-    configure_pool(device);
-    CK(cudaEventCreate(&ev0));
-    CK(cudaEventCreate(&ev1));
-  }
-
-  // Upload P (upper), q and the row block [r0, r1) of A, l, u — the only
-  // host->device traffic of a solve.  slice == false: A as given (rows 0..m).
-  void load(const HostCsr<T>& Pu, const T* q, const HostCsr<T>& A, const T* l, const T* u,
-            uint32_t r0, uint32_t r1, bool slice) {
-    const double th = now_s();
-    const uint32_t n = Pu.rows, m = r1 - r0;
-    p_square = Pu.rows == Pu.cols;
-    a_cols_ok = A.cols == Pu.cols;
-    pu_nnz = Pu.nnz;
-    pu_cols = Pu.cols;
-    a_cols = A.cols;
-    D.n = n;
-    D.m = m;
-    uint32_t e0 = 0, e1 = A.nnz;
-    if (slice) {  // row_ptr is valid here (shard_cuts checked it on the host)
-      e0 = host_rp(A, r0);
-      e1 = host_rp(A, r1);
-    }
-    row0 = r0;
-    nnz0 = e0;
-    const uint32_t annz = e1 - e0;
-    pu_rp = alloc<uint32_t>(n + 1);
-    pu_ci = alloc<uint32_t>(Pu.nnz);
-    pu_v = alloc<T>(Pu.nnz);
-    a_rp = alloc<uint32_t>(m + 1);
-    a_ci = alloc<uint32_t>(annz);
-    a_v = alloc<T>(annz);
-    D.q_o = alloc<T>(n);
-    D.l_o = alloc<T>(m);
-    D.u_o = alloc<T>(m);
-    upload(pu_rp, Pu.row_ptr, sizeof(uint32_t) * (n + 1));
-    upload(pu_ci, Pu.col_indices, sizeof(uint32_t) * Pu.nnz);
-    upload(pu_v, Pu.values, sizeof(T) * Pu.nnz);
-    upload(a_rp, A.row_ptr + r0, sizeof(uint32_t) * (m + 1));
-    upload(a_ci, A.col_indices + e0, sizeof(uint32_t) * annz);
-    upload(a_v, A.values + e0, sizeof(T) * annz);
-    upload(D.q_o, q, sizeof(T) * n);
-    upload(D.l_o, l + r0, sizeof(T) * m);
-    upload(D.u_o, u + r0, sizeof(T) * m);
-    if (slice && e0 != 0) {
-      uint32_t* rp = a_rp;
-      for_n(m + 1, [=] __device__(uint32_t i) { rp[i] -= e0; }, s);
-    }
-    D.A = DevCsr<T>{m, A.cols, annz, a_v, a_rp, a_ci};
-    if (opt.input_memory == QPCG_MEM_HOST) {
-      CK(cudaStreamSynchronize(s));
-      h2d_seconds = now_s() - th;
-    }
-  }
-  uint32_t host_rp(const HostCsr<T>& A, uint32_t r) {
-    if (opt.input_memory == QPCG_MEM_HOST) return A.row_ptr[r];
-    uint32_t v = 0;
-    CK(cudaMemcpyAsync(&v, A.row_ptr + r, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    return v;
-  }
-
-  // Validation (problem.hpp:46-92, sparse.hpp:98-124): three stage keys, each
-  // the minimum (category, global index, position) found; raise_first applies
-  // the reference's check order.  Keys of row blocks combine by min.
-  struct ValKeys {
-    unsigned long long k[3];  // P rows, A rows, values/bounds
-    uint32_t ends[4];         // P row_ptr ends, A row_ptr ends (block-local)
-  };
-  ValKeys validate_keys() {
-    const uint32_t n = D.n, m = D.m;
-    ValKeys v;
-    CK(cudaMemcpyAsync(v.ends + 0, pu_rp, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(v.ends + 1, pu_rp + n, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(v.ends + 2, a_rp, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(v.ends + 3, a_rp + m, 4, cudaMemcpyDeviceToHost, s));
-    unsigned long long* key = alloc<unsigned long long>(3);
-    CK(cudaMemsetAsync(key, 0xff, 24, s));
-    CK(cudaStreamSynchronize(s));
-    const bool p_ok = v.ends[0] == 0 && v.ends[1] == pu_nnz;
-    const bool a_ok = v.ends[2] == 0 && v.ends[3] == D.A.nnz;
-    if (p_ok) {
-      validate_csr_rows_kernel<<<grid_for(n), kThreads, 0, s>>>(pu_rp, pu_ci, n, pu_cols, kValPRowPtr,
-                                                               p_square ? 1 : 0, key, 0);
-      CK_LAUNCH();
-    }
-    if (a_ok) {
-      validate_csr_rows_kernel<<<grid_for(m), kThreads, 0, s>>>(a_rp, a_ci, m, a_cols, kValARowPtr, 0,
-                                                               key + 1, row0);
-      CK_LAUNCH();
-      validate_values_kernel<T><<<grid_for(pu_nnz), kThreads, 0, s>>>(pu_v, pu_nnz, kValPFinite, key + 2, 0);
-      validate_values_kernel<T><<<grid_for(D.A.nnz), kThreads, 0, s>>>(a_v, D.A.nnz, kValAFinite, key + 2, nnz0);
-      validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.q_o, n, kValQFinite, key + 2, 0);
-      validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(D.l_o, D.u_o, m, key + 2, row0);
-      CK_LAUNCH();
-    }
-    CK(cudaMemcpyAsync(v.k, key, 24, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    return v;
-  }
-  void raise_first(const ValKeys& v) const {
-    if (v.ends[0] != 0 || v.ends[1] != pu_nnz)
-      throw InvalidArgument("csr: row_ptr must start at 0 and end at nnz");
-    if ((v.k[0] >> 56) == kValPRowPtr) throw InvalidArgument(validation_message(v.k[0]));
-    if (v.ends[2] != 0 || v.ends[3] != D.A.nnz)
-      throw InvalidArgument("csr: row_ptr must start at 0 and end at nnz");
-    if ((v.k[1] >> 56) == kValARowPtr) throw InvalidArgument(validation_message(v.k[1]));
-    if (!p_square) throw InvalidArgument("problem: P must be square");
-    if (D.n == 0) throw InvalidArgument("problem: at least one variable required");
-    if ((v.k[0] >> 56) == kValPBelow) throw InvalidArgument(validation_message(v.k[0]));
-    if (!a_cols_ok) throw InvalidArgument("problem: A column count must equal n");
-    if (v.k[2] != ~0ull) throw InvalidArgument(validation_message(v.k[2]));
-  }
-
-  static bool compress_indices() {  // QPCG_COMPRESS=0: uint32 column streams
-    const char* e = std::getenv("QPCG_COMPRESS");
-    return !(e && e[0] == '0');
-  }
-
-  // symmetrize_upper, transpose_csr, plans, the original and scaled copies
-  void build_structures() {
-    const uint32_t n = D.n, m = D.m, annz = D.A.nnz;
-    DevCsr<T> Pup{n, n, pu_nnz, pu_v, pu_rp, pu_ci};
-    SpmvPlan<T> pPu = plan_build<T>(pu_rp, n, tmp, s);
-    D.pA = plan_build<T>(a_rp, m, tmp, s);
-    uint32_t* row_of = alloc<uint32_t>(std::max(pu_nnz, annz));
-    plan_visit(Pup, pPu, RowOfFn{row_of}, s);
-    // symmetrize_upper (solver.hpp:397)
-    DevCsr<T> Pfull;
-    symmetrize_upper_dev(Pup, row_of, Pfull, tmp, s);
-    allocs.push_back(Pfull.rp);
-    allocs.push_back(Pfull.ci);
-    allocs.push_back(Pfull.val);
-    plan_free(pPu);
-    D.pP = plan_build<T>(Pfull.rp, n, tmp, s);
-    D.Po = Pfull;
-    // transpose_csr (solver.hpp:398)
-    plan_visit(D.A, D.pA, RowOfFn{row_of}, s);
-    uint32_t* at_rp = alloc<uint32_t>(n + 1);
-    uint32_t* at_ci = alloc<uint32_t>(annz);
-    permA = alloc<uint32_t>(annz);
-    transpose_structure(a_ci, row_of, n, annz, at_rp, at_ci, permA, tmp, s);
-    T* ato_v = alloc<T>(annz);
-    gather_values(a_v, permA, annz, ato_v, s);
-    D.Ao = DevCsr<T>{m, n, annz, a_v, a_rp, a_ci};
-    D.ATo = DevCsr<T>{n, m, annz, ato_v, at_rp, at_ci};
-    D.pAT = plan_build<T>(at_rp, n, tmp, s);
-    if (compress_indices()) {  // 16-bit column offsets for the A / A^T streams
-      plan_compress(D.pA, a_ci, annz, n, tmp, s);
-      plan_compress(D.pAT, at_ci, annz, m, tmp, s);
-    }
-    D.pPo = D.pP;
-    D.pAo = D.pA;
-    D.pATo = D.pAT;
-    // ---- control block + reductions
-    D.ctl = alloc<Ctl<T>>(1);
-    D.red = alloc<T>(kRedBlocks * kMaxQ);
-    CK(cudaMemsetAsync(D.ctl, 0, sizeof(Ctl<T>), s));
-    ruiz_scal = vec(8);
-    // q_inf_orig (solver.hpp:399)
-    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q_o, n, D.red, &D.ctl->red_counter,
-                                                      ruiz_scal + 5);
-    CK_LAUNCH();
-    // ---- scaled copies
-    D.P = DevCsr<T>{n, n, Pfull.nnz, alloc<T>(Pfull.nnz), Pfull.rp, Pfull.ci};
-    D.A = DevCsr<T>{m, n, annz, alloc<T>(annz), a_rp, a_ci};
-    D.AT = DevCsr<T>{n, m, annz, alloc<T>(annz), at_rp, at_ci};
-    CK(cudaMemcpyAsync(D.P.val, Pfull.val, sizeof(T) * Pfull.nnz, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(D.A.val, a_v, sizeof(T) * annz, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(D.AT.val, ato_v, sizeof(T) * annz, cudaMemcpyDeviceToDevice, s));
-    D.q = vec(n, false);
-    CK(cudaMemcpyAsync(D.q, D.q_o, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
-    D.d = vec(n, false);
-    D.e = vec(m, false);
-    D.d_inv = vec(n, false);
-    D.e_inv = vec(m, false);
-    D.l = vec(m, false);
-    D.u = vec(m, false);
-    fill(D.d, n, T(1));
-    fill(D.e, m, T(1));
-    const T c = T(1);
-    CK(cudaMemcpyAsync(ruiz_scal + 3, &c, sizeof(T), cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
-  }
-
-  // modified Ruiz equilibration (scaling.hpp:92-187), bit-exact, one pass per
-  // ruiz_norms / ruiz_delta / ruiz_scale; ruiz_scal[4] = the pass deviation.
-  // Row blocks combine rz_atn (max) and the deviation (max) in between: both
-  // maxima are order-free, so the sharded scaling is bit-identical too.
-  void ruiz_prepare() {
-    const uint32_t n = D.n, m = D.m;
-    rz_dx = vec(n, false);
-    rz_dz = vec(m, false);
-    rz_pn = vec(n, false);
-    rz_atn = vec(n, false);
-    rz_an = vec(m, false);
-    // rows of P_full with entries, for the ordered mean (structure is fixed)
-    uint32_t* flags = alloc<uint32_t>(n + 1);
-    uint32_t* pos = alloc<uint32_t>(n + 1);
-    p_rows = alloc<uint32_t>(n + 1);
-    nonempty_flags_kernel<<<grid_for(n), kThreads, 0, s>>>(D.P.rp, n, flags);
-    CK_LAUNCH();
-    exclusive_scan_u32(flags, pos, n, tmp, s);
-    n_prows = scan_total(flags, pos, n, s);
-    compact_kernel<<<grid_for(n), kThreads, 0, s>>>(flags, pos, n, p_rows);
-    CK_LAUNCH();
-  }
-  void ruiz_norms() {
-    row_inf_norms(D.P, D.pP, rz_pn, s);
-    if (D.m == 0 || D.AT.nnz == 0)  // empty block: no column contributes
-      CK(cudaMemsetAsync(rz_atn, 0, sizeof(T) * D.n, s));
-    else
-      row_inf_norms(D.AT, D.pAT, rz_atn, s);
-    row_inf_norms(D.A, D.pA, rz_an, s);
-  }
-  void ruiz_delta() {
-    const uint32_t n = D.n, m = D.m;
-    k_ruiz_delta<T><<<red_grid<T>(std::max(n, m)), kThreads, 0, s>>>(
-        rz_pn, rz_atn, n, rz_an, m, rz_dx, rz_dz, D.d, D.e, D.q, D.red, &D.ctl->red_counter,
-        ruiz_scal + 4);
-    CK_LAUNCH();
-  }
-  // The cost scaling (the sequential mean of P's row norms, |q|, gamma, P and
-  // q *= gamma) only depends on P and q: it runs on a side stream while the
-  // main stream scales A and A^T (the mean is a latency-bound dependent chain).
-  cudaStream_t s_side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  void ruiz_scale() {
-    const uint32_t n = D.n;
-    if (!s_side) {
-      CK(cudaStreamCreateWithFlags(&s_side, cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    }
-    plan_visit(D.P, D.pP, ScaleRowColFn<T>{D.P.val, D.P.ci, rz_dx, rz_dx}, s);
-    row_inf_norms(D.P, D.pP, rz_pn, s);
-    CK(cudaEventRecord(ev_fork, s));
-    CK(cudaStreamWaitEvent(s_side, ev_fork, 0));
-    // cost scaling (scaling.hpp:156-162), side stream
-    T* mean = ruiz_scal + 0;
-    T* qinf = ruiz_scal + 1;
-    T* gamma = ruiz_scal + 2;
-    T* cc = ruiz_scal + 3;
-    ordered_mean_kernel<T><<<1, 256, 0, s_side>>>(rz_pn, p_rows, n_prows, n, mean);
-    CK_LAUNCH();
-    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s_side>>>(D.q, n, D.red, &D.ctl->red_counter, qinf);
-    CK_LAUNCH();
-    k_ruiz_gamma<T><<<1, 1, 0, s_side>>>(mean, qinf, gamma, cc);
-    CK_LAUNCH();
-    k_scale_by<T><<<grid_for(D.P.nnz), kThreads, 0, s_side>>>(D.P.val, D.P.nnz, gamma);
-    k_scale_by<T><<<grid_for(n), kThreads, 0, s_side>>>(D.q, n, gamma);
-    CK_LAUNCH();
-    CK(cudaEventRecord(ev_join, s_side));
-    // main stream meanwhile: A rows (dz) then cols (dx); A^T rows (dx) then cols (dz)
-    plan_visit(D.A, D.pA, ScaleRowColFn<T>{D.A.val, D.A.ci, rz_dz, rz_dx}, s);
-    plan_visit(D.AT, D.pAT, ScaleRowColFn<T>{D.AT.val, D.AT.ci, rz_dx, rz_dz}, s);
-    CK(cudaStreamWaitEvent(s, ev_join, 0));
-  }
-
-  // scaling.hpp:166-176 (A^T re-derived from the scaled A, reciprocals, l, u),
-  // q_inf_scaled, diag(P)
-  void finish_scaling(uint32_t passes, T deviation) {
-    const uint32_t n = D.n, m = D.m;
-    equil_passes = passes;
-    equil_residual = deviation;
-    if (set.scaling_enabled) gather_values(D.A.val, permA, D.A.nnz, D.AT.val, s);
-    {
-      T *d = D.d, *e = D.e, *di = D.d_inv, *ei = D.e_inv, *lo = D.l_o, *uo = D.u_o, *ls = D.l,
-        *us = D.u;
-      for_n(n, [=] __device__(uint32_t i) { di[i] = T(1) / d[i]; }, s);
-      for_n(m, [=] __device__(uint32_t j) {
-        ei[j] = T(1) / e[j];
-        ls[j] = e[j] * lo[j];
-        us[j] = e[j] * uo[j];
-      }, s);
-    }
-    if (!set.scaling_enabled) {  // identity_scaled_problem (scaling.hpp:190-205): l, u copied
-      CK(cudaMemcpyAsync(D.l, D.l_o, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
-      CK(cudaMemcpyAsync(D.u, D.u_o, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
-    }
-    // q_inf_scaled (solver.hpp:407)
-    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q, n, D.red, &D.ctl->red_counter,
-                                                      ruiz_scal + 6);
-    CK_LAUNCH();
-    // ---- operator caches + Jacobi (linsys.hpp:59-60, 137-148)
-    D.diag_p = vec(n, false);
-    D.diag_ata = vec(n, false);
-    D.dinv = vec(n, false);
-    extract_diag_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.P, D.diag_p);
-    CK_LAUNCH();
-  }
-
-  // state and workspace vectors, the control block, the Jacobi diagonal
-  void finish_setup() {
-    const uint32_t n = D.n, m = D.m;
-    D.x = vec(n); D.xt = vec(n); D.dx = vec(n); D.b = vec(n); D.r = vec(n); D.p = vec(n);
-    D.kp = vec(n); D.best = vec(n); D.px = vec(n); D.aty = vec(n); D.rdual = vec(n);
-    D.xo = vec(n); D.pxo = vec(n);
-    D.z = vec(m); D.y = vec(m); D.zt = vec(m); D.dy = vec(m); D.t = vec(m); D.ax = vec(m);
-    D.zo = vec(m); D.yo = vec(m);
-    D.cert = vec(std::max(n, m));
-    D.g2m = alloc<pair_t<T>>(m);
-    D.g2n = alloc<pair_t<T>>(n);
-    if (D.split) {
-      D.part = vec(2 * size_t(n));
-      D.shsc = vec(kShScal);
-    }
-    const uint32_t cap = opt.record_diagnostics ? set.max_admm_iter : 0u;
-    D.calls = alloc<DiagRec<T>>(cap);
-    D.checks = alloc<uint32_t>(cap);
-    D.rhos = alloc<RhoRec<T>>(cap);
-    // ---- control block
-    T hs[8];
-    CK(cudaMemcpyAsync(hs, ruiz_scal, sizeof(T) * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const qpcg_settings& st = set;
-    std::memset(&hc, 0, sizeof(hc));
-    hc.alpha = T(st.alpha);
-    hc.sigma = T(st.sigma);
-    hc.eps_abs = T(st.eps_abs);
-    hc.eps_rel = T(st.eps_rel);
-    hc.eps_pinf = T(st.eps_pinf);
-    hc.eps_dinf = T(st.eps_dinf);
-    hc.lambda = T(st.lambda_pcg);
-    hc.eps_min = T(st.eps_pcg_min);
-    hc.max_iter = st.max_admm_iter;
-    hc.check_interval = st.check_interval;
-    hc.rho_interval = st.rho_update_interval;
-    hc.pcg_cap = pcg_cap(n);
-    const T c = hs[3];
-    hc.c = c;
-    hc.c_inv = T(1) / c;
-    hc.q_inf_orig = hs[5];
-    hc.q_inf_scaled = hs[6];
-    hc.rho = T(st.rho_bar_init);
-    hc.status = QPCG_STATUS_MAX_ITER_REACHED;
-    hc.diag_cap = cap;
-    push_ctl();
-    k_precond<T><<<grid_for(n), kThreads, 0, s>>>(D, 1);
-    CK_LAUNCH();
-  }
-
-  static uint32_t pcg_cap(uint32_t n) {  // solver.hpp:330-334, evaluated in T
-    const uint32_t by_dim = (uint32_t)std::ceil(T(20) * std::sqrt(static_cast<T>(n)));
-    return std::max<uint32_t>(20, std::min<uint32_t>(by_dim, n));
-  }
-
-  static void validate_settings(const qpcg_settings& s) {  // settings.hpp:44-75 in T
-    auto bad = [](const char* m) { throw InvalidArgument(m); };
-    const T alpha = T(s.alpha);
-    if (!(alpha > T(0)) || !(alpha < T(2))) bad("settings: alpha must be in (0, 2)");
-    if (!(T(s.sigma) > T(0))) bad("settings: sigma must be positive");
-    if (!(T(s.rho_bar_init) > T(0))) bad("settings: rho_bar_init must be positive");
-    if (T(s.eps_abs) < T(0) || T(s.eps_rel) < T(0)) bad("settings: tolerances must be >= 0");
-    if (!(T(s.eps_pinf) > T(0)) || !(T(s.eps_dinf) > T(0)))
-      bad("settings: infeasibility tolerances must be positive");
-    if (s.max_admm_iter < 1 || s.check_interval < 1 || s.rho_update_interval < 1)
-      bad("settings: iteration counts must be >= 1");
-    if (!(T(s.lambda_pcg) > T(0)) || !(T(s.lambda_pcg) < T(1)))
-      bad("settings: lambda_pcg must be in (0, 1)");
-    if (!(T(s.eps_pcg_min) > T(0))) bad("settings: eps_pcg_min must be positive");
-    if (!(T(s.eps_equil) > T(0)) || s.equil_max_passes < 1)
-      bad("settings: bad equilibration parameters");
-  }
-
-  // ------------------------------------------------------ enqueue helpers
-  void enq_rhs(const Handles&) {
-    k_pack_rhs<T><<<grid_for(D.m), kThreads, 0, s>>>(D);
-    CK_LAUNCH();
-    launch_spmv<T, 2, SumOp>(D.AT, D.pAT, GatherRhs<T>{D.g2m}, EpiRhs<T>{D, T(0)}, s);
-  }
-  void enq_pcg_init(const Handles& H) {
-    k_pcg_init<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D, H);
-    CK_LAUNCH();
-  }
-  void enq_pcg_iter(const Handles& H) {
-    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
-    launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
-    k_pcg_dot<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D);
-    CK_LAUNCH();
-    k_pcg_update<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D, H);
-    CK_LAUNCH();
-    k_pcg_pupdate<T><<<grid_for(D.n), kThreads, 0, s>>>(D);
-    CK_LAUNCH();
-  }
-  void enq_post_pcg(const Handles& H) {
-    k_pcg_fin<T><<<grid_for(D.n), kThreads, 0, s>>>(D);
-    CK_LAUNCH();
-    launch_spmv<T, 2, SumOp>(D.A, D.pA, GatherAdmm<T>{D.g2n},
-                             EpiAdmm<T, 2>{D, T(0), T(0), T(0), false}, s);
-    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.xt},
-                             EpiAdmm<T, 1>{D, T(0), T(0), T(0), false}, s);
-    k_xupdate<T><<<grid_for(D.n), kThreads, 0, s>>>(D, H);
-    CK_LAUNCH();
-  }
-  void enq_check(const Handles& H, int mode) {
-    launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.y}, EpiDual<T>{D}, s);
-    k_residuals<T><<<red_grid<T>(std::max(D.n, D.m)), kThreads, 0, s>>>(D, mode, H);
-    CK_LAUNCH();
-  }
-  void enq_infeas(const Handles&) {
-    k_infeas_vec<T><<<red_grid<T>(std::max(D.n, D.m)), kThreads, 0, s>>>(D);
-    CK_LAUNCH();
-    launch_spmv<T, 1, SumOp>(
-        D.ATo, D.pATo, GatherCertY<T>{D.e, D.dy, D.ctl, T(0), T(0)},
-        EpiNormMax<T>{&D.ctl->atv_inf_bits, &D.ctl->need_pinf}, s);
-    launch_spmv<T, 1, SumOp>(D.Po, D.pPo, GatherCertX<T>{D.d, D.dx, D.ctl, T(0)},
-                             EpiNormMax<T>{&D.ctl->pv_inf_bits, &D.ctl->need_dinf}, s);
-    k_infeas_mid<T><<<1, 1, 0, s>>>(D);
-    CK_LAUNCH();
-    launch_spmv<T, 1, SumOp>(
-        D.Ao, D.pAo, GatherCertX<T>{D.d, D.dx, D.ctl, T(0)},
-        EpiDualRows<T>{D.l_o, D.u_o, &D.ctl->dinf_bad, &D.ctl->need_dinf, T(0), D.ctl}, s);
-    k_infeas<T><<<1, 1, 0, s>>>(D);
-    CK_LAUNCH();
-  }
-  void enq_rho_flag(const Handles& H) {
-    k_rho_flag<T><<<1, 1, 0, s>>>(D, H);
-    CK_LAUNCH();
-  }
-  void enq_rho(const Handles&) {
-    k_rho<T><<<red_grid<T>(D.m), kThreads, 0, s>>>(D);
-    CK_LAUNCH();
-    k_precond<T><<<grid_for(D.n), kThreads, 0, s>>>(D, 0);
-    CK_LAUNCH();
-  }
-  void enq_admm_cond(const Handles& H) {
-    k_admm_cond<T><<<1, 1, 0, s>>>(D, H);
-    CK_LAUNCH();
-  }
-  // residuals at the current iterates (solver.hpp:436, :517)
-  void enq_residuals_fresh(int mode) {
-    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.x}, EpiStore<T>{D.ax}, s);
-    enq_check(Handles{}, mode);
-  }
-
-  // ------------------------------------------------------- graph build
-  cudaGraph_t add_cond_in_capture(cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
-    cudaStreamCaptureStatus cs;
-    cudaGraph_t g;
-    const cudaGraphNode_t* deps = nullptr;
-    size_t nd = 0;
-    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = h;
-    cp.conditional.type = type;
-    cp.conditional.size = 1;
-    cudaGraphNode_t node;
-    CK(cudaGraphAddNode(&node, g, deps, nd, &cp));
-    CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
-    return cp.conditional.phGraph_out[0];
-  }
-
-  void build_graph() {
-    CK(cudaGraphCreate(&graph, 0));
-    cudaGraphConditionalHandle h_admm, h_pcg, h_chk, h_inf, h_rho;
-    CK(cudaGraphConditionalHandleCreate(&h_admm, graph, 1, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = h_admm;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t n_admm;
-    CK(cudaGraphAddNode(&n_admm, graph, nullptr, 0, &cp));
-    cudaGraph_t b_admm = cp.conditional.phGraph_out[0];
-    CK(cudaGraphConditionalHandleCreate(&h_pcg, b_admm, 0, cudaGraphCondAssignDefault));
-    CK(cudaGraphConditionalHandleCreate(&h_chk, b_admm, 0, cudaGraphCondAssignDefault));
-    CK(cudaGraphConditionalHandleCreate(&h_rho, b_admm, 0, cudaGraphCondAssignDefault));
-    Handles H;
-    H.admm = (unsigned long long)h_admm;
-    H.pcg = (unsigned long long)h_pcg;
-    H.chk = (unsigned long long)h_chk;
-    H.rho = (unsigned long long)h_rho;
-    cudaGraph_t b_pcg, b_chk, b_rho, b_inf, g_out;
-    CK(cudaStreamBeginCaptureToGraph(s, b_admm, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    enq_rhs(H);
-    enq_pcg_init(H);
-    b_pcg = add_cond_in_capture(h_pcg, cudaGraphCondTypeWhile);
-    enq_post_pcg(H);
-    b_chk = add_cond_in_capture(h_chk, cudaGraphCondTypeIf);
-    enq_rho_flag(H);
-    b_rho = add_cond_in_capture(h_rho, cudaGraphCondTypeIf);
-    enq_admm_cond(H);
-    CK(cudaStreamEndCapture(s, &g_out));
-    CK(cudaStreamBeginCaptureToGraph(s, b_pcg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    enq_pcg_iter(H);
-    CK(cudaStreamEndCapture(s, &g_out));
-    CK(cudaGraphConditionalHandleCreate(&h_inf, b_chk, 0, cudaGraphCondAssignDefault));
-    H.inf = (unsigned long long)h_inf;
-    CK(cudaStreamBeginCaptureToGraph(s, b_chk, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    enq_check(H, 0);
-    b_inf = add_cond_in_capture(h_inf, cudaGraphCondTypeIf);
-    CK(cudaStreamEndCapture(s, &g_out));
-    CK(cudaStreamBeginCaptureToGraph(s, b_inf, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    enq_infeas(H);
-    CK(cudaStreamEndCapture(s, &g_out));
-    CK(cudaStreamBeginCaptureToGraph(s, b_rho, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    enq_rho(H);
-    CK(cudaStreamEndCapture(s, &g_out));
-    CK(cudaGraphInstantiate(&exec, graph, 0));
-  }
-
-  // ------------------------------------------------- persistent loop
-  // The small-problem path (persist.cuh): the whole loop in one cooperative
-  // kernel.  Chosen automatically in graph mode while A fits the L2 budget.
-  T* persist_part = nullptr;
-  static uint64_t persist_max_nnz() {
-    const char* e = std::getenv("QPCG_PERSIST_MAX_NNZ");
-    return e ? std::strtoull(e, nullptr, 10) : 2000000ull;
-  }
-  bool use_persistent() const {
-    if (D.split) return false;
-    if (opt.mode == QPCG_MODE_PERSISTENT) return true;
-    return opt.mode == QPCG_MODE_GRAPH && uint64_t(D.A.nnz) + D.P.nnz <= persist_max_nnz();
-  }
-  static uint64_t cluster_max_nnz() {
-    const char* e = std::getenv("QPCG_CLUSTER_MAX_NNZ");
-    return e ? std::strtoull(e, nullptr, 10) : 15000ull;
-  }
-  void run_persistent() {
-    if (!persist_part) persist_part = alloc<T>(2 * kMaxQ * kMaxVirtual);
-    PersistBufs<T> B{persist_part, D.ctl};
-    void* args[] = {(void*)&D, (void*)&B};
-    const uint64_t work = uint64_t(D.A.nnz) + D.P.nnz;
-    static int cluster = -1;  // largest cluster the kernel can run as (same device model)
-    if (cluster < 0) {
-      cluster = 0;
-      auto* kc = k_admm_persistent<T, ClusterSync>;
-      if (cudaFuncSetAttribute(kc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
-        for (int c : {16, 8}) {
-          cudaLaunchConfig_t cfg = {};
-          cudaLaunchAttribute at[1];
-          at[0].id = cudaLaunchAttributeClusterDimension;
-          at[0].val.clusterDim.x = c;
-          at[0].val.clusterDim.y = 1;
-          at[0].val.clusterDim.z = 1;
-          cfg.gridDim = dim3(c);
-          cfg.blockDim = dim3(kThreads);
-          cfg.attrs = at;
-          cfg.numAttrs = 1;
-          int nc = 0;
-          if (cudaOccupancyMaxActiveClusters(&nc, kc, &cfg) == cudaSuccess && nc > 0) {
-            cluster = c;
-            break;
-          }
-        }
-      }
-      cudaGetLastError();
-    }
-    if (cluster > 0 && work <= cluster_max_nnz()) {
-      // tiny problem: one cluster, hardware barriers
-      cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = cluster;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3(cluster);
-      cfg.blockDim = dim3(kThreads);
-      cfg.stream = s;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      CK(cudaLaunchKernelExC(&cfg, (const void*)k_admm_persistent<T, ClusterSync>, args));
-      CK_LAUNCH();
-      return;
-    }
-    static int max_grid = 0;  // co-resident blocks (same device model for every workspace)
-    if (max_grid == 0) {
-      int per_sm = 0, sms = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_admm_persistent<T, GridSync>,
-                                                       kThreads, 0));
-      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-      max_grid = std::max(1, per_sm) * sms;
-    }
-    const int grid = max_grid;  // measured: more co-resident blocks is faster at every size
-    CK(cudaLaunchCooperativeKernel((const void*)k_admm_persistent<T, GridSync>, dim3(grid),
-                                   dim3(kThreads), args, 0, s));
-    CK_LAUNCH();
-  }
-
-  // ------------------------------------------------------- eager loop
-  void run_eager() {
-    Handles H{};
-    for (;;) {
-      pull_ctl();
-      if (hc.done || hc.error || hc.iter >= hc.max_iter) break;
-      enq_rhs(H);
-      enq_pcg_init(H);
-      pull_ctl();
-      while (hc.pcg_active && !hc.error) {
-        enq_pcg_iter(H);
-        pull_ctl();
-      }
-      enq_post_pcg(H);
-      pull_ctl();
-      if (hc.is_check && !hc.error) {
-        enq_check(H, 0);
-        pull_ctl();
-        if (hc.inf_branch) enq_infeas(H);
-      }
-      enq_rho_flag(H);
-      enq_rho(H);
-    }
-  }
-
-  // ------------------------------------------------------------ solve
-  // reset the per-solve state (solver.hpp:412, :430-443)
-  void reset_solve_state() {
-    pull_ctl();
-    hc.iter = 0;
-    hc.done = 0;
-    hc.error = 0;
-    hc.status = QPCG_STATUS_MAX_ITER_REACHED;
-    hc.pcg_total = 0;
-    hc.rho_update_count = 0;
-    hc.n_calls = hc.n_checks = hc.n_rho = 0;
-    hc.pcg_active = 0;
-    hc.red_counter = 0;
-    hc.n_inf = 0;
-    hc.n_rho_branch = 0;
-    push_ctl();
-  }
-  void raise_device_error() {
-    if (hc.error == kErrNotPD)
-      throw NotPositiveDefinite("pcg: encountered direction of nonpositive curvature");
-    if (hc.error == kErrInvalid) {
-      if (hc.n_rho > 0 && !(hc.rho > T(0))) throw InvalidArgument("kkt operator: rho must be positive");
-      throw InvalidArgument("pcg: warm start must be finite");
-    }
-  }
-  void fill_info(qpcg_info* info, double solve_s, double d2h, uint32_t n, uint32_t m) const {
-    const bool has_cert = hc.status == 1 || hc.status == 2;
-    std::memset(info, 0, sizeof(*info));
-    info->status = int32_t(hc.status);
-    info->iterations = hc.iter;
-    info->pcg_iterations_total = hc.pcg_total;
-    info->objective = double(hc.objective);
-    info->r_prim_inf = double(hc.rp_o);
-    info->r_dual_inf = double(hc.rd_o);
-    info->equil_passes = equil_passes;
-    info->rho_update_count = hc.rho_update_count;
-    info->equil_residual = double(equil_residual);
-    info->rho_final = double(hc.rho);
-    info->certificate_valid = has_cert;
-    info->n = n;
-    info->m = m;
-    info->setup_seconds = setup_seconds;
-    info->solve_seconds = solve_s;
-    info->h2d_seconds = h2d_seconds;
-    info->d2h_seconds = opt.input_memory == QPCG_MEM_HOST ? d2h : 0.0;
-    info->h2d_bytes = h2d_bytes;
-    info->d2h_bytes = opt.input_memory == QPCG_MEM_HOST
-                          ? sizeof(T) * (uint64_t(n) + 2ull * m) +
-                                (has_cert ? sizeof(T) * (hc.status == 1 ? m : n) : 0)
-                          : 0;
-  }
-
-  void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) {
-    CK(cudaSetDevice(device));
-    AllocScope scope(s);
-    const double w0 = now_s();
-    CK(cudaEventRecord(ev0, s));
-    reset_solve_state();
-    uint64_t graph_build = 0;
-    const uint64_t l0 = g_launches;
-    // initial residuals and PCG tolerance (solver.hpp:436-441)
-    enq_residuals_fresh(1);
-    if (opt.mode == QPCG_MODE_EAGER) {
-      run_eager();
-    } else if (use_persistent()) {
-      run_persistent();
-    } else {
-      if (!exec) {
-        const uint64_t b0 = g_launches;
-        build_graph();
-        graph_build = g_launches - b0;
-      }
-      CK(cudaGraphLaunch(exec, s));
-    }
-    pull_ctl();
-    raise_device_error();
-    if (!hc.residuals_current) enq_residuals_fresh(2);
-    k_unscale<T><<<grid_for(std::max(D.n, D.m)), kThreads, 0, s>>>(D);
-    CK_LAUNCH();
-    if (hc.status != 1 && hc.status != 2)
-      launch_spmv<T, 1, SumOp>(D.Po, D.pPo, GatherVec<T>{D.xo}, EpiStore<T>{D.pxo}, s);
-    k_objective<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D);
-    CK_LAUNCH();
-    CK(cudaEventRecord(ev1, s));
-    pull_ctl();
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, ev0, ev1));
-    const double td = now_s();
-    download(x, D.xo, sizeof(T) * D.n);
-    download(z, D.zo, sizeof(T) * D.m);
-    download(y, D.yo, sizeof(T) * D.m);
-    const bool has_cert = hc.status == 1 || hc.status == 2;
-    uint64_t launches = g_launches - l0 - graph_build;
-    if (opt.mode != QPCG_MODE_EAGER && !use_persistent())  // kernels executed inside the graph
-      launches += 9ull * hc.iter + 5ull * hc.pcg_total + 2ull * hc.n_checks + 6ull * hc.n_inf +
-                  2ull * hc.n_rho_branch;
-    if (has_cert) download(cert, D.cert, sizeof(T) * (hc.status == 1 ? D.m : D.n));
-    CK(cudaStreamSynchronize(s));
-    const double d2h = now_s() - td;
-    have_solved = true;
-    if (info) {
-      fill_info(info, ms * 1e-3, d2h, D.n, D.m);
-      info->runtime_seconds = now_s() - w0;
-      info->kernel_launches = launches + (have_counted_setup ? 0 : setup_launches);
-    }
-    have_counted_setup = true;
-  }
-
-  // ------------------------------------------------- OSQP-style updates
-  void warm_start(const T* x, const T* z, const T* y) {  // solver.hpp:413-428
-    CK(cudaSetDevice(device));
-    AllocScope scope(s);
-    if (warm_stage(x, z, y) != ~0ull) throw InvalidArgument("solve: warm start must be finite");
-    warm_apply();
-  }
-  // upload + finiteness key (~0 = all finite); the sharded path combines the
-  // keys of its row blocks before anyone throws
-  T *w_tx = nullptr, *w_tz = nullptr, *w_ty = nullptr;
-  unsigned long long warm_stage(const T* x, const T* z, const T* y) {
-    const uint32_t n = D.n, m = D.m;
-    w_tx = vec(n, false);
-    w_tz = vec(m, false);
-    w_ty = vec(m, false);
-    upload(w_tx, x, sizeof(T) * n);
-    upload(w_tz, z, sizeof(T) * m);
-    upload(w_ty, y, sizeof(T) * m);
-    unsigned long long* key = alloc<unsigned long long>(1);
-    CK(cudaMemsetAsync(key, 0xff, 8, s));
-    validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(w_tx, n, 1, key);
-    validate_values_kernel<T><<<grid_for(m), kThreads, 0, s>>>(w_tz, m, 1, key);
-    validate_values_kernel<T><<<grid_for(m), kThreads, 0, s>>>(w_ty, m, 1, key);
-    CK_LAUNCH();
-    unsigned long long k;
-    CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    return k;
-  }
-  void warm_apply() {
-    const uint32_t n = D.n, m = D.m;
-    const T c = hc.c;
-    T *X = D.x, *XT = D.xt, *Z = D.z, *Y = D.y, *di = D.d_inv, *e = D.e, *ei = D.e_inv;
-    const T *tx = w_tx, *tz = w_tz, *ty = w_ty;
-    for_n(n, [=] __device__(uint32_t i) {
-      const T v = di[i] * tx[i];
-      X[i] = v;
-      XT[i] = v;
-    }, s);
-    for_n(m, [=] __device__(uint32_t j) {
-      Z[j] = e[j] * tz[j];
-      Y[j] = (ei[j] * ty[j]) * c;
-    }, s);
-    // keep the invariant zt == A x~ used by the fused r0 (pcg_warm = x)
-    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.xt}, EpiStore<T>{D.zt}, s);
-    CK(cudaStreamSynchronize(s));
-  }
-
-  void update_rho(T rho) {  // linsys.hpp:153-157
-    if (!(rho > T(0))) throw InvalidArgument("kkt operator: rho must be positive");
-    CK(cudaSetDevice(device));
-    pull_ctl();
-    hc.rho = rho;
-    push_ctl();
-    k_precond<T><<<grid_for(D.n), kThreads, 0, s>>>(D, 1);
-    CK_LAUNCH();
-    CK(cudaStreamSynchronize(s));
-  }
-
-  // ----------------------------------------------------- debug / bench
-  void debug_scaled(T* pv, uint32_t* prp, uint32_t* pci, T* q, T* av, T* atv, uint32_t* atrp,
-                    uint32_t* atci, T* l, T* u, T* d, T* e, double* scal) {
-    CK(cudaSetDevice(device));
-    auto dl = [&](void* dst, const void* src, size_t b) {
-      if (dst) CK(cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToHost, s));
-    };
-    dl(pv, D.P.val, sizeof(T) * D.P.nnz);
-    dl(prp, D.P.rp, 4 * (size_t(D.n) + 1));
-    dl(pci, D.P.ci, 4 * size_t(D.P.nnz));
-    dl(q, D.q, sizeof(T) * D.n);
-    dl(av, D.A.val, sizeof(T) * D.A.nnz);
-    dl(atv, D.AT.val, sizeof(T) * D.AT.nnz);
-    dl(atrp, D.AT.rp, 4 * (size_t(D.n) + 1));
-    dl(atci, D.AT.ci, 4 * size_t(D.AT.nnz));
-    dl(l, D.l, sizeof(T) * D.m);
-    dl(u, D.u, sizeof(T) * D.m);
-    dl(d, D.d, sizeof(T) * D.n);
-    dl(e, D.e, sizeof(T) * D.m);
-    CK(cudaStreamSynchronize(s));
-    if (scal) {
-      scal[0] = double(hc.c);
-      scal[1] = double(hc.c_inv);
-      scal[2] = double(equil_passes);
-      scal[3] = double(equil_residual);
-    }
-  }
-
-  void debug_operator(const T* x, T* kx, T* dinv) {
-    CK(cudaSetDevice(device));
-    AllocScope scope(s);
-    pull_ctl();
-    const Ctl<T> saved = hc;
-    hc.pcg_active = 1;
-    hc.error = 0;
-    push_ctl();
-    CK(cudaMemcpyAsync(D.p, x, sizeof(T) * D.n, cudaMemcpyHostToDevice, s));
-    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
-    launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
-    if (kx) CK(cudaMemcpyAsync(kx, D.kp, sizeof(T) * D.n, cudaMemcpyDeviceToHost, s));
-    if (dinv) CK(cudaMemcpyAsync(dinv, D.dinv, sizeof(T) * D.n, cudaMemcpyDeviceToHost, s));
-    hc = saved;
-    push_ctl();
-    CK(cudaStreamSynchronize(s));
-  }
-
-  // CUDA-event timing of the PCG-iteration kernels (bench.py roofline)
-  void bench_kernels(uint32_t reps, double* out) {
-    CK(cudaSetDevice(device));
-    AllocScope scope(s);
-    pull_ctl();
-    const Ctl<T> saved = hc;
-    Ctl<T> run = hc;
-    run.pcg_active = 1;
-    run.error = 0;
-    run.done = 0;
-    run.rm = T(1);
-    run.thr = T(0);
-    run.best_norm = (T)INFINITY;
-    run.pcg_cap = 0xffffffffu;
-    run.k = 0;
-    fill(D.p, D.n, T(1));
-    fill(D.r, D.n, T(1));
-    std::vector<cudaEvent_t> ev(2 * reps);
-    for (auto& e : ev) CK(cudaEventCreate(&e));
-    double acc[3] = {0, 0, 0};
-    for (int which = 0; which < 3; ++which) {
-      for (uint32_t i = 0; i < reps; ++i) {
-        hc = run;
-        push_ctl();
-        CK(cudaEventRecord(ev[2 * i], s));
-        if (which == 0)
-          launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
-        else if (which == 1)
-          launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
-        else
-          enq_pcg_iter(Handles{});
-        CK(cudaEventRecord(ev[2 * i + 1], s));
-      }
-      CK(cudaStreamSynchronize(s));
-      double tot = 0;
-      for (uint32_t i = 0; i < reps; ++i) {
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
-        tot += ms;
-      }
-      acc[which] = tot / reps;
-    }
-    for (auto& e : ev) cudaEventDestroy(e);
-    hc = saved;
-    push_ctl();
-    CK(cudaStreamSynchronize(s));
-    const double S = sizeof(T);
-    auto mb = [&](const DevCsr<T>& M) { return double(M.nnz) * (S + 4) + (double(M.rows) + 1) * 4; };
-    const double n = D.n, m = D.m;
-    out[0] = acc[0];
-    out[1] = acc[1];
-    out[2] = acc[2];
-    out[3] = mb(D.A) + S * n + S * m;                    // read A, p; write t
-    out[4] = mb(D.AT) + mb(D.P) + S * m + 2 * S * n;     // read A^T, P, t, p; write Kp
-    out[5] = mb(D.A) + mb(D.AT) + mb(D.P) + S * (2 * m + 11 * n);
-    // the same with the bytes of the formats actually streamed (compressed
-    // column offsets where the plan has them)
-    const double fa = plan_stream_bytes(D.A, D.pA), fat = plan_stream_bytes(D.AT, D.pAT);
-    out[6] = fa + S * n + S * m;
-    out[7] = fat + mb(D.P) + S * m + 2 * S * n;
-    out[8] = fa + fat + mb(D.P) + S * (2 * m + 11 * n);
-  }
-
-  // Not in the reference: rescale with the existing D, E, c.
-  void update_vectors(const T* q, const T* l, const T* u) {
-    CK(cudaSetDevice(device));
-    AllocScope scope(s);
-    const unsigned long long k = vectors_stage(q, l, u);
-    if (k != ~0ull) throw InvalidArgument(validation_message(k));
-    vectors_apply();
-  }
-  unsigned long long vectors_stage(const T* q, const T* l, const T* u) {
-    const uint32_t n = D.n, m = D.m;
-    if (q) upload(D.q_o, q, sizeof(T) * n);
-    if (l) upload(D.l_o, l, sizeof(T) * m);
-    if (u) upload(D.u_o, u, sizeof(T) * m);
-    unsigned long long* key = alloc<unsigned long long>(1);
-    CK(cudaMemsetAsync(key, 0xff, 8, s));
-    validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.q_o, n, kValQFinite, key);
-    validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(D.l_o, D.u_o, m, key, row0);
-    CK_LAUNCH();
-    unsigned long long k;
-    CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    return k;
-  }
-  void vectors_apply() {
-    const uint32_t n = D.n, m = D.m;
-    const T c = hc.c;
-    T *qs = D.q, *qo = D.q_o, *d = D.d, *e = D.e, *ls = D.l, *us = D.u, *lo = D.l_o, *uo = D.u_o;
-    for_n(n, [=] __device__(uint32_t i) { qs[i] = c * (d[i] * qo[i]); }, s);
-    for_n(m, [=] __device__(uint32_t j) {
-      ls[j] = e[j] * lo[j];
-      us[j] = e[j] * uo[j];
-    }, s);
-    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q_o, n, D.red, &D.ctl->red_counter,
-                                                      &D.ctl->q_inf_orig);
-    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s>>>(D.q, n, D.red, &D.ctl->red_counter,
-                                                      &D.ctl->q_inf_scaled);
-    CK_LAUNCH();
-    CK(cudaStreamSynchronize(s));
-    pull_ctl();
-  }
-};
-
-}  // namespace qpcg_b200
+// engine.cu — the C-ABI (include/qpcg_b200.h, include/qpcg_b200_ops.h) over
+// the B200 ADMM/PCG workspace (workspace.cuh) and its row-sharded variant
+// (shard.cuh).  See workspace.cuh for the per-step kernel sequence.
+#include "workspace.cuh"
 
 #include "shard.cuh"
 
@@ -1183,10 +12,8 @@ using namespace qpcg_b200;
 
 struct qpcg_workspace {
   int precision = 64;
-  std::unique_ptr<Workspace<double>> w64;
-  std::unique_ptr<Workspace<float>> w32;
-  std::unique_ptr<Sharded<double>> s64;  // row-sharded (options.virtual_shards / nccl)
-  std::unique_ptr<Sharded<float>> s32;
+  std::unique_ptr<IEngine<double>> e64;  // Workspace<double> or Sharded<double>
+  std::unique_ptr<IEngine<float>> e32;
   std::string err;
 };
 
@@ -1227,17 +54,11 @@ HostCsr<T> host_csr(const CsrT* c) {
 }
 
 template <typename T>
-std::unique_ptr<Workspace<T>>& slot(qpcg_workspace* ws);
+std::unique_ptr<IEngine<T>>& slot(qpcg_workspace* ws);
 template <>
-std::unique_ptr<Workspace<double>>& slot<double>(qpcg_workspace* ws) { return ws->w64; }
+std::unique_ptr<IEngine<double>>& slot<double>(qpcg_workspace* ws) { return ws->e64; }
 template <>
-std::unique_ptr<Workspace<float>>& slot<float>(qpcg_workspace* ws) { return ws->w32; }
-template <typename T>
-std::unique_ptr<Sharded<T>>& sslot(qpcg_workspace* ws);
-template <>
-std::unique_ptr<Sharded<double>>& sslot<double>(qpcg_workspace* ws) { return ws->s64; }
-template <>
-std::unique_ptr<Sharded<float>>& sslot<float>(qpcg_workspace* ws) { return ws->s32; }
+std::unique_ptr<IEngine<float>>& slot<float>(qpcg_workspace* ws) { return ws->e32; }
 
 bool is_sharded(const qpcg_options& o) { return o.virtual_shards > 1 || o.nccl_id != nullptr; }
 
@@ -1258,13 +79,8 @@ int setup_impl(qpcg_workspace** out, const CsrT* p, const T* q, const CsrT* a, c
   qpcg_default_options(&op);
   if (o) op = *o;
   const int rc = guarded(ws, [&] {
-    if (is_sharded(op)) {
-      sslot<T>(ws).reset(new Sharded<T>());
-      sslot<T>(ws)->setup(host_csr<T>(p), q, host_csr<T>(a), l, u, st, op);
-    } else {
-      slot<T>(ws).reset(new Workspace<T>());
-      slot<T>(ws)->setup(host_csr<T>(p), q, host_csr<T>(a), l, u, st, op);
-    }
+    slot<T>(ws).reset(make_engine<T>(is_sharded(op)));
+    slot<T>(ws)->setup(host_csr<T>(p), q, host_csr<T>(a), l, u, st, op);
   });
   if (rc != QPCG_OK) {
     g_last_error = ws->err;
@@ -1277,21 +93,9 @@ int setup_impl(qpcg_workspace** out, const CsrT* p, const T* q, const CsrT* a, c
 }
 
 template <typename T>
-Workspace<T>* get(qpcg_workspace* ws) {
-  if (ws == nullptr || !slot<T>(ws)) throw InvalidArgument("workspace: wrong precision or null");
-  return slot<T>(ws).get();
-}
-// f(engine) on the workspace's single-device or sharded engine
-template <typename T, typename F>
-void run(qpcg_workspace* ws, F&& f) {
-  if (ws != nullptr && sslot<T>(ws)) return f(*sslot<T>(ws));
-  f(*get<T>(ws));
-}
-// the block whose control block and diagnostics speak for the solve
-template <typename T>
-Workspace<T>* primary(const qpcg_workspace* w) {
+IEngine<T>* get(const qpcg_workspace* w) {
   auto* ws = const_cast<qpcg_workspace*>(w);
-  if (sslot<T>(ws)) return &sslot<T>(ws)->w0();
+  if (ws == nullptr || !slot<T>(ws)) throw InvalidArgument("workspace: wrong precision or null");
   return slot<T>(ws).get();
 }
 
@@ -1303,10 +107,8 @@ int solve_problem_impl(const CsrT* p, const T* q, const CsrT* a, const T* l, con
   const double t0 = now_s();
   qpcg_workspace* ws = nullptr;
   int rc = setup_impl<T>(&ws, p, q, a, l, u, s, o);
-  if (rc == QPCG_OK && wx != nullptr)
-    rc = guarded(ws, [&] { run<T>(ws, [&](auto& w) { w.warm_start(wx, wz, wy); }); });
-  if (rc == QPCG_OK)
-    rc = guarded(ws, [&] { run<T>(ws, [&](auto& w) { w.solve(info, x, z, y, cert); }); });
+  if (rc == QPCG_OK && wx != nullptr) rc = guarded(ws, [&] { get<T>(ws)->warm_start(wx, wz, wy); });
+  if (rc == QPCG_OK) rc = guarded(ws, [&] { get<T>(ws)->solve(info, x, z, y, cert); });
   if (rc == QPCG_OK && info) info->runtime_seconds = now_s() - t0;  // solver.hpp:392 -> :537
   if (rc != QPCG_OK && msg && msg_len) {
     const std::string& e = ws ? ws->err : g_last_error;
@@ -1316,44 +118,18 @@ int solve_problem_impl(const CsrT* p, const T* q, const CsrT* a, const T* l, con
   return rc;
 }
 
-template <typename T>
-uint32_t calls_of(Workspace<T>* w, qpcg_pcg_call* out, uint32_t cap) {
-  const uint32_t n = std::min(w->hc.n_calls, w->hc.diag_cap);
-  std::vector<DiagRec<T>> recs(n);
-  if (n) {
-    cudaMemcpy(recs.data(), w->D.calls, sizeof(DiagRec<T>) * n, cudaMemcpyDeviceToHost);
-  }
-  for (uint32_t i = 0; i < n && i < cap; ++i) {
-    out[i].admm_iter = recs[i].admm_iter;
-    out[i].iterations = recs[i].iterations;
-    out[i].eps = double(recs[i].eps);
-    out[i].r_prim_scaled_inf = double(recs[i].rp);
-    out[i].r_dual_scaled_inf = double(recs[i].rd);
-    out[i].converged = int32_t(recs[i].converged);
-    out[i].reserved_ = 0;
-  }
-  return n;
-}
-template <typename T>
-uint32_t rhos_of(Workspace<T>* w, qpcg_rho_update* out, uint32_t cap) {
-  const uint32_t n = std::min(w->hc.n_rho, w->hc.diag_cap);
-  std::vector<RhoRec<T>> recs(n);
-  if (n) cudaMemcpy(recs.data(), w->D.rhos, sizeof(RhoRec<T>) * n, cudaMemcpyDeviceToHost);
-  for (uint32_t i = 0; i < n && i < cap; ++i) {
-    out[i].admm_iter = recs[i].admm_iter;
-    out[i].reserved_ = 0;
-    out[i].rho_before = double(recs[i].before);
-    out[i].rho_after = double(recs[i].after);
-  }
-  return n;
-}
-template <typename T>
-uint32_t checks_of(Workspace<T>* w, uint32_t* out, uint32_t cap) {
-  const uint32_t n = std::min(w->hc.n_checks, w->hc.diag_cap);
-  std::vector<uint32_t> recs(n);
-  if (n) cudaMemcpy(recs.data(), w->D.checks, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost);
-  for (uint32_t i = 0; i < n && i < cap; ++i) out[i] = recs[i];
-  return n;
+// f(engine) on whichever precision the workspace holds
+template <typename F>
+int either(const qpcg_workspace* w, F&& f) {
+  auto* ws = const_cast<qpcg_workspace*>(w);
+  return guarded(ws, [&] {
+    if (ws && ws->e64)
+      f(*ws->e64);
+    else if (ws && ws->e32)
+      f(*ws->e32);
+    else
+      throw InvalidArgument("workspace: null");
+  });
 }
 
 }  // namespace
@@ -1390,7 +166,7 @@ void qpcg_default_options(qpcg_options* o) {
 
 int qpcg_validate_settings(const qpcg_settings* s, char* msg, size_t msg_len) {
   try {
-    Workspace<double>::validate_settings(*s);
+    validate_settings_in<double>(*s);
     return QPCG_OK;
   } catch (const std::exception& e) {
     if (msg && msg_len) std::snprintf(msg, msg_len, "%s", e.what());
@@ -1411,30 +187,30 @@ int qpcg_f32_setup(qpcg_workspace** ws, const qpcg_csr_f32* p, const float* q,
   return setup_impl<float>(ws, p, q, a, l, u, s, o);
 }
 int qpcg_f64_warm_start(qpcg_workspace* ws, const double* x, const double* z, const double* y) {
-  return guarded(ws, [&] { run<double>(ws, [&](auto& w) { w.warm_start(x, z, y); }); });
+  return guarded(ws, [&] { get<double>(ws)->warm_start(x, z, y); });
 }
 int qpcg_f32_warm_start(qpcg_workspace* ws, const float* x, const float* z, const float* y) {
-  return guarded(ws, [&] { run<float>(ws, [&](auto& w) { w.warm_start(x, z, y); }); });
+  return guarded(ws, [&] { get<float>(ws)->warm_start(x, z, y); });
 }
 int qpcg_f64_update_rho(qpcg_workspace* ws, double rho) {
-  return guarded(ws, [&] { run<double>(ws, [&](auto& w) { w.update_rho(rho); }); });
+  return guarded(ws, [&] { get<double>(ws)->update_rho(rho); });
 }
 int qpcg_f32_update_rho(qpcg_workspace* ws, double rho) {
-  return guarded(ws, [&] { run<float>(ws, [&](auto& w) { w.update_rho(float(rho)); }); });
+  return guarded(ws, [&] { get<float>(ws)->update_rho(float(rho)); });
 }
 int qpcg_f64_update_vectors(qpcg_workspace* ws, const double* q, const double* l, const double* u) {
-  return guarded(ws, [&] { run<double>(ws, [&](auto& w) { w.update_vectors(q, l, u); }); });
+  return guarded(ws, [&] { get<double>(ws)->update_vectors(q, l, u); });
 }
 int qpcg_f32_update_vectors(qpcg_workspace* ws, const float* q, const float* l, const float* u) {
-  return guarded(ws, [&] { run<float>(ws, [&](auto& w) { w.update_vectors(q, l, u); }); });
+  return guarded(ws, [&] { get<float>(ws)->update_vectors(q, l, u); });
 }
 int qpcg_f64_solve(qpcg_workspace* ws, qpcg_info* info, double* x, double* z, double* y,
                    double* cert) {
-  return guarded(ws, [&] { run<double>(ws, [&](auto& w) { w.solve(info, x, z, y, cert); }); });
+  return guarded(ws, [&] { get<double>(ws)->solve(info, x, z, y, cert); });
 }
 int qpcg_f32_solve(qpcg_workspace* ws, qpcg_info* info, float* x, float* z, float* y,
                    float* cert) {
-  return guarded(ws, [&] { run<float>(ws, [&](auto& w) { w.solve(info, x, z, y, cert); }); });
+  return guarded(ws, [&] { get<float>(ws)->solve(info, x, z, y, cert); });
 }
 int qpcg_f64_solve_problem(const qpcg_csr_f64* p, const double* q, const qpcg_csr_f64* a,
                            const double* l, const double* u, const qpcg_settings* s,
@@ -1474,111 +250,52 @@ const char* qpcg_last_error(const qpcg_workspace* ws) {
 }
 
 uint32_t qpcg_get_pcg_calls(const qpcg_workspace* ws, qpcg_pcg_call* out, uint32_t cap) {
-  if (!ws) return 0;
-  if (Workspace<double>* w = primary<double>(ws)) return calls_of(w, out, cap);
-  if (Workspace<float>* w = primary<float>(ws)) return calls_of(w, out, cap);
-  return 0;
+  uint32_t k = 0;
+  either(ws, [&](auto& e) { k = e.pcg_calls(out, cap); });
+  return k;
 }
 uint32_t qpcg_get_rho_updates(const qpcg_workspace* ws, qpcg_rho_update* out, uint32_t cap) {
-  if (!ws) return 0;
-  if (Workspace<double>* w = primary<double>(ws)) return rhos_of(w, out, cap);
-  if (Workspace<float>* w = primary<float>(ws)) return rhos_of(w, out, cap);
-  return 0;
+  uint32_t k = 0;
+  either(ws, [&](auto& e) { k = e.rho_updates(out, cap); });
+  return k;
 }
 uint32_t qpcg_get_check_iterations(const qpcg_workspace* ws, uint32_t* out, uint32_t cap) {
-  if (!ws) return 0;
-  if (Workspace<double>* w = primary<double>(ws)) return checks_of(w, out, cap);
-  if (Workspace<float>* w = primary<float>(ws)) return checks_of(w, out, cap);
-  return 0;
+  uint32_t k = 0;
+  either(ws, [&](auto& e) { k = e.check_iterations(out, cap); });
+  return k;
 }
 
 int qpcg_debug_dims(const qpcg_workspace* ws, uint64_t* dims) {
-  if (!ws) return QPCG_ERR_INVALID;
-  auto fill = [&](auto* w) {
-    dims[0] = w->D.n;
-    dims[1] = w->D.m;
-    dims[2] = w->D.P.nnz;
-    dims[3] = w->D.A.nnz;
-    dims[4] = w->equil_passes;
-    dims[5] = 0;
-  };
-  if (ws->w64) fill(ws->w64.get());
-  else if (ws->w32) fill(ws->w32.get());
-  else return QPCG_ERR_INVALID;
-  return QPCG_OK;
+  return either(ws, [&](auto& e) { e.dims(dims); });
 }
 
 int qpcg_debug_scaled(const qpcg_workspace* ws, void* pv, uint32_t* prp, uint32_t* pci, void* q,
                       void* av, void* atv, uint32_t* atrp, uint32_t* atci, void* l, void* u,
                       void* d, void* e, double* scal) {
-  auto* w = const_cast<qpcg_workspace*>(ws);
-  return guarded(w, [&] {
-    if (w->w64)
-      w->w64->debug_scaled((double*)pv, prp, pci, (double*)q, (double*)av, (double*)atv, atrp,
-                           atci, (double*)l, (double*)u, (double*)d, (double*)e, scal);
-    else
-      get<float>(w)->debug_scaled((float*)pv, prp, pci, (float*)q, (float*)av, (float*)atv, atrp,
-                                  atci, (float*)l, (float*)u, (float*)d, (float*)e, scal);
+  return either(ws, [&](auto& en) {
+    using T = typename std::remove_reference_t<decltype(en)>::value_type;
+    en.debug_scaled((T*)pv, prp, pci, (T*)q, (T*)av, (T*)atv, atrp, atci, (T*)l, (T*)u, (T*)d,
+                    (T*)e, scal);
   });
 }
 
 int qpcg_debug_operator(qpcg_workspace* ws, const void* x, void* kx, void* dinv) {
-  return guarded(ws, [&] {
-    if (ws && ws->w64)
-      ws->w64->debug_operator((const double*)x, (double*)kx, (double*)dinv);
-    else
-      get<float>(ws)->debug_operator((const float*)x, (float*)kx, (float*)dinv);
+  return either(ws, [&](auto& en) {
+    using T = typename std::remove_reference_t<decltype(en)>::value_type;
+    en.debug_operator((const T*)x, (T*)kx, (T*)dinv);
   });
 }
 
 int qpcg_bench_kernels(qpcg_workspace* ws, uint32_t reps, double* out) {
   // (sharded workspaces: the kernels of this process's first row block)
-  return guarded(ws, [&] {
-    if (Workspace<double>* w = ws ? primary<double>(ws) : nullptr)
-      w->bench_kernels(reps, out);
-    else if (Workspace<float>* w = ws ? primary<float>(ws) : nullptr)
-      w->bench_kernels(reps, out);
-    else
-      throw InvalidArgument("workspace: null");
-  });
+  return either(ws, [&](auto& e) { e.bench_kernels(reps, out); });
 }
 
 }  // extern "C"
 
 template <typename T, typename CsrT>
 static int op_spmv_impl(const CsrT* mv, const T* x, T* y, int device) {
-  return guarded(nullptr, [&] {
-    if (device >= 0) CK(cudaSetDevice(device));
-    cudaStream_t s;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    AllocScope scope(s);
-    CubTemp tmp;
-    DevCsr<T> M{mv->rows, mv->cols, mv->nnz, nullptr, nullptr, nullptr};
-    T *dx, *dy;
-    CK(dmalloc(&M.val, sizeof(T) * (M.nnz + 1)));
-    CK(dmalloc(&M.ci, 4 * (size_t(M.nnz) + 1)));
-    CK(dmalloc(&M.rp, 4 * (size_t(M.rows) + 1)));
-    CK(dmalloc(&dx, sizeof(T) * (M.cols + 1)));
-    CK(dmalloc(&dy, sizeof(T) * (M.rows + 1)));
-    CK(cudaMemcpyAsync(M.val, mv->values, sizeof(T) * M.nnz, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(M.ci, mv->col_indices, 4 * size_t(M.nnz), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(M.rp, mv->row_ptr, 4 * (size_t(M.rows) + 1), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(dx, x, sizeof(T) * M.cols, cudaMemcpyHostToDevice, s));
-    SpmvPlan<T> P = plan_build<T>(M.rp, M.rows, tmp, s);
-    launch_spmv<T, 1, SumOp>(M, P, GatherVec<T>{dx}, EpiStore<T>{dy}, s);
-    CK(cudaMemcpyAsync(y, dy, sizeof(T) * M.rows, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    plan_free(P);
-    dfree(M.val);
-    dfree(M.ci);
-    dfree(M.rp);
-    dfree(dx);
-    dfree(dy);
-    if (tmp.ptr) dfree(tmp.ptr);
-    tmp.ptr = nullptr;
-    CK(cudaStreamSynchronize(s));
-    cudaStreamDestroy(s);
-  });
+  return guarded(nullptr, [&] { op_spmv<T>(host_csr<T>(mv), x, y, device); });
 }
 
 extern "C" {

@@ -1,0 +1,59 @@
+// engine_f64.cu — the double engine: explicit instantiation of Workspace<double> and
+// Sharded<double> plus the typed entry points behind IEngine (workspace.cuh).
+// engine.cu, engine_f64.cu and engine_f32.cu compile in parallel (build.py).
+#include "workspace.cuh"
+#include "shard.cuh"
+
+namespace qpcg_b200 {
+
+template class Workspace<double>;
+template class Sharded<double>;
+
+template <>
+IEngine<double>* make_engine<double>(bool sharded) {
+  if (sharded) return new Sharded<double>();
+  return new Workspace<double>();
+}
+
+template <>
+void validate_settings_in<double>(const qpcg_settings& s) {
+  Workspace<double>::validate_settings(s);
+}
+
+// y = M x through the plan-driven SpMV (operator-level entry point)
+template <>
+void op_spmv<double>(const HostCsr<double>& mv, const double* x, double* y, int device) {
+  using T = double;
+  if (device >= 0) CK(cudaSetDevice(device));
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  AllocScope scope(s);
+  CubTemp tmp;
+  DevCsr<T> M{mv.rows, mv.cols, mv.nnz, nullptr, nullptr, nullptr};
+  T *dx, *dy;
+  CK(dmalloc(&M.val, sizeof(T) * (M.nnz + 1)));
+  CK(dmalloc(&M.ci, 4 * (size_t(M.nnz) + 1)));
+  CK(dmalloc(&M.rp, 4 * (size_t(M.rows) + 1)));
+  CK(dmalloc(&dx, sizeof(T) * (M.cols + 1)));
+  CK(dmalloc(&dy, sizeof(T) * (M.rows + 1)));
+  CK(cudaMemcpyAsync(M.val, mv.values, sizeof(T) * M.nnz, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(M.ci, mv.col_indices, 4 * size_t(M.nnz), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(M.rp, mv.row_ptr, 4 * (size_t(M.rows) + 1), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dx, x, sizeof(T) * M.cols, cudaMemcpyHostToDevice, s));
+  SpmvPlan<T> P = plan_build<T>(M.rp, M.rows, tmp, s);
+  launch_spmv<T, 1, SumOp>(M, P, GatherVec<T>{dx}, EpiStore<T>{dy}, s);
+  CK(cudaMemcpyAsync(y, dy, sizeof(T) * M.rows, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  plan_free(P);
+  dfree(M.val);
+  dfree(M.ci);
+  dfree(M.rp);
+  dfree(dx);
+  dfree(dy);
+  if (tmp.ptr) dfree(tmp.ptr);
+  tmp.ptr = nullptr;
+  CK(cudaStreamSynchronize(s));
+  cudaStreamDestroy(s);
+}
+
+}  // namespace qpcg_b200

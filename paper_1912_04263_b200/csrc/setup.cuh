@@ -93,7 +93,7 @@ __device__ __forceinline__ void val_report(unsigned long long* key, uint32_t cat
 // j-th entry, 2j+2 = ordering of j-th entry
 // (off: global index of element 0 — a row block of A reports global rows, so
 // the minimum over blocks is the unsharded first error)
-__global__ void validate_csr_rows_kernel(const uint32_t* rp, const uint32_t* ci, uint32_t rows,
+static __global__ void validate_csr_rows_kernel(const uint32_t* rp, const uint32_t* ci, uint32_t rows,
                                          uint32_t cols, uint32_t cat, int check_upper,
                                          unsigned long long* key, uint32_t off = 0) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
@@ -171,7 +171,7 @@ struct TransposeMap {
   uint32_t* perm = nullptr;  // [nnz] output position -> source entry index
 };
 
-__global__ void count_cols_kernel(const uint32_t* ci, uint32_t nnz, uint32_t* cnt) {
+static __global__ void count_cols_kernel(const uint32_t* ci, uint32_t nnz, uint32_t* cnt) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += gridDim.x * blockDim.x)
     atomicAdd(cnt + ci[k], 1u);
 }
@@ -379,11 +379,11 @@ __global__ void __launch_bounds__(256) ordered_mean_kernel(const T* __restrict__
 }
 
 // rows of a CSR structure with at least one stored entry, in increasing order
-__global__ void nonempty_flags_kernel(const uint32_t* rp, uint32_t rows, uint32_t* flags) {
+static __global__ void nonempty_flags_kernel(const uint32_t* rp, uint32_t rows, uint32_t* flags) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
     flags[r] = rp[r + 1] > rp[r];
 }
-__global__ void compact_kernel(const uint32_t* flags, const uint32_t* pos, uint32_t rows,
+static __global__ void compact_kernel(const uint32_t* flags, const uint32_t* pos, uint32_t rows,
                                uint32_t* list) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
     if (flags[r]) list[pos[r]] = r;

@@ -26,7 +26,7 @@
 namespace qpcg_b200 {
 
 template <typename T>
-class Sharded {
+class Sharded : public IEngine<T> {
  public:
   ShardComm comm;
   std::vector<std::unique_ptr<Workspace<T>>> sh;
@@ -89,7 +89,7 @@ class Sharded {
 
   // ------------------------------------------------------------- setup
   void setup(const HostCsr<T>& Pu, const T* q, const HostCsr<T>& A, const T* l, const T* u,
-             const qpcg_settings& st, const qpcg_options& op) {
+             const qpcg_settings& st, const qpcg_options& op) override {
     const double w0s = now_s();
     const uint64_t l0 = g_launches;
     opt = op;
@@ -322,7 +322,7 @@ class Sharded {
   }
 
   // ------------------------------------------------------------ solve
-  void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) {
+  void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) override {
     CK(cudaSetDevice(device));
     AllocScope scope(s);
     const double w0s = now_s();
@@ -407,8 +407,32 @@ class Sharded {
     w0().download(dst, full_m, sizeof(T) * m);
   }
 
+  // ------------------------- diagnostics / debug: the first row block
+  uint32_t pcg_calls(qpcg_pcg_call* out, uint32_t cap) override { return w0().pcg_calls(out, cap); }
+  uint32_t rho_updates(qpcg_rho_update* out, uint32_t cap) override {
+    return w0().rho_updates(out, cap);
+  }
+  uint32_t check_iterations(uint32_t* out, uint32_t cap) override {
+    return w0().check_iterations(out, cap);
+  }
+  void dims(uint64_t* d) override {
+    w0().dims(d);
+    d[1] = m;  // global m; nnz(A) of every block summed
+    uint64_t nnz = 0;
+    each([&](Workspace<T>& w) { nnz += w.D.A.nnz; });
+    d[3] = nnz;
+  }
+  void debug_scaled(T*, uint32_t*, uint32_t*, T*, T*, T*, uint32_t*, uint32_t*, T*, T*, T*, T*,
+                    double*) override {
+    throw InvalidArgument("debug_scaled: not available on a row-sharded workspace");
+  }
+  void debug_operator(const T*, T*, T*) override {
+    throw InvalidArgument("debug_operator: not available on a row-sharded workspace");
+  }
+  void bench_kernels(uint32_t reps, double* out) override { w0().bench_kernels(reps, out); }
+
   // --------------------------------------------------- OSQP-style updates
-  void warm_start(const T* x, const T* z, const T* y) {
+  void warm_start(const T* x, const T* z, const T* y) override {
     CK(cudaSetDevice(device));
     AllocScope scope(s);
     std::vector<unsigned long long> keys;
@@ -416,10 +440,10 @@ class Sharded {
     if (agree_min(keys) != ~0ull) throw InvalidArgument("solve: warm start must be finite");
     each([](Workspace<T>& w) { w.warm_apply(); });
   }
-  void update_rho(T rho) {
+  void update_rho(T rho) override {
     each([&](Workspace<T>& w) { w.update_rho(rho); });
   }
-  void update_vectors(const T* q, const T* l, const T* u) {
+  void update_vectors(const T* q, const T* l, const T* u) override {
     CK(cudaSetDevice(device));
     AllocScope scope(s);
     std::vector<unsigned long long> keys;

@@ -280,7 +280,7 @@ void launch_spmv(const DevCsr<T>& M, const SpmvPlan<T>& P, const Gather& g, cons
 }
 
 // ------------------------------------------------------------ plan build
-__global__ void plan_classify_kernel(const uint32_t* __restrict__ rp, uint32_t rows,
+static __global__ void plan_classify_kernel(const uint32_t* __restrict__ rp, uint32_t rows,
                                      uint32_t* is_short, uint32_t* nch, uint32_t* is_multi,
                                      uint32_t* multi_nch) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
@@ -294,7 +294,7 @@ __global__ void plan_classify_kernel(const uint32_t* __restrict__ rp, uint32_t r
   }
 }
 
-__global__ void plan_emit_kernel(const uint32_t* __restrict__ rp, uint32_t rows,
+static __global__ void plan_emit_kernel(const uint32_t* __restrict__ rp, uint32_t rows,
                                  const uint32_t* is_short, const uint32_t* short_pos,
                                  const uint32_t* nch, const uint32_t* item_off,
                                  const uint32_t* lr_idx, const uint32_t* pbase,
@@ -325,12 +325,12 @@ __global__ void plan_emit_kernel(const uint32_t* __restrict__ rp, uint32_t rows,
   }
 }
 
-__global__ void iota_kernel(uint32_t* out, uint32_t n) {
+static __global__ void iota_kernel(uint32_t* out, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = i;
 }
 
-__global__ void plan_gather_items_kernel(const WorkItem* in, const uint32_t* order, uint32_t n,
+static __global__ void plan_gather_items_kernel(const WorkItem* in, const uint32_t* order, uint32_t n,
                                          WorkItem* out) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = in[order[i]];
@@ -399,14 +399,14 @@ void plan_free(SpmvPlan<T>& P) {
   P = SpmvPlan<T>{};
 }
 
-__global__ void chunk_count_kernel(const WorkItem* items, uint32_t n, uint32_t* nch) {
+static __global__ void chunk_count_kernel(const WorkItem* items, uint32_t n, uint32_t* nch) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     nch[i] = ceil_div(items[i].end - items[i].beg, 32u);
 }
 
 // warp per item: classify every 32-entry chunk, write offsets / wide columns.
 // fill == 0 only counts the wide chunks (sizing pass).
-__global__ void compress_kernel(const uint32_t* __restrict__ ci, const WorkItem* items, uint32_t n,
+static __global__ void compress_kernel(const uint32_t* __restrict__ ci, const WorkItem* items, uint32_t n,
                                 const uint32_t* c0, uint16_t* off16, uint32_t* cbase,
                                 uint32_t* wide, uint32_t* n_wide, int fill) {
   const uint32_t lane = threadIdx.x & 31;
