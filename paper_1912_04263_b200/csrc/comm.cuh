@@ -18,6 +18,7 @@
 #include <dlfcn.h>
 #include <nccl.h>  // types and enums only: every symbol is resolved through dlopen
 
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -120,17 +121,32 @@ struct ShardComm {
   int global_count() const { return local * nranks; }
   int global_index(int l) const { return rank * local + l; }
 
+  // Communicators are cached per (unique id, rank, ranks, device) for the life
+  // of the process: creating one costs a rendezvous of every rank (tens to
+  // hundreds of ms), and a solve loop (bench steps, receding-horizon MPC)
+  // sets up workspace after workspace on the same group.
   void init_nccl(const void* id, int r, int nr) {
     NcclApi& api = nccl_api();
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     rank = r;
     nranks = nr;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::string key(reinterpret_cast<const char*>(&uid), sizeof(uid));
+    key += ":" + std::to_string(r) + ":" + std::to_string(nr) + ":" + std::to_string(dev);
+    static std::mutex mu;
+    static std::map<std::string, ncclComm_t> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      comm = it->second;
+      return;
+    }
     nccl_check(api.CommInitRank(&comm, nr, uid, r), "ncclCommInitRank");
+    cache.emplace(key, comm);
   }
-  ~ShardComm() {
-    if (comm) nccl_api().CommDestroy(comm);
-  }
+  ~ShardComm() {}  // the cached communicator outlives the workspace
 
   // in-place allreduce of `count` elements held in one buffer per local shard
   template <typename T>
