@@ -153,11 +153,13 @@ typedef struct {
 #define QPCG_MODE_GRAPH 0 /* device-resident control flow: CUDA graph with
                              conditional while/if nodes (default) */
 #define QPCG_MODE_EAGER 1 /* host-driven loop with a sync per decision (debug) */
-#define QPCG_MODE_PERSISTENT 2 /* the whole loop in one kernel: one thread-block
-                                  cluster (hardware barriers) while nnz(A) +
-                                  nnz(P) <= 15e3 (env QPCG_CLUSTER_MAX_NNZ),
-                                  else a cooperative grid.  GRAPH picks it by
-                                  itself while nnz(A) + nnz(P) <= 2e6 (env
+#define QPCG_MODE_PERSISTENT 2 /* the whole loop in one kernel: one block (its
+                                  L1 holding the matrices) while nnz(A) +
+                                  nnz(P) <= 1200 (env QPCG_BLOCK_MAX_NNZ), one
+                                  thread-block cluster (hardware barriers)
+                                  while <= 1e4 (QPCG_CLUSTER_MAX_NNZ), else a
+                                  cooperative grid.  GRAPH picks it by itself
+                                  while nnz(A) + nnz(P) <= 2e6 (env
                                   QPCG_PERSIST_MAX_NNZ).  All modes give
                                   bitwise-identical results. */
 

@@ -41,13 +41,30 @@ constexpr uint32_t kMaxVirtual = 2 * kNumSMs;  // red_grid() never exceeds kRedB
 // The barrier between phases: the whole grid (cooperative launch, one or two
 // blocks per SM) or one thread-block cluster (up to 16 SMs, hardware barrier:
 // the tiny-problem variant, where barrier latency is the whole cost).
+// rank() / count(): this block among the blocks solving the instance.
+// kL1: the matrices are read through the L1 (one SM holds the whole instance,
+// so after the first pass they are served on-chip; the grid variants stream
+// them past L1 like the stand-alone kernels).
 struct GridSync {
   cgp::grid_group g;
+  static constexpr bool kL1 = false;
   __device__ GridSync() : g(cgp::this_grid()) {}
   __device__ __forceinline__ void sync() { g.sync(); }
+  __device__ __forceinline__ uint32_t rank() const { return blockIdx.x; }
+  __device__ __forceinline__ uint32_t count() const { return gridDim.x; }
 };
 struct ClusterSync {
+  static constexpr bool kL1 = false;
   __device__ __forceinline__ void sync() { cgp::this_cluster().sync(); }
+  __device__ __forceinline__ uint32_t rank() const { return blockIdx.x; }
+  __device__ __forceinline__ uint32_t count() const { return gridDim.x; }
+};
+// one block = one instance: __syncthreads barriers, L1-resident matrices
+struct BlockSync {
+  static constexpr bool kL1 = true;
+  __device__ __forceinline__ void sync() { __syncthreads(); }
+  __device__ __forceinline__ uint32_t rank() const { return 0u; }
+  __device__ __forceinline__ uint32_t count() const { return 1u; }
 };
 
 // Reduction with the stand-alone kernels' geometry: virtual block vb of
@@ -57,7 +74,7 @@ __device__ __forceinline__ void preduce(F&& elems, uint32_t len, uint32_t max_ma
                                         Sync& grid, T (&tot)[NQ]) {
   __shared__ T sm[33];
   const uint32_t Gv = red_grid<T>(len);
-  for (uint32_t vb = blockIdx.x; vb < Gv; vb += gridDim.x) {
+  for (uint32_t vb = grid.rank(); vb < Gv; vb += grid.count()) {
     T v[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) v[q] = T(0);
@@ -85,21 +102,21 @@ __device__ __forceinline__ void preduce(F&& elems, uint32_t len, uint32_t max_ma
 // One SpMV pass over the plan with the whole grid (warps stride the items,
 // threads stride the short rows); same per-item / per-row arithmetic as
 // spmv_kernel.
-template <typename T, int NCOL, class Op, class Gather, class Epi>
-__device__ __forceinline__ void spmv_phase(const DevCsr<T>& M, const SpmvPlan<T>& P, Gather gather,
-                                           Epi epi) {
+template <typename T, int NCOL, class Op, class Gather, class Epi, class Sync>
+__device__ __forceinline__ void spmv_phase(const Sync& sy, const DevCsr<T>& M,
+                                           const SpmvPlan<T>& P, Gather gather, Epi epi) {
   if (!epi.init()) return;
   gather.init();
-  const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  const uint32_t t0 = sy.rank() * blockDim.x + threadIdx.x, stride = sy.count() * blockDim.x;
   const uint32_t lane = threadIdx.x & 31;
   for (uint32_t it = t0 >> 5; it < P.n_items; it += stride >> 5) {
     if (P.off16 != nullptr)
-      spmv_item<T, NCOL, Op, Gather, Epi, 8, true>(M, P, gather, epi, it, lane);
+      spmv_item<T, NCOL, Op, Gather, Epi, 8, true, Sync::kL1>(M, P, gather, epi, it, lane);
     else
-      spmv_item<T, NCOL, Op, Gather, Epi, 4, false>(M, P, gather, epi, it, lane);
+      spmv_item<T, NCOL, Op, Gather, Epi, 4, false, Sync::kL1>(M, P, gather, epi, it, lane);
   }
   for (uint32_t idx = t0; idx < P.n_short; idx += stride)
-    spmv_short<T, NCOL, Op, Gather, Epi>(M, P, gather, epi, idx);
+    spmv_short<T, NCOL, Op, Gather, Epi, Sync::kL1>(M, P, gather, epi, idx);
 }
 
 template <typename T, class Sync>
@@ -112,8 +129,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
   D.ctl = &sctl;
   Ctl<T>* C = &sctl;
   const Handles H{};
-  const bool rec = blockIdx.x == 0;  // the one writer of diagnostics records
-  const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  const bool rec = grid.rank() == 0;  // the one writer of diagnostics records
+  const uint32_t t0 = grid.rank() * blockDim.x + threadIdx.x, stride = grid.count() * blockDim.x;
   uint32_t pp = 0;
   auto part = [&]() { return B.part + (pp++ & 1u) * (kMaxQ * kMaxVirtual); };
   const uint32_t nm = D.n > D.m ? D.n : D.m;
@@ -122,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
     // ---- rhs + r0 (solver.hpp:351-355, linsys.hpp:218-219)
     if (!C->error) pack_rhs_elems(D, t0, stride);
     grid.sync();
-    spmv_phase<T, 2, SumOp>(D.AT, D.pAT, GatherRhs<T, false>{D.g2m}, EpiRhs<T>{D, T(0)});
+    spmv_phase<T, 2, SumOp>(grid, D.AT, D.pAT, GatherRhs<T, false>{D.g2m}, EpiRhs<T>{D, T(0)});
     grid.sync();
     if (!C->error) {  // k_pcg_init
       T tot[4];
@@ -133,9 +150,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
     }
     // ---- PCG iterations
     while (C->pcg_active && !C->error) {
-      spmv_phase<T, 1, SumOp>(D.A, D.pA, GatherVec<T, false>{D.p}, EpiAp<T>{D.t, C, T(0)});
+      spmv_phase<T, 1, SumOp>(grid, D.A, D.pA, GatherVec<T, false>{D.p}, EpiAp<T>{D.t, C, T(0)});
       grid.sync();
-      spmv_phase<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T, false>{D.t}, EpiKp<T>{D, T(0)});
+      spmv_phase<T, 1, SumOp>(grid, D.AT, D.pAT, GatherVec<T, false>{D.t}, EpiKp<T>{D, T(0)});
       grid.sync();
       {
         T tot[1];
@@ -162,9 +179,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
       __syncthreads();
     }
     grid.sync();
-    spmv_phase<T, 2, SumOp>(D.A, D.pA, GatherAdmm<T, false>{D.g2n},
+    spmv_phase<T, 2, SumOp>(grid, D.A, D.pA, GatherAdmm<T, false>{D.g2n},
                             EpiAdmm<T, 2>{D, T(0), T(0), T(0), false});
-    spmv_phase<T, 1, SumOp>(D.A, D.pA, GatherVec<T, false>{D.xt},
+    spmv_phase<T, 1, SumOp>(grid, D.A, D.pA, GatherVec<T, false>{D.xt},
                             EpiAdmm<T, 1>{D, T(0), T(0), T(0), false});
     grid.sync();
     if (!C->error) {
@@ -176,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
     grid.sync();
     // ---- termination check (solver.hpp:458-496)
     if (C->is_check && !C->error) {
-      spmv_phase<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T, false>{D.y}, EpiDual<T>{D});
+      spmv_phase<T, 1, SumOp>(grid, D.AT, D.pAT, GatherVec<T, false>{D.y}, EpiDual<T>{D});
       grid.sync();
       {
         T tot[14];
@@ -187,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
       }
       if (C->inf_branch) {
         // atomic slots of the certificate passes live in the global block
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (grid.rank() == 0 && threadIdx.x == 0) {
           B.gctl->atv_inf_bits = 0ull;
           B.gctl->pv_inf_bits = 0ull;
           B.gctl->dinf_bad = 0u;
@@ -199,9 +216,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
           if (threadIdx.x == 0) infeas_vec_decide(C, tot);
           __syncthreads();
         }
-        spmv_phase<T, 1, SumOp>(D.ATo, D.pATo, GatherCertY<T, false>{D.e, D.dy, C, T(0), T(0)},
+        spmv_phase<T, 1, SumOp>(grid, D.ATo, D.pATo, GatherCertY<T, false>{D.e, D.dy, C, T(0), T(0)},
                                 EpiNormMax<T>{&B.gctl->atv_inf_bits, &C->need_pinf});
-        spmv_phase<T, 1, SumOp>(D.Po, D.pPo, GatherCertX<T, false>{D.d, D.dx, C, T(0)},
+        spmv_phase<T, 1, SumOp>(grid, D.Po, D.pPo, GatherCertX<T, false>{D.d, D.dx, C, T(0)},
                                 EpiNormMax<T>{&B.gctl->pv_inf_bits, &C->need_dinf});
         grid.sync();
         if (threadIdx.x == 0) {
@@ -210,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
           infeas_mid_decide(C);
         }
         __syncthreads();
-        spmv_phase<T, 1, SumOp>(
+        spmv_phase<T, 1, SumOp>(grid, 
             D.Ao, D.pAo, GatherCertX<T, false>{D.d, D.dx, C, T(0)},
             EpiDualRows<T>{D.l_o, D.u_o, &B.gctl->dinf_bad, &C->need_dinf, T(0), C});
         grid.sync();
@@ -234,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
       grid.sync();
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (grid.rank() == 0 && threadIdx.x == 0) {
     C->admm_continue = 0;
     *Dg.ctl = sctl;
   }

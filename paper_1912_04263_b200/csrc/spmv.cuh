@@ -121,7 +121,15 @@ __device__ __forceinline__ uint16_t ld_stream(const uint16_t* p) {
 // One warp, one work item: lanes stride the item 32 entries at a time
 // (coalesced), U strides in flight; the last < 32U entries in one predicated
 // step.  CMP: columns from the compressed index (SpmvPlan::off16).
-template <typename T, int NCOL, class Op, class Gather, int U, bool CMP>
+// L1: read the matrix through the L1 (the one-SM persistent variant, whose
+// whole instance stays on-chip); otherwise stream it past L1.
+template <bool L1, typename V>
+__device__ __forceinline__ V ld_mat(const V* p) {
+  if constexpr (L1) return __ldg(p);
+  else return ld_stream(p);
+}
+
+template <typename T, int NCOL, class Op, class Gather, int U, bool CMP, bool L1 = false>
 __device__ __forceinline__ void item_loop(const DevCsr<T>& M, const SpmvPlan<T>& P,
                                           const Gather& gather, const WorkItem& item, uint32_t c0,
                                           uint32_t lane, T (&acc)[NCOL]) {
@@ -134,10 +142,10 @@ __device__ __forceinline__ void item_loop(const DevCsr<T>& M, const SpmvPlan<T>&
   auto load_col = [&](uint32_t kk, uint32_t bl, int u, bool ok, uint32_t& c, uint16_t& o,
                       uint32_t& b) {
     if (!CMP) {
-      c = ok ? ld_stream(ci + kk) : 0u;
+      c = ok ? ld_mat<L1>(ci + kk) : 0u;
     } else {
       b = __shfl_sync(0xffffffffu, bl, u);
-      o = ok ? ld_stream(P.off16 + kk) : (uint16_t)0;
+      o = ok ? ld_mat<L1>(P.off16 + kk) : (uint16_t)0;
     }
   };
   auto col_of = [&](uint32_t c, uint16_t o, uint32_t b) -> uint32_t {
@@ -151,7 +159,7 @@ __device__ __forceinline__ void item_loop(const DevCsr<T>& M, const SpmvPlan<T>&
     const uint32_t bl = (CMP && lane < (uint32_t)U) ? __ldg(P.cbase + ch + lane) : 0u;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      v[u] = ld_stream(val + k + 32u * u);
+      v[u] = ld_mat<L1>(val + k + 32u * u);
       if (Op::kNeedsGather) load_col(k + 32u * u, bl, u, true, c[u], o[u], b[u]);
     }
 #pragma unroll
@@ -172,7 +180,7 @@ __device__ __forceinline__ void item_loop(const DevCsr<T>& M, const SpmvPlan<T>&
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool ok = k + 32u * u < end;
-      v[u] = ok ? ld_stream(val + k + 32u * u) : T(0);
+      v[u] = ok ? ld_mat<L1>(val + k + 32u * u) : T(0);
       if (Op::kNeedsGather) load_col(k + 32u * u, bl, u, ok, c[u], o[u], b[u]);
     }
 #pragma unroll
@@ -191,7 +199,8 @@ __device__ __forceinline__ void item_loop(const DevCsr<T>& M, const SpmvPlan<T>&
 // One work item (one warp; lane 0 runs the epilogue).  Multi-item rows
 // publish a partial; the last item to arrive combines them in item order
 // (deterministic).
-template <typename T, int NCOL, class Op, class Gather, class Epi, int U, bool CMP>
+template <typename T, int NCOL, class Op, class Gather, class Epi, int U, bool CMP,
+          bool L1 = false>
 __device__ __forceinline__ void spmv_item(const DevCsr<T>& M, const SpmvPlan<T>& P,
                                           const Gather& gather, const Epi& epi, uint32_t it,
                                           uint32_t lane) {
@@ -199,8 +208,8 @@ __device__ __forceinline__ void spmv_item(const DevCsr<T>& M, const SpmvPlan<T>&
   T acc[NCOL];
 #pragma unroll
   for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
-  item_loop<T, NCOL, Op, Gather, U, CMP && Op::kNeedsGather>(M, P, gather, item,
-                                                              CMP ? P.c0[it] : 0u, lane, acc);
+  item_loop<T, NCOL, Op, Gather, U, CMP && Op::kNeedsGather, L1>(M, P, gather, item,
+                                                                  CMP ? P.c0[it] : 0u, lane, acc);
 #pragma unroll
   for (int j = 0; j < NCOL; ++j) acc[j] = Op::warp(acc[j]);
   if (lane != 0) return;
@@ -230,7 +239,7 @@ __device__ __forceinline__ void spmv_item(const DevCsr<T>& M, const SpmvPlan<T>&
 }
 
 // One short row (<= kShortRowMax nnz), one thread, left to right: bit-exact.
-template <typename T, int NCOL, class Op, class Gather, class Epi>
+template <typename T, int NCOL, class Op, class Gather, class Epi, bool L1 = false>
 __device__ __forceinline__ void spmv_short(const DevCsr<T>& M, const SpmvPlan<T>& P,
                                            const Gather& gather, const Epi& epi, uint32_t idx) {
   const uint32_t r = P.short_rows[idx];
@@ -239,9 +248,9 @@ __device__ __forceinline__ void spmv_short(const DevCsr<T>& M, const SpmvPlan<T>
 #pragma unroll
   for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
   for (uint32_t k = b; k < e; ++k) {
-    const T v = ld_stream(M.val + k);
+    const T v = ld_mat<L1>(M.val + k);
     T g[NCOL];
-    if (Op::kNeedsGather) gather(ld_stream(M.ci + k), g);
+    if (Op::kNeedsGather) gather(ld_mat<L1>(M.ci + k), g);
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) Op::acc(acc[j], v, Op::kNeedsGather ? g[j] : T(0));
   }

@@ -798,9 +798,13 @@ class Workspace : public IEngine<T> {
     if (opt.mode == QPCG_MODE_PERSISTENT) return true;
     return opt.mode == QPCG_MODE_GRAPH && uint64_t(D.A.nnz) + D.P.nnz <= persist_max_nnz();
   }
+  static uint64_t block_max_nnz() {
+    const char* e = std::getenv("QPCG_BLOCK_MAX_NNZ");
+    return e ? std::strtoull(e, nullptr, 10) : 1200ull;
+  }
   static uint64_t cluster_max_nnz() {
     const char* e = std::getenv("QPCG_CLUSTER_MAX_NNZ");
-    return e ? std::strtoull(e, nullptr, 10) : 15000ull;
+    return e ? std::strtoull(e, nullptr, 10) : 10000ull;
   }
   void run_persistent() {
     if (!persist_part) persist_part = alloc<T>(2 * kMaxQ * kMaxVirtual);
@@ -831,6 +835,12 @@ class Workspace : public IEngine<T> {
         }
       }
       cudaGetLastError();
+    }
+    if (work <= block_max_nnz()) {
+      // tiny problem: one block, __syncthreads barriers, matrices held in its L1
+      k_admm_persistent<T, BlockSync><<<1, kThreads, 0, s>>>(D, B);
+      CK_LAUNCH();
+      return;
     }
     if (cluster > 0 && work <= cluster_max_nnz()) {
       // tiny problem: one cluster, hardware barriers
