@@ -129,12 +129,19 @@ def test_cadence_matches_reference():
     assert [c["iterations"] for c in dg.pcg_calls[:k]] == [c["iterations"] for c in do.pcg_calls[:k]]
 
 
-def test_config2_full_size_against_reference_run():
-    """BASELINE config 2 at full size (1.5e8 nnz) against the reference's own
-    completed solve of the identical instance (tests/golden/config2_reference_solve.json,
-    produced by scripts/ref_solve_config.py: 330 s on one CPU core)."""
-    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "config2_reference_solve.json")))
-    p = G.config("2")
+GOLD_CONFIGS = sorted(f[len("config"):-len("_reference_solve.json")]
+                      for f in os.listdir(os.path.join(os.path.dirname(__file__), "golden"))
+                      if f.startswith("config") and f.endswith("_reference_solve.json"))
+
+
+@pytest.mark.parametrize("cfg", GOLD_CONFIGS)
+def test_full_size_config_against_reference_run(cfg):
+    """BASELINE configs at full size (1.4e8-1.5e8 nnz) against the reference's own
+    completed solve of the identical instance (tests/golden/config*_reference_solve.json,
+    produced by scripts/ref_solve_config.py: 5-6 minutes on one CPU core each)."""
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                      f"config{cfg}_reference_solve.json")))
+    p = G.config(cfg)
     s = Settings(lambda_pcg=ref["lambda_pcg"])
     g = solver.solve(p, s, device=0)
     assert g.status == ref["status"] == "solved"
@@ -142,3 +149,4 @@ def test_config2_full_size_against_reference_run():
     assert rel(g.objective, ref["objective"]) < 1e-6
     xs = g.x[::ref["x_sample_stride"]]
     assert np.max(np.abs(xs - np.array(ref["x_sample"]))) <= 1e-4 * max(1.0, ref["x_inf"])
+    assert kkt_ok(p, g, s)
