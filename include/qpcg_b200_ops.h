@@ -22,6 +22,21 @@ extern "C" {
 int qpcg_f64_op_spmv(const qpcg_csr_f64* m, const double* x, double* y, int device);
 int qpcg_f32_op_spmv(const qpcg_csr_f32* m, const float* x, float* y, int device);
 
+/* pcg_solve (linsys.hpp:190-276) on the ReducedKktOperator built from
+ * (p_full, a, a_t, sigma, rho) (linsys.hpp:39-61; a_t must equal
+ * transpose_csr(a) bit for bit) with its Jacobi preconditioner
+ * (linsys.hpp:137-148), run by the engine's own PCG kernels.  x[n] receives
+ * the solution; res[0..2] = iterations, final residual norm (the best one on
+ * an iteration-cap exit), converged (0/1).  QPCG_ERR_NOT_PD on a direction
+ * of nonpositive curvature; QPCG_ERR_INVALID on the reference's argument
+ * errors (eps <= 0, dimensions, non-finite warm start, a_t mismatch). */
+int qpcg_f64_op_pcg(const qpcg_csr_f64* p_full, const qpcg_csr_f64* a, const qpcg_csr_f64* a_t,
+                    double sigma, double rho, const double* b, const double* warm, double eps,
+                    uint32_t max_iter, double* x, double* res, int device);
+int qpcg_f32_op_pcg(const qpcg_csr_f32* p_full, const qpcg_csr_f32* a, const qpcg_csr_f32* a_t,
+                    double sigma, double rho, const float* b, const float* warm, double eps,
+                    uint32_t max_iter, float* x, double* res, int device);
+
 /* dims[0..5] = n, m, nnz(P full), nnz(A), equil passes, 0 */
 int qpcg_debug_dims(const qpcg_workspace* ws, uint64_t* dims);
 

@@ -307,4 +307,21 @@ int qpcg_f32_op_spmv(const qpcg_csr_f32* m, const float* x, float* y, int device
   return op_spmv_impl<float>(m, x, y, device);
 }
 
+int qpcg_f64_op_pcg(const qpcg_csr_f64* p_full, const qpcg_csr_f64* a, const qpcg_csr_f64* a_t,
+                    double sigma, double rho, const double* b, const double* warm, double eps,
+                    uint32_t max_iter, double* x, double* res, int device) {
+  return guarded(nullptr, [&] {
+    op_pcg<double>(host_csr<double>(p_full), host_csr<double>(a), host_csr<double>(a_t), sigma, rho,
+                   b, warm, eps, max_iter, x, res, device);
+  });
+}
+int qpcg_f32_op_pcg(const qpcg_csr_f32* p_full, const qpcg_csr_f32* a, const qpcg_csr_f32* a_t,
+                    double sigma, double rho, const float* b, const float* warm, double eps,
+                    uint32_t max_iter, float* x, double* res, int device) {
+  return guarded(nullptr, [&] {
+    op_pcg<float>(host_csr<float>(p_full), host_csr<float>(a), host_csr<float>(a_t), float(sigma),
+                  float(rho), b, warm, float(eps), max_iter, x, res, device);
+  });
+}
+
 }  // extern "C"

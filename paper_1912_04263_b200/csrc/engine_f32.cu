@@ -57,4 +57,13 @@ void op_spmv<float>(const HostCsr<float>& mv, const float* x, float* y, int devi
   cudaStreamDestroy(s);
 }
 
+template <>
+void op_pcg<float>(const HostCsr<float>& pf, const HostCsr<float>& a, const HostCsr<float>& at, float sigma,
+                float rho, const float* b, const float* warm, float eps, uint32_t max_iter, float* x,
+                double* res, int device) {
+  Workspace<float> w;
+  w.setup_operator(pf, a, at, sigma, rho, device);
+  w.op_pcg(b, warm, eps, max_iter, x, res);
+}
+
 }  // namespace qpcg_b200

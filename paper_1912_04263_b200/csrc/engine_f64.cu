@@ -57,4 +57,13 @@ void op_spmv<double>(const HostCsr<double>& mv, const double* x, double* y, int 
   cudaStreamDestroy(s);
 }
 
+template <>
+void op_pcg<double>(const HostCsr<double>& pf, const HostCsr<double>& a, const HostCsr<double>& at, double sigma,
+                double rho, const double* b, const double* warm, double eps, uint32_t max_iter, double* x,
+                double* res, int device) {
+  Workspace<double> w;
+  w.setup_operator(pf, a, at, sigma, rho, device);
+  w.op_pcg(b, warm, eps, max_iter, x, res);
+}
+
 }  // namespace qpcg_b200

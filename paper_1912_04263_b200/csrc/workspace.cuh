@@ -124,6 +124,10 @@ template <typename T>
 void validate_settings_in(const qpcg_settings& s);  // engine_fXX.cu (settings.hpp:44-75 in T)
 template <typename T>
 void op_spmv(const HostCsr<T>& m, const T* x, T* y, int device);  // engine_fXX.cu
+template <typename T>
+void op_pcg(const HostCsr<T>& pf, const HostCsr<T>& a, const HostCsr<T>& at, T sigma, T rho,
+            const T* b, const T* warm, T eps, uint32_t max_iter, T* x, double* res,
+            int device);  // engine_fXX.cu
 
 // =====================================================================
 template <typename T>
@@ -1172,6 +1176,159 @@ class Workspace : public IEngine<T> {
     out[6] = fa + S * n + S * m;
     out[7] = fat + mb(D.P) + S * m + 2 * S * n;
     out[8] = fa + fat + mb(D.P) + S * (2 * m + 11 * n);
+  }
+
+  // ------------------------------------- operator-level PCG (ops C-ABI)
+  // ReducedKktOperator (linsys.hpp:39-61) + Jacobi (:137-148) on caller
+  // matrices (P full, A, A^T), then pcg_solve (linsys.hpp:190-276) run by the
+  // same kernels as the ADMM loop (k_pcg_init / the two SpMV passes /
+  // k_pcg_dot / k_pcg_update / k_pcg_pupdate / k_pcg_fin).
+  void setup_operator(const HostCsr<T>& Pf, const HostCsr<T>& A, const HostCsr<T>& AT, T sigma,
+                      T rho, int dev) {
+    if (!(sigma > T(0)) || !(rho > T(0)))
+      throw InvalidArgument("kkt operator: sigma and rho must be positive");
+    if (Pf.rows != Pf.cols || A.cols != Pf.cols || AT.rows != A.cols || AT.cols != A.rows)
+      throw InvalidArgument("kkt operator: dimension mismatch");
+    qpcg_settings st;
+    std::memset(&st, 0, sizeof(st));
+    st.alpha = 1.6;
+    st.sigma = double(sigma);
+    st.rho_bar_init = double(rho);
+    st.eps_abs = st.eps_rel = 1e-3;
+    st.eps_pinf = st.eps_dinf = 1e-4;
+    st.max_admm_iter = st.check_interval = st.rho_update_interval = 1;
+    st.lambda_pcg = 0.15;
+    st.eps_pcg_min = 1e-7;
+    st.eps_equil = 1e-3;
+    st.equil_max_passes = 1;
+    qpcg_options op;
+    std::memset(&op, 0, sizeof(op));
+    op.device = dev;
+    op.input_memory = QPCG_MEM_HOST;
+    op.mode = QPCG_MODE_EAGER;
+    begin(st, op, nullptr);
+    AllocScope scope(s);
+    const uint32_t n = Pf.rows, m = A.rows;
+    D.n = n;
+    D.m = m;
+    auto up = [&](const HostCsr<T>& H) {
+      DevCsr<T> M{H.rows, H.cols, H.nnz, alloc<T>(H.nnz), alloc<uint32_t>(size_t(H.rows) + 1),
+                  alloc<uint32_t>(H.nnz)};
+      upload(M.val, H.values, sizeof(T) * H.nnz);
+      upload(M.rp, H.row_ptr, 4 * (size_t(H.rows) + 1));
+      upload(M.ci, H.col_indices, 4 * size_t(H.nnz));
+      return M;
+    };
+    D.P = up(Pf);
+    D.A = up(A);
+    D.AT = up(AT);
+    D.pP = plan_build<T>(D.P.rp, n, tmp, s);
+    D.pA = plan_build<T>(D.A.rp, m, tmp, s);
+    D.pAT = plan_build<T>(D.AT.rp, n, tmp, s);
+    // linsys.hpp:54-58: a_t must be transpose_csr(a) bit for bit
+    {
+      uint32_t* row_of = alloc<uint32_t>(A.nnz);
+      plan_visit(D.A, D.pA, RowOfFn{row_of}, s);
+      uint32_t* trp = alloc<uint32_t>(size_t(n) + 1);
+      uint32_t* tci = alloc<uint32_t>(A.nnz);
+      uint32_t* perm = alloc<uint32_t>(A.nnz);
+      transpose_structure(D.A.ci, row_of, n, A.nnz, trp, tci, perm, tmp, s);
+      uint32_t* bad = alloc<uint32_t>(1);
+      CK(cudaMemsetAsync(bad, 0, 4, s));
+      const uint32_t *atrp = D.AT.rp, *atci = D.AT.ci, *pm = perm;
+      const T *av = D.A.val, *atv = D.AT.val;
+      const uint32_t annz = A.nnz, AT_nnz = AT.nnz;
+      if (AT_nnz != annz) {
+        CK(cudaMemsetAsync(bad, 1, 1, s));
+      } else {
+        for_n(n + 1, [=] __device__(uint32_t i) { if (trp[i] != atrp[i]) *bad = 1u; }, s);
+        for_n(annz, [=] __device__(uint32_t i) {
+          // bitwise value comparison (the reference compares std::vector<T>)
+          if (tci[i] != atci[i] || !(av[pm[i]] == atv[i] || (av[pm[i]] != av[pm[i]] && atv[i] != atv[i])))
+            *bad = 1u;
+        }, s);
+      }
+      uint32_t hb = 0;
+      CK(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (hb) throw InvalidArgument("kkt operator: a_t is not the transpose of a");
+    }
+    if (compress_indices()) {
+      plan_compress(D.pA, D.A.ci, A.nnz, n, tmp, s);
+      plan_compress(D.pAT, D.AT.ci, AT.nnz, m, tmp, s);
+    }
+    D.ctl = alloc<Ctl<T>>(1);
+    D.red = alloc<T>(kRedBlocks * kMaxQ);
+    CK(cudaMemsetAsync(D.ctl, 0, sizeof(Ctl<T>), s));
+    D.diag_p = vec(n, false);
+    D.diag_ata = vec(n, false);
+    D.dinv = vec(n, false);
+    extract_diag_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.P, D.diag_p);
+    CK_LAUNCH();
+    diag_ata_kernel<T><<<grid_for(uint64_t(n) * 32), kThreads, 0, s>>>(D.AT, D.diag_ata, nullptr);
+    CK_LAUNCH();
+    D.x = vec(n); D.xt = vec(n); D.b = vec(n); D.r = vec(n); D.p = vec(n); D.kp = vec(n);
+    D.best = vec(n);
+    D.t = vec(m);
+    D.g2n = alloc<pair_t<T>>(n);
+    std::memset(&hc, 0, sizeof(hc));
+    hc.alpha = T(1.6);
+    hc.sigma = sigma;
+    hc.rho = rho;
+    hc.check_interval = 1;
+    push_ctl();
+    k_precond<T><<<grid_for(n), kThreads, 0, s>>>(D, 1);
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(s));
+  }
+
+  void op_pcg(const T* b, const T* warm, T eps, uint32_t max_iter, T* x, double* res) {
+    CK(cudaSetDevice(device));
+    AllocScope scope(s);
+    if (!(eps > T(0))) throw InvalidArgument("pcg: eps must be positive");
+    const uint32_t n = D.n;
+    upload(D.b, b, sizeof(T) * n);
+    upload(D.xt, warm, sizeof(T) * n);
+    pull_ctl();
+    hc.error = 0;
+    hc.done = 0;
+    hc.pcg_eps = eps;
+    hc.pcg_cap = max_iter;
+    hc.pcg_active = 1;  // enables the operator passes below
+    hc.iter = 0;
+    push_ctl();
+    // r0 = K x0 - b (linsys.hpp:219-220): the passes read p
+    CK(cudaMemcpyAsync(D.p, D.xt, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
+    launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
+    {
+      T *r = D.r, *kp = D.kp;
+      const T* bb = D.b;
+      for_n(n, [=] __device__(uint32_t i) { r[i] = kp[i] - bb[i]; }, s);
+    }
+    enq_pcg_init(Handles{});
+    pull_ctl();
+    if (hc.pcg_active && hc.pcg_cap == 0) {  // linsys.hpp:235-241 before any iteration
+      hc.pcg_active = 0;
+      hc.pcg_exit = kPcgCap;
+      push_ctl();
+    }
+    while (hc.pcg_active && !hc.error) {
+      enq_pcg_iter(Handles{});
+      pull_ctl();
+    }
+    if (hc.error == kErrNotPD)
+      throw NotPositiveDefinite("pcg: encountered direction of nonpositive curvature");
+    if (hc.error == kErrInvalid) throw InvalidArgument("pcg: warm start must be finite");
+    k_pcg_fin<T><<<grid_for(n), kThreads, 0, s>>>(D);
+    CK_LAUNCH();
+    download(x, D.xt, sizeof(T) * n);
+    CK(cudaStreamSynchronize(s));
+    pull_ctl();
+    const bool cap = hc.pcg_exit == kPcgCap, zero = hc.pcg_exit == kPcgZeroRhs;
+    res[0] = double(hc.k);
+    res[1] = zero ? 0.0 : double(cap ? hc.best_norm : hc.r_norm);
+    res[2] = cap ? 0.0 : 1.0;
   }
 
   // ---------------------------------------------------- diagnostics (C-ABI)
