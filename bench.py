@@ -240,7 +240,15 @@ class Engine:
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_baseline(problem, counts: dict, budget_reps: int = 1) -> dict:
+def full_reference_seconds(cfg: str, lam: float):
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ref_solve_config{cfg}_lam{lam:g}.json")) as f:
+            return float(json.load(f)["runtime_seconds"])
+    except Exception:
+        return None
+
+
+def cpu_baseline(problem, counts: dict, budget_reps: int = 1, cfg: str = "", lam: float = 0.0) -> dict:
     """The reference (oracle/_ref, unmodified headers, 1 core) on a bounded
     sample of the same instance; solve time extrapolated from its measured
     components and the solve's iteration counts."""
@@ -258,6 +266,7 @@ def cpu_baseline(problem, counts: dict, budget_reps: int = 1) -> dict:
         raise RuntimeError(lib.qref_last_error().decode())
     wall = time.time() - t0
     t_sym, t_trans, t_ruiz1, t_op, t_k, t_at, t_a, t_res = (float(v) for v in out[:8])
+    full = full_reference_seconds(cfg, lam) if cfg else None
     passes = int(counts.get("equil_passes", 10))
     iters = int(counts["iterations"])
     pcg = int(counts["pcg_iterations_total"])
@@ -270,14 +279,19 @@ def cpu_baseline(problem, counts: dict, budget_reps: int = 1) -> dict:
     # residuals (3 spmv) and, while unsolved, the A^T infeasibility spmv.
     pass_body = max(t_ruiz1 - 2.0 * t_trans, 0.0)
     setup = t_sym + t_trans + t_ruiz1 + (passes - 1) * pass_body + t_op
-    loop = iters * (t_at + t_k + t_a) + pcg * t_k + checks * (t_res + t_at)
+    # initial residuals; per unsolved check the residuals plus the two
+    # certificate products over the original matrices (A_o^T v, A_o v)
+    loop = t_res + iters * (t_at + t_k + t_a) + pcg * t_k + checks * (t_res + t_at + t_a)
     return {"value": setup + loop, "unit": "s", "cores": 1, "kind": "reference",
             "sample": (f"oracle/_ref (unmodified reference headers, g++ -O3 -ffp-contract=off, "
                        f"1 thread) on the same instance: symmetrize {t_sym:.2f}s, transpose "
                        f"{t_trans:.2f}s, 1-pass Ruiz {t_ruiz1:.2f}s, operator build {t_op:.2f}s, "
                        f"K-apply {t_k:.3f}s, A^T spmv {t_at:.3f}s, A spmv {t_a:.3f}s, residuals "
                        f"{t_res:.3f}s ({wall:.1f}s of CPU); solve time EXTRAPOLATED to {passes} "
-                       f"Ruiz passes, {iters} ADMM / {pcg} PCG iterations, {checks} checks"),
+                       f"Ruiz passes, {iters} ADMM / {pcg} PCG iterations, {checks} checks"
+                       + (f"; the reference's complete solve of this instance took {full:.0f} s on one "
+                          f"core of the build container (profiles/ref_solve_config{cfg}_*.json)"
+                          if full else "")),
             "extrapolated": True, "nproc": os.cpu_count(),
             "components_s": {"symmetrize": t_sym, "transpose": t_trans, "ruiz_1pass": t_ruiz1,
                              "operator_build": t_op, "k_apply": t_k, "at_spmv": t_at,
@@ -339,7 +353,7 @@ def run_reference(args, rank: int) -> None:
     counts = load_counts(args.config)
     vals = []
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(problem, counts)
+        cb = cpu_baseline(problem, counts, cfg=args.config, lam=args.lambda_pcg)
         if i >= args.warmup:
             vals.append(cb["value"])
     v = float(np.mean(vals))
@@ -510,7 +524,7 @@ def main():
             line["cpu_baseline"] = cpu_baseline(problem, {
                 "iterations": int(last.iterations),
                 "pcg_iterations_total": int(last.pcg_iterations_total),
-                "equil_passes": int(last.equil_passes)})
+                "equil_passes": int(last.equil_passes)}, cfg=args.config, lam=args.lambda_pcg)
         except Exception as e:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "error": repr(e)}
     print(json.dumps(line), flush=True)
