@@ -10,7 +10,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <stdexcept>
+#include <unordered_map>
 #include <string>
 
 namespace qpcg_b200 {
@@ -52,21 +55,156 @@ inline thread_local uint64_t g_launches = 0;
 // recycled from the pool by the next workspace instead of being unmapped and
 // re-mapped (cudaMalloc/cudaFree of multi-GB buffers costs ~100 ms per solve).
 inline thread_local cudaStream_t g_alloc_stream = nullptr;
-template <typename U>
-inline cudaError_t dmalloc(U** p, size_t bytes) {
-  return cudaMallocAsync(reinterpret_cast<void**>(p), bytes ? bytes : 1, g_alloc_stream);
-}
-inline cudaError_t dfree(void* p) { return p ? cudaFreeAsync(p, g_alloc_stream) : cudaSuccess; }
 inline void configure_pool(int device) {
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
   uint64_t thr = ~0ull;
   cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
 }
-struct AllocScope {  // routes dmalloc/dfree of this thread to stream s
+// A workspace's long-lived buffers (its matrices, scaled copies and vectors;
+// ~9 GB at config 2) are recycled through a process-wide cache keyed by
+// (device, size): the stream-ordered pool alone fragments across solves of the
+// same problem (the next setup then grows the pool, i.e. maps new physical
+// memory: 0.2-1.5 s).  A buffer enters the cache only after its owner has
+// synchronised every stream that used it, so any stream may take it next.
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> idle;  // (device, bytes) -> block
+  std::unordered_map<void*, std::pair<int, size_t>> owned;
+  size_t idle_bytes = 0;
+};
+inline BlockCache& block_cache() {
+  static BlockCache c;
+  return c;
+}
+constexpr size_t kCacheMin = size_t(1) << 20;     // smaller buffers: the pool
+constexpr size_t kCacheMax = size_t(96) << 30;    // idle bytes kept at most
+inline void cache_flush_idle() {
+  BlockCache& c = block_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  for (auto& kv : c.idle) {
+    c.owned.erase(kv.second);
+    cudaFree(kv.second);
+  }
+  c.idle.clear();
+  c.idle_bytes = 0;
+}
+inline cudaError_t cache_get(void** p, size_t bytes) {
+  if (bytes < kCacheMin) return cudaMallocAsync(p, bytes ? bytes : 1, g_alloc_stream);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  BlockCache& c = block_cache();
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    auto it = c.idle.lower_bound({dev, bytes});
+    if (it != c.idle.end() && it->first.first == dev && it->first.second <= bytes + bytes / 8) {
+      *p = it->second;
+      c.idle_bytes -= it->first.second;
+      c.idle.erase(it);
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaMallocAsync(p, bytes, g_alloc_stream);
+  if (e == cudaErrorMemoryAllocation) {  // idle blocks first, then retry once
+    cudaGetLastError();
+    cache_flush_idle();
+    e = cudaMallocAsync(p, bytes, g_alloc_stream);
+  }
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> g(c.mu);
+    c.owned[*p] = {dev, bytes};
+  }
+  return e;
+}
+// p's owner has synchronised the streams that used it
+inline void cache_put(void* p) {
+  if (!p) return;
+  BlockCache& c = block_cache();
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    auto it = c.owned.find(p);
+    if (it != c.owned.end()) {
+      if (c.idle_bytes + it->second.second <= kCacheMax) {
+        c.idle.emplace(it->second, p);
+        c.idle_bytes += it->second.second;
+        return;
+      }
+      c.owned.erase(it);
+    }
+  }
+  cudaFreeAsync(p, g_alloc_stream);
+}
+
+inline bool cache_owned(void* p, size_t* bytes) {
+  BlockCache& c = block_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  auto it = c.owned.find(p);
+  if (it == c.owned.end()) return false;
+  *bytes = it->second.second;
+  return true;
+}
+
+// A workspace's arena: every cached block it took, and the ones it already
+// released again (stream-ordered on its stream, so reusable by its later
+// allocations on that stream: the transient buffers of setup — sort keys,
+// cub scratch, scan flags — cycle through here instead of the pool).  The
+// owner returns all of them to the cache once its streams are idle.
+struct Arena {
+  std::multimap<size_t, void*> released;
+  std::vector<void*> taken;
+  void* get(size_t bytes) {
+    auto it = released.lower_bound(bytes);
+    if (it != released.end() && it->first <= bytes + bytes / 8) {
+      void* p = it->second;
+      released.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    if (cache_get(&p, bytes) != cudaSuccess) return nullptr;
+    taken.push_back(p);
+    return p;
+  }
+  void put(void* p, size_t bytes) { released.emplace(bytes, p); }
+  void return_all() {  // owner's streams synchronised
+    for (void* p : taken) cache_put(p);
+    taken.clear();
+    released.clear();
+  }
+};
+inline thread_local Arena* g_arena = nullptr;
+
+template <typename U>
+inline cudaError_t dmalloc(U** p, size_t bytes) {
+  if (g_arena && bytes >= kCacheMin) {
+    void* q = g_arena->get(bytes);
+    if (!q) return cudaErrorMemoryAllocation;
+    *p = static_cast<U*>(q);
+    return cudaSuccess;
+  }
+  return cudaMallocAsync(reinterpret_cast<void**>(p), bytes ? bytes : 1, g_alloc_stream);
+}
+inline cudaError_t dfree(void* p) {
+  if (!p) return cudaSuccess;
+  size_t bytes = 0;
+  if (g_arena && cache_owned(p, &bytes)) {
+    g_arena->put(p, bytes);
+    return cudaSuccess;
+  }
+  return cudaFreeAsync(p, g_alloc_stream);
+}
+
+struct AllocScope {  // routes dmalloc/dfree of this thread to stream s (and arena a)
   cudaStream_t prev;
-  explicit AllocScope(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
-  ~AllocScope() { g_alloc_stream = prev; }
+  Arena* prev_arena;
+  explicit AllocScope(cudaStream_t s, Arena* a = nullptr)
+      : prev(g_alloc_stream), prev_arena(g_arena) {
+    g_alloc_stream = s;
+    g_arena = a;
+  }
+  ~AllocScope() {
+    g_alloc_stream = prev;
+    g_arena = prev_arena;
+  }
 };
 
 // ------------------------------------------------------------ constants

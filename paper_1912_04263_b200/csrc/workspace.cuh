@@ -157,6 +157,11 @@ class Workspace : public IEngine<T> {
   bool have_counted_setup = false;
 
   ~Workspace() {
+    if (s_up) {
+      cudaStreamSynchronize(s_up);
+      cudaStreamDestroy(s_up);
+    }
+    if (ev_vals) cudaEventDestroy(ev_vals);
     if (s_side) {
       cudaStreamSynchronize(s_side);
       cudaStreamDestroy(s_side);
@@ -166,22 +171,26 @@ class Workspace : public IEngine<T> {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     {
-      AllocScope scope(s);
-      for (void* p : allocs) dfree(p);
+      AllocScope scope(s, &arena);
+      if (s) cudaStreamSynchronize(s);  // every stream that used the buffers is idle now
+      for (void* p : allocs) dfree(p);  // arena blocks: back to the arena; others: the pool
       for (SpmvPlan<T>* p : {&D.pP, &D.pA, &D.pAT}) plan_free(*p);
       if (tmp.ptr) dfree(tmp.ptr);
       tmp.ptr = nullptr;
       tmp.bytes = 0;
       if (s) cudaStreamSynchronize(s);
+      arena.return_all();
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (s && own_stream) cudaStreamDestroy(s);
   }
 
+  Arena arena;  // see common.cuh
   template <typename U>
   U* alloc(size_t count) {
     void* p = nullptr;
+    AllocScope scope(s, &arena);
     CK(dmalloc(&p, sizeof(U) * (count ? count : 1)));
     allocs.push_back(p);
     return static_cast<U*>(p);
@@ -225,8 +234,15 @@ class Workspace : public IEngine<T> {
     const double w0 = now_s();
     const uint64_t l0 = g_launches;
     begin(st, op, nullptr);
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     CK(cudaEventRecord(ev0, s));
+    // host input: A's values (2/3 of the upload) come in on a side stream
+    // while the structural setup (validation of the rows, plans, symmetrize,
+    // the transpose structure, the compressed index) runs on the main one
+    {
+      const char* e = std::getenv("QPCG_NO_DEFER");
+      defer_values = op.input_memory == QPCG_MEM_HOST && !(e && e[0] == '1');
+    }
     load(Pu, q, A, l, u, 0, A.rows, false);
     ValKeys k = validate_keys();
     raise_first(k);
@@ -326,7 +342,20 @@ class Workspace : public IEngine<T> {
     upload(pu_v, Pu.values, sizeof(T) * Pu.nnz);
     upload(a_rp, A.row_ptr + r0, sizeof(uint32_t) * (m + 1));
     upload(a_ci, A.col_indices + e0, sizeof(uint32_t) * annz);
-    upload(a_v, A.values + e0, sizeof(T) * annz);
+    if (defer_values && annz) {
+      if (!s_up) {
+        CK(cudaStreamCreateWithFlags(&s_up, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_vals, cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(ev_vals, s));  // a_v is allocated on s
+      CK(cudaStreamWaitEvent(s_up, ev_vals, 0));
+      CK(cudaMemcpyAsync(a_v, A.values + e0, sizeof(T) * annz, cudaMemcpyHostToDevice, s_up));
+      h2d_bytes += sizeof(T) * annz;
+      CK(cudaEventRecord(ev_vals, s_up));
+      values_pending = true;
+    } else {
+      upload(a_v, A.values + e0, sizeof(T) * annz);
+    }
     upload(D.q_o, q, sizeof(T) * n);
     upload(D.l_o, l + r0, sizeof(T) * m);
     upload(D.u_o, u + r0, sizeof(T) * m);
@@ -335,10 +364,23 @@ class Workspace : public IEngine<T> {
       for_n(m + 1, [=] __device__(uint32_t i) { rp[i] -= e0; }, s);
     }
     D.A = DevCsr<T>{m, A.cols, annz, a_v, a_rp, a_ci};
-    if (opt.input_memory == QPCG_MEM_HOST) {
+    h2d_t0 = th;
+    if (opt.input_memory == QPCG_MEM_HOST && !values_pending) {
       CK(cudaStreamSynchronize(s));
       h2d_seconds = now_s() - th;
     }
+  }
+  // deferred-values bookkeeping (single-device host-input setup)
+  bool defer_values = false, values_pending = false;
+  cudaStream_t s_up = nullptr;
+  cudaEvent_t ev_vals = nullptr;
+  double h2d_t0 = 0;
+  void wait_values() {
+    if (!values_pending) return;
+    CK(cudaStreamWaitEvent(s, ev_vals, 0));
+    CK(cudaEventSynchronize(ev_vals));
+    h2d_seconds = now_s() - h2d_t0;  // upload wall time, overlapped with the structural setup
+    values_pending = false;
   }
   uint32_t host_rp(const HostCsr<T>& A, uint32_t r) {
     if (opt.input_memory == QPCG_MEM_HOST) return A.row_ptr[r];
@@ -376,15 +418,33 @@ class Workspace : public IEngine<T> {
       validate_csr_rows_kernel<<<grid_for(m), kThreads, 0, s>>>(a_rp, a_ci, m, a_cols, kValARowPtr, 0,
                                                                key + 1, row0);
       CK_LAUNCH();
-      validate_values_kernel<T><<<grid_for(pu_nnz), kThreads, 0, s>>>(pu_v, pu_nnz, kValPFinite, key + 2, 0);
-      validate_values_kernel<T><<<grid_for(D.A.nnz), kThreads, 0, s>>>(a_v, D.A.nnz, kValAFinite, key + 2, nnz0);
-      validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.q_o, n, kValQFinite, key + 2, 0);
-      validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(D.l_o, D.u_o, m, key + 2, row0);
-      CK_LAUNCH();
+      if (!values_pending) launch_value_checks(key + 2);
     }
     CK(cudaMemcpyAsync(v.k, key, 24, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (values_pending) value_key = key + 2;  // checked once the values have arrived
     return v;
+  }
+  unsigned long long* value_key = nullptr;
+  void launch_value_checks(unsigned long long* key) {
+    const uint32_t n = D.n, m = D.m;
+    validate_values_kernel<T><<<grid_for(pu_nnz), kThreads, 0, s>>>(pu_v, pu_nnz, kValPFinite, key, 0);
+    validate_values_kernel<T><<<grid_for(D.A.nnz), kThreads, 0, s>>>(a_v, D.A.nnz, kValAFinite, key, nnz0);
+    validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.q_o, n, kValQFinite, key, 0);
+    validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(D.l_o, D.u_o, m, key, row0);
+    CK_LAUNCH();
+  }
+  // the values' checks (problem.hpp:75-91, the last in the reference's order)
+  // after a deferred upload
+  void check_values_late() {
+    if (!value_key) return;
+    wait_values();
+    launch_value_checks(value_key);
+    unsigned long long k = 0;
+    CK(cudaMemcpyAsync(&k, value_key, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    value_key = nullptr;
+    if (k != ~0ull) throw InvalidArgument(validation_message(k));
   }
   void raise_first(const ValKeys& v) const {
     if (v.ends[0] != 0 || v.ends[1] != pu_nnz)
@@ -428,15 +488,17 @@ class Workspace : public IEngine<T> {
     uint32_t* at_ci = alloc<uint32_t>(annz);
     permA = alloc<uint32_t>(annz);
     transpose_structure(a_ci, row_of, n, annz, at_rp, at_ci, permA, tmp, s);
-    T* ato_v = alloc<T>(annz);
-    gather_values(a_v, permA, annz, ato_v, s);
-    D.Ao = DevCsr<T>{m, n, annz, a_v, a_rp, a_ci};
-    D.ATo = DevCsr<T>{n, m, annz, ato_v, at_rp, at_ci};
     D.pAT = plan_build<T>(at_rp, n, tmp, s);
     if (compress_indices()) {  // 16-bit column offsets for the A / A^T streams
       plan_compress(D.pA, a_ci, annz, n, tmp, s);
       plan_compress(D.pAT, at_ci, annz, m, tmp, s);
     }
+    // ---- from here on A's values are needed
+    check_values_late();
+    T* ato_v = alloc<T>(annz);
+    gather_values(a_v, permA, annz, ato_v, s);
+    D.Ao = DevCsr<T>{m, n, annz, a_v, a_rp, a_ci};
+    D.ATo = DevCsr<T>{n, m, annz, ato_v, at_rp, at_ci};
     D.pPo = D.pP;
     D.pAo = D.pA;
     D.pATo = D.pAT;
@@ -956,7 +1018,7 @@ class Workspace : public IEngine<T> {
 
   void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) override {
     CK(cudaSetDevice(device));
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     const double w0 = now_s();
     CK(cudaEventRecord(ev0, s));
     reset_solve_state();
@@ -1013,7 +1075,7 @@ class Workspace : public IEngine<T> {
   // ------------------------------------------------- OSQP-style updates
   void warm_start(const T* x, const T* z, const T* y) override {  // solver.hpp:413-428
     CK(cudaSetDevice(device));
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     if (warm_stage(x, z, y) != ~0ull) throw InvalidArgument("solve: warm start must be finite");
     warm_apply();
   }
@@ -1099,7 +1161,7 @@ class Workspace : public IEngine<T> {
 
   void debug_operator(const T* x, T* kx, T* dinv) override {
     CK(cudaSetDevice(device));
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     pull_ctl();
     const Ctl<T> saved = hc;
     hc.pcg_active = 1;
@@ -1118,7 +1180,7 @@ class Workspace : public IEngine<T> {
   // CUDA-event timing of the PCG-iteration kernels (bench.py roofline)
   void bench_kernels(uint32_t reps, double* out) override {
     CK(cudaSetDevice(device));
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     pull_ctl();
     const Ctl<T> saved = hc;
     Ctl<T> run = hc;
@@ -1207,7 +1269,7 @@ class Workspace : public IEngine<T> {
     op.input_memory = QPCG_MEM_HOST;
     op.mode = QPCG_MODE_EAGER;
     begin(st, op, nullptr);
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     const uint32_t n = Pf.rows, m = A.rows;
     D.n = n;
     D.m = m;
@@ -1284,7 +1346,7 @@ class Workspace : public IEngine<T> {
 
   void op_pcg(const T* b, const T* warm, T eps, uint32_t max_iter, T* x, double* res) {
     CK(cudaSetDevice(device));
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     if (!(eps > T(0))) throw InvalidArgument("pcg: eps must be positive");
     const uint32_t n = D.n;
     upload(D.b, b, sizeof(T) * n);
@@ -1378,7 +1440,7 @@ class Workspace : public IEngine<T> {
   // Not in the reference: rescale with the existing D, E, c.
   void update_vectors(const T* q, const T* l, const T* u) override {
     CK(cudaSetDevice(device));
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     const unsigned long long k = vectors_stage(q, l, u);
     if (k != ~0ull) throw InvalidArgument(validation_message(k));
     vectors_apply();
