@@ -10,13 +10,21 @@
 //   while PCG: A pass [t = rho A p] ; A^T pass [Kp = P p + sigma p + A^T t] ;
 //              k_pcg_dot ; k_pcg_update ; k_pcg_pupdate
 //   k_pcg_fin
-//   A pass    [z~ = A x~, m-side relax/project/dual update ; A x_new]    2 cols
+//   A pass    [z~ = A x~, m-side relax/project/dual update (; A x_new on
+//             check iterations: 2 cols, else 1 col)]
 //   k_xupdate
 //   if check: A^T pass [A^T y, P x, r_dual] ; k_residuals
 //             if not optimal: A_o^T, P_o, A_o passes ; k_infeas
 //   if rho:   k_rho ; k_precond
 // The matrix streams are A and A^T once per PCG iteration plus once each per
 // ADMM step (the reference streams 4 A-sized matrices + P per step).
+//
+// Three drivers run this sequence with bitwise-identical results: a CUDA
+// graph with conditional WHILE/IF nodes (default), the persistent kernel of
+// persist.cuh (one block / one cluster / a cooperative grid; picked by the
+// graph mode for small problems) and a host-driven eager loop.  The row-
+// sharded engine (shard.cuh) drives one Workspace per row block.  Setup
+// allocations go through the workspace's arena (common.cuh).
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
