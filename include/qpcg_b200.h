@@ -184,7 +184,21 @@ typedef struct {
   const void* nccl_id;     /* NULL: no NCCL.  Else the QPCG_NCCL_ID_BYTES-byte
                               id from qpcg_nccl_unique_id on rank 0, shared by
                               all ranks (e.g. a torch.distributed broadcast) */
+  int32_t transport;       /* QPCG_TRANSPORT_*: how the ranks' row blocks are
+                              combined */
+  int32_t reserved2_;
+  const char* rendezvous_dir; /* QPCG_TRANSPORT_PEER without an NCCL id: a
+                              directory shared by the ranks (fresh per group)
+                              through which they exchange their IPC handles */
 } qpcg_options;
+
+/* NCCL collectives (default), or stores into every peer's memory (CUDA IPC /
+ * NVLink P2P) with device-side barriers: the ranks' partials are summed in
+ * block order, bitwise identical to a one-process run with the same number
+ * of virtual blocks.  nccl_rank / nccl_ranks give the rank and group size
+ * for both transports. */
+#define QPCG_TRANSPORT_NCCL 0
+#define QPCG_TRANSPORT_PEER 1
 
 #define QPCG_NCCL_ID_BYTES 128
 

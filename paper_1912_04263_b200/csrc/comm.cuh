@@ -18,8 +18,12 @@
 #include <dlfcn.h>
 #include <nccl.h>  // types and enums only: every symbol is resolved through dlopen
 
+#include <chrono>
+#include <cstdio>
 #include <map>
 #include <mutex>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -41,6 +45,8 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -63,6 +69,7 @@ inline NcclApi& nccl_api() {
     sym(api.Broadcast, "ncclBroadcast");
     sym(api.Send, "ncclSend");
     sym(api.Recv, "ncclRecv");
+    sym(api.AllGather, "ncclAllGather");
     sym(api.GroupStart, "ncclGroupStart");
     sym(api.GroupEnd, "ncclGroupEnd");
     sym(api.GetErrorString, "ncclGetErrorString");
@@ -111,12 +118,213 @@ __global__ void k_local_combine(ShardPtrs<T> b, int L, size_t count) {
   }
 }
 
+// ------------------------------------------------------- peer transport
+// The collectives over peer memory (NVLink P2P stores between the GPUs of one
+// box; CUDA IPC mappings between processes).  Every rank owns one symmetric
+// area (same layout everywhere), maps every peer's area, and:
+//   * allreduce: each rank stores its blocks' partials into slot g (= global
+//     block index) of EVERY rank's area, a device-side barrier (system-scope
+//     arrival counters in every area), then each rank sums the G slots in
+//     block order.  The combination is a flat sequential sum in block order on
+//     every rank: bitwise identical across ranks AND to the single-process run
+//     with the same G virtual blocks (k_local_combine).  The slot sets are
+//     double-buffered, so no trailing barrier is needed;
+//   * the diag(A^T A) chain and the block gather of the m-vectors use the
+//     same stores and barriers.
+// Bootstrap (exchanging the IPC handles) goes through NCCL when the caller
+// gave an NCCL id, else through a rendezvous directory.
+struct PeerPtrs {
+  char* p[kMaxLocalShards];
+};
+
+template <typename T>
+__global__ void k_p2p_publish(ShardPtrs<T> src, int L, size_t count, PeerPtrs dst, int R,
+                              size_t off_bytes, size_t slot_bytes) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    for (int l = 0; l < L; ++l) {
+      const T v = src.p[l][i];
+      for (int r = 0; r < R; ++r)
+        reinterpret_cast<T*>(dst.p[r] + off_bytes + l * slot_bytes)[i] = v;
+    }
+  }
+}
+
+// one thread: fence, arrive at every rank's counter, wait for my counter
+static __global__ void k_p2p_barrier(PeerPtrs area, int R, int rank, unsigned long long target) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  __threadfence_system();
+  for (int r = 0; r < R; ++r)
+    atomicAdd_system(reinterpret_cast<unsigned long long*>(area.p[r]), 1ull);
+  const volatile unsigned long long* mine =
+      reinterpret_cast<const volatile unsigned long long*>(area.p[rank]);
+  while (*mine < target) __nanosleep(200);
+  __threadfence_system();
+}
+
+template <typename T, bool MAX>
+__global__ void k_p2p_reduce(const char* slots, size_t slot_bytes, int G, size_t count,
+                             ShardPtrs<T> out, int L) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    T a = __ldcv(reinterpret_cast<const T*>(slots) + i);
+    for (int g = 1; g < G; ++g) {
+      const T v = __ldcv(reinterpret_cast<const T*>(slots + g * slot_bytes) + i);
+      a = MAX ? smax(a, v) : a + v;
+    }
+    for (int l = 0; l < L; ++l) out.p[l][i] = a;
+  }
+}
+
+static __global__ void k_p2p_min_u64(const char* slots, size_t slot_bytes, int R,
+                              unsigned long long* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long a = ~0ull;
+  for (int r = 0; r < R; ++r) {
+    const unsigned long long v = __ldcv(reinterpret_cast<const unsigned long long*>(slots + r * slot_bytes));
+    a = v < a ? v : a;
+  }
+  *out = a;
+}
+
+struct P2PArea {
+  int rank = 0, R = 1, G = 1, L = 1;
+  char* mine = nullptr;
+  size_t bytes = 0, vcap = 0, m = 0, n = 0;
+  size_t off_vec = 0, off_u64 = 0, off_gbuf = 0, off_chain = 0;  // (flags at 0)
+  std::vector<char*> peer;
+  unsigned long long epoch = 0;  // barriers so far (identical on every rank)
+  uint32_t parity = 0;           // slot set of the next allreduce
+  size_t vec_slot() const { return vcap * 8; }
+  size_t vec_set() const { return vec_slot() * G; }
+};
+
+inline void p2p_exchange_file(const std::string& dir, int rank, int R, const void* mine, size_t bytes,
+                              std::vector<std::string>& all) {
+  // write my handle atomically, then poll for every rank's
+  const std::string me = dir + "/rank" + std::to_string(rank) + ".ipc";
+  {
+    const std::string tmp = me + ".tmp";
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    if (!f) throw NcclError("p2p: cannot write the rendezvous file " + tmp);
+    std::fwrite(mine, 1, bytes, f);
+    std::fclose(f);
+    std::rename(tmp.c_str(), me.c_str());
+  }
+  all.assign(R, std::string());
+  const double t0 = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  for (int r = 0; r < R; ++r) {
+    const std::string fn = dir + "/rank" + std::to_string(r) + ".ipc";
+    for (;;) {
+      FILE* f = std::fopen(fn.c_str(), "rb");
+      if (f) {
+        std::string buf(bytes, '\0');
+        const size_t got = std::fread(&buf[0], 1, bytes, f);
+        std::fclose(f);
+        if (got == bytes) {
+          all[r] = buf;
+          break;
+        }
+      }
+      const double t = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+      if (t - t0 > 120.0) throw NcclError("p2p: rendezvous timed out waiting for rank " + std::to_string(r));
+      std::this_thread::sleep_for(std::chrono::milliseconds(2));
+    }
+  }
+}
+
 // ------------------------------------------------------------------ comm
 struct ShardComm {
-  int rank = 0, nranks = 1;  // NCCL process group (nranks == 1 and no comm: local only)
+  int rank = 0, nranks = 1;  // process group (nranks == 1 and no transport: local only)
   int local = 1;             // shards on this device
   ncclComm_t comm = nullptr;
   cudaStream_t s = nullptr;
+  P2PArea* p2p = nullptr;    // the peer-memory transport (owned), else NCCL
+
+  bool multi() const { return comm != nullptr || p2p != nullptr; }
+
+  // Set up the peer transport for G = local * R blocks of an (n, m) problem.
+  // The NCCL comm, when there is one, only carries the bootstrap.
+  void init_p2p(int r, int R, const char* dir, size_t n, size_t m) {
+    rank = r;
+    nranks = R;
+    auto* a = new P2PArea();
+    p2p = a;
+    a->rank = r;
+    a->R = R;
+    a->L = local;
+    a->G = local * R;
+    a->n = n;
+    a->m = m;
+    a->vcap = std::max<size_t>(2 * n, 16);
+    size_t off = 64;
+    a->off_vec = off;
+    off += 2 * a->vec_set();
+    a->off_u64 = off;
+    off += 8 * size_t(R);
+    a->off_gbuf = off;
+    off += 8 * std::max<size_t>(m, 1);
+    a->off_chain = off;
+    off += 8 * std::max<size_t>(n, 1);
+    a->bytes = off;
+    CK(cudaMalloc(&a->mine, a->bytes));  // IPC needs a plain allocation
+    CK(cudaMemset(a->mine, 0, a->bytes));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, a->mine));
+    std::vector<std::string> all;
+    if (comm) {  // bootstrap over NCCL
+      char *dsend = nullptr, *drecv = nullptr;
+      CK(cudaMalloc(&dsend, sizeof(h)));
+      CK(cudaMalloc(&drecv, sizeof(h) * R));
+      CK(cudaMemcpy(dsend, &h, sizeof(h), cudaMemcpyHostToDevice));
+      nccl_check(nccl_api().AllGather(dsend, drecv, sizeof(h), ncclChar, comm, s), "ncclAllGather");
+      std::string buf(sizeof(h) * R, '\0');
+      CK(cudaMemcpyAsync(&buf[0], drecv, buf.size(), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      cudaFree(dsend);
+      cudaFree(drecv);
+      all.assign(R, std::string());
+      for (int i = 0; i < R; ++i) all[i] = buf.substr(i * sizeof(h), sizeof(h));
+    } else {
+      if (!dir) throw InvalidArgument("options: the peer transport needs an NCCL id or a rendezvous directory");
+      p2p_exchange_file(dir, r, R, &h, sizeof(h), all);
+    }
+    a->peer.assign(R, nullptr);
+    for (int i = 0; i < R; ++i) {
+      if (i == r) {
+        a->peer[i] = a->mine;
+        continue;
+      }
+      cudaIpcMemHandle_t hi;
+      std::memcpy(&hi, all[i].data(), sizeof(hi));
+      void* q = nullptr;
+      CK(cudaIpcOpenMemHandle(&q, hi, cudaIpcMemLazyEnablePeerAccess));
+      a->peer[i] = static_cast<char*>(q);
+    }
+    barrier();  // every rank has mapped every area
+    CK(cudaStreamSynchronize(s));
+  }
+  void free_p2p() {
+    if (!p2p) return;
+    cudaStreamSynchronize(s);
+    barrier();  // nobody writes into an area after it is unmapped
+    cudaStreamSynchronize(s);
+    for (int i = 0; i < p2p->R; ++i)
+      if (i != p2p->rank && p2p->peer[i]) cudaIpcCloseMemHandle(p2p->peer[i]);
+    cudaFree(p2p->mine);
+    delete p2p;
+    p2p = nullptr;
+  }
+  PeerPtrs peers(size_t off) const {
+    PeerPtrs pp{};
+    for (int i = 0; i < p2p->R; ++i) pp.p[i] = p2p->peer[i] + off;
+    return pp;
+  }
+  void barrier() {
+    p2p->epoch += 1;
+    k_p2p_barrier<<<1, 32, 0, s>>>(peers(0), p2p->R, p2p->rank, p2p->epoch * p2p->R);
+    CK_LAUNCH();
+  }
 
   int global_count() const { return local * nranks; }
   int global_index(int l) const { return rank * local + l; }
@@ -146,12 +354,33 @@ struct ShardComm {
     nccl_check(api.CommInitRank(&comm, nr, uid, r), "ncclCommInitRank");
     cache.emplace(key, comm);
   }
-  ~ShardComm() {}  // the cached communicator outlives the workspace
+  ~ShardComm() { free_p2p(); }  // (the cached NCCL communicator outlives the workspace)
 
   // in-place allreduce of `count` elements held in one buffer per local shard
   template <typename T>
   void allreduce(const std::vector<T*>& bufs, size_t count, bool max) {
     if (count == 0) return;
+    if (p2p) {  // publish into every rank's slots, barrier, ordered sum of all G slots
+      P2PArea& a = *p2p;
+      if (count > a.vcap) throw InvalidArgument("p2p: allreduce larger than the slots");
+      ShardPtrs<T> src{};
+      for (size_t l = 0; l < bufs.size(); ++l) src.p[l] = bufs[l];
+      const size_t set = a.off_vec + (a.parity & 1u) * a.vec_set();
+      a.parity ^= 1u;
+      const uint32_t g = (uint32_t)std::min<size_t>((count + kThreads - 1) / kThreads, 4u * kNumSMs);
+      k_p2p_publish<T><<<g, kThreads, 0, s>>>(src, (int)bufs.size(), count, peers(set), a.R,
+                                               size_t(rank) * a.L * a.vec_slot(), a.vec_slot());
+      CK_LAUNCH();
+      barrier();
+      if (max)
+        k_p2p_reduce<T, true><<<g, kThreads, 0, s>>>(a.mine + set, a.vec_slot(), a.G, count, src,
+                                                     (int)bufs.size());
+      else
+        k_p2p_reduce<T, false><<<g, kThreads, 0, s>>>(a.mine + set, a.vec_slot(), a.G, count, src,
+                                                      (int)bufs.size());
+      CK_LAUNCH();
+      return;
+    }
     if (bufs.size() > 1) {
       ShardPtrs<T> p{};
       for (size_t l = 0; l < bufs.size(); ++l) p.p[l] = bufs[l];
@@ -173,6 +402,16 @@ struct ShardComm {
 
   // min over every rank of one device-resident uint64 (validation keys)
   void allreduce_min_u64(unsigned long long* dev) {
+    if (p2p) {
+      P2PArea& a = *p2p;
+      for (int r = 0; r < a.R; ++r)
+        CK(cudaMemcpyAsync(a.peer[r] + a.off_u64 + 8 * size_t(rank), dev, 8, cudaMemcpyDeviceToDevice, s));
+      barrier();
+      k_p2p_min_u64<<<1, 32, 0, s>>>(a.mine + a.off_u64, 8, a.R, dev);
+      CK_LAUNCH();
+      barrier();  // the u64 slots are single-buffered
+      return;
+    }
     if (comm)
       nccl_check(nccl_api().AllReduce(dev, dev, 1, ncclUint64, ncclMin, comm, s), "ncclAllReduce");
   }
@@ -182,6 +421,24 @@ struct ShardComm {
   // sent on to r+1 and the final value is broadcast from the last rank.
   template <typename T, typename F>
   void chain(T* acc, size_t count, F&& body) {
+    if (p2p) {  // rank k continues the running value, hands it to k+1; the last one to all
+      P2PArea& a = *p2p;
+      T* mine = reinterpret_cast<T*>(a.mine + a.off_chain);
+      for (int k = 0; k < a.R; ++k) {
+        if (k == rank) {
+          if (k > 0) CK(cudaMemcpyAsync(acc, mine, sizeof(T) * count, cudaMemcpyDeviceToDevice, s));
+          body();
+          for (int r = (k + 1 < a.R ? k + 1 : 0); r < (k + 1 < a.R ? k + 2 : a.R); ++r)
+            if (r != rank)
+              CK(cudaMemcpyAsync(a.peer[r] + a.off_chain, acc, sizeof(T) * count,
+                                 cudaMemcpyDeviceToDevice, s));
+        }
+        barrier();
+      }
+      if (rank + 1 < a.R) CK(cudaMemcpyAsync(acc, mine, sizeof(T) * count, cudaMemcpyDeviceToDevice, s));
+      barrier();  // the chain buffer is single-buffered
+      return;
+    }
     NcclApi* api = comm ? &nccl_api() : nullptr;
     if (comm && rank > 0) nccl_check(api->Recv(acc, count, nccl_type<T>(), rank - 1, comm, s), "ncclRecv");
     body();
@@ -195,6 +452,24 @@ struct ShardComm {
   // (already in place locally); afterwards every rank holds all of it.
   template <typename T>
   void allgather_blocks(T* full, const std::vector<uint32_t>& off) {
+    if (p2p) {
+      P2PArea& a = *p2p;
+      const size_t b = off[rank], cnt = off[rank + 1] - off[rank];
+      if (cnt)
+        for (int r = 0; r < a.R; ++r)
+          if (r != rank)
+            CK(cudaMemcpyAsync(a.peer[r] + a.off_gbuf + sizeof(T) * b, full + b, sizeof(T) * cnt,
+                               cudaMemcpyDeviceToDevice, s));
+      barrier();
+      for (int r = 0; r < a.R; ++r) {
+        const size_t rb = off[r], rc = off[r + 1] - off[r];
+        if (r != rank && rc)
+          CK(cudaMemcpyAsync(full + rb, a.mine + a.off_gbuf + sizeof(T) * rb, sizeof(T) * rc,
+                             cudaMemcpyDeviceToDevice, s));
+      }
+      barrier();  // the gather buffer is single-buffered
+      return;
+    }
     if (!comm || nranks == 1) return;
     NcclApi& api = nccl_api();
     nccl_check(api.GroupStart(), "ncclGroupStart");

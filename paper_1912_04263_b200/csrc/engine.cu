@@ -60,7 +60,9 @@ std::unique_ptr<IEngine<double>>& slot<double>(qpcg_workspace* ws) { return ws->
 template <>
 std::unique_ptr<IEngine<float>>& slot<float>(qpcg_workspace* ws) { return ws->e32; }
 
-bool is_sharded(const qpcg_options& o) { return o.virtual_shards > 1 || o.nccl_id != nullptr; }
+bool is_sharded(const qpcg_options& o) {
+  return o.virtual_shards > 1 || o.nccl_id != nullptr || o.transport == QPCG_TRANSPORT_PEER;
+}
 
 template <typename T, typename CsrT>
 int setup_impl(qpcg_workspace** out, const CsrT* p, const T* q, const CsrT* a, const T* l,

@@ -45,6 +45,7 @@ class Sharded : public IEngine<T> {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   ~Sharded() {
+    comm.free_p2p();  // a collective: every rank tears down together
     sh.clear();  // blocks free their buffers on the shared stream
     if (full_m) {
       AllocScope scope(s);
@@ -77,7 +78,7 @@ class Sharded : public IEngine<T> {
   unsigned long long agree_min(const std::vector<unsigned long long>& keys) {
     unsigned long long k = ~0ull;
     for (auto v : keys) k = std::min(k, v);
-    if (comm.comm) {
+    if (comm.multi()) {
       unsigned long long* d = w0().template alloc<unsigned long long>(1);
       CK(cudaMemcpyAsync(d, &k, 8, cudaMemcpyHostToDevice, s));
       comm.allreduce_min_u64(d);
@@ -109,14 +110,17 @@ class Sharded : public IEngine<T> {
     comm.s = s;
     comm.local = op.virtual_shards > 1 ? op.virtual_shards : 1;
     if (comm.local > kMaxLocalShards) throw InvalidArgument("options: at most 16 virtual shards");
-    if (op.nccl_id != nullptr) {
+    const bool peer = op.transport == QPCG_TRANSPORT_PEER;
+    if (op.nccl_id != nullptr || peer) {
       if (op.nccl_ranks < 1 || op.nccl_rank < 0 || op.nccl_rank >= op.nccl_ranks)
-        throw InvalidArgument("options: bad nccl rank / ranks");
-      comm.init_nccl(op.nccl_id, op.nccl_rank, op.nccl_ranks);
+        throw InvalidArgument("options: bad rank / ranks");
+      if (op.nccl_ranks > kMaxLocalShards) throw InvalidArgument("options: at most 16 ranks");
     }
-    const uint32_t L = comm.local, R = comm.nranks, G = L * R;
+    if (op.nccl_id != nullptr) comm.init_nccl(op.nccl_id, op.nccl_rank, op.nccl_ranks);
     n = Pu.rows;
     m = A.rows;
+    if (peer) comm.init_p2p(op.nccl_rank, op.nccl_ranks, op.rendezvous_dir, n, m);
+    const uint32_t L = comm.local, R = comm.nranks, G = L * R;
     // ---- nnz-balanced cuts from the (host copy of) row_ptr
     std::vector<uint32_t> hrp;
     const uint32_t* rp = A.row_ptr;

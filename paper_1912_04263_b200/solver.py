@@ -79,10 +79,11 @@ def _pre(dtype) -> str:
 
 def make_options(device: int = -1, mode: str = "graph", record_diagnostics: bool = False,
                  device_memory: bool = False, shards: int = 1,
-                 nccl: tuple | None = None) -> _abi.Options:
+                 nccl: tuple | None = None, peer: tuple | None = None) -> _abi.Options:
     """shards: row blocks of A held on this device (virtual shards);
     nccl: (rank, ranks, id_bytes) to join the row-sharded NCCL group
-    (id_bytes from nccl_unique_id() on rank 0)."""
+    (SURVEY.md §8(e); id_bytes from nccl_unique_id() on rank 0);
+    peer: (rank, ranks, rendezvous_dir) for the peer-memory transport."""
     o = _abi.Options()
     o.device = device
     o.input_memory = _abi.MEM_DEVICE if device_memory else _abi.MEM_HOST
@@ -95,6 +96,13 @@ def make_options(device: int = -1, mode: str = "graph", record_diagnostics: bool
         o.nccl_rank, o.nccl_ranks = int(rank), int(ranks)
         o.nccl_id = C.cast(buf, C.c_void_p)
         o._keep_id = buf  # the id must outlive the setup call
+    if peer is not None:  # (rank, ranks, rendezvous_dir or None with an NCCL id)
+        rank, ranks, rdir = peer
+        o.transport = _abi.TRANSPORT_PEER
+        o.nccl_rank, o.nccl_ranks = int(rank), int(ranks)
+        if rdir is not None:
+            o._keep_dir = C.create_string_buffer(str(rdir).encode())
+            o.rendezvous_dir = C.cast(o._keep_dir, C.c_char_p)
     return o
 
 
@@ -122,13 +130,14 @@ class Workspace:
 
     def __init__(self, problem: QpProblem, settings: Settings | None = None, device: int = -1,
                  mode: str = "graph", record_diagnostics: bool = False, shards: int = 1,
-                 nccl: tuple | None = None):
+                 nccl: tuple | None = None, peer: tuple | None = None):
         self.lib = load_library()
         self.problem = problem
         self.dtype = problem.dtype
         self.pre = _pre(self.dtype)
         self.settings = settings or Settings()
-        self._opts = make_options(device, mode, record_diagnostics, shards=shards, nccl=nccl)
+        self._opts = make_options(device, mode, record_diagnostics, shards=shards, nccl=nccl,
+                                  peer=peer)
         self._s = self.settings.to_c()
         self._pv, self._av = problem.p_upper.view(), problem.a.view()
         self.ws = C.c_void_p()
@@ -205,12 +214,12 @@ def fetch_diagnostics(lib, ws, diag: SolveDiagnostics):
 
 def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | None = None,
           diag: SolveDiagnostics | None = None, device: int = -1, mode: str = "graph",
-          shards: int = 1, nccl: tuple | None = None):
+          shards: int = 1, nccl: tuple | None = None, peer: tuple | None = None):
     """Drop-in for qpcg::solve (solver.hpp:386-541) on the B200 engine.
-    shards > 1 / nccl: the row-sharded engine."""
+    shards > 1 / nccl / peer: the row-sharded engine."""
     if diag is not None:
         with Workspace(p, settings, device, mode, record_diagnostics=True, shards=shards,
-                       nccl=nccl) as ws:
+                       nccl=nccl, peer=peer) as ws:
             if initial is not None:
                 ws.warm_start(initial.x, initial.z, initial.y)
             return ws.solve(diag)
@@ -219,7 +228,7 @@ def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | N
     n, m = p.n, p.m
     dt = p.dtype
     s = (settings or Settings()).to_c()
-    o = make_options(device, mode, shards=shards, nccl=nccl)
+    o = make_options(device, mode, shards=shards, nccl=nccl, peer=peer)
     x, z, y = np.zeros(n, dt), np.zeros(m, dt), np.zeros(m, dt)
     cert = np.zeros(max(n, m), dt)
     info = _abi.Info()
