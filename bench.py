@@ -24,10 +24,12 @@ RNG and recipes; fp64; settings {"lambda_pcg": 1e-3} (0.01, the survey's choice,
 
 --impl reference runs only the reference CPU arm (rank 0), same metric/config.
 Multi-GPU (torchrun, N > 1): the ROW-SHARDED engine — every
-rank holds an nnz-balanced block of A's rows (+ its own A_g^T), the A^T
-partials are summed with NCCL once per operator apply; one instance solved by
-all N GPUs ("strong" scaling), value = max over ranks of the device-timed
-solve.  --replicas instead solves an independent instance per rank ("weak").
+rank holds an nnz-balanced block of A's rows (+ its own A_g^T), and the A^T
+partials are combined once per operator apply: by default the SpMV epilogue
+stores its rows straight into every peer's memory (NVLink P2P via CUDA IPC)
+and a device-side barrier + block-ordered sum follows (--transport nccl: NCCL
+allreduce instead); one instance solved by all N GPUs ("strong" scaling),
+value = max over ranks of the device-timed solve.  --replicas instead solves an independent instance per rank ("weak").
 --shards K (N = 1) runs the sharded engine with K row blocks on one GPU.
 """
 from __future__ import annotations
@@ -80,6 +82,9 @@ def parse():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent instance per rank instead of the row-sharded solve")
     ap.add_argument("--shards", type=int, default=1, help="row blocks per GPU (virtual shards)")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: combine the ranks' A^T partials by stores into every peer's "
+                         "memory fused into the SpMV epilogue (peer) or by NCCL allreduce")
     ap.add_argument("--sweep", default="",
                     help="CLASSES:SCALES[:INSTANCES] (e.g. lasso,svm:1,3,5:10): instead of the "
                          "headline line, print the bench/runner.hpp CSV sweep solved by the engine "
@@ -161,7 +166,8 @@ def _views(arrs, n, m, dev):
 
 
 class Engine:
-    def __init__(self, problem, settings, device, stream_ptr, dtype, mode, shards=1, nccl=None):
+    def __init__(self, problem, settings, device, stream_ptr, dtype, mode, shards=1, nccl=None,
+                 transport="nccl"):
         import torch
         from paper_1912_04263_b200 import _abi, solver
         self.lib = solver.load_library()
@@ -194,10 +200,12 @@ class Engine:
             o.record_diagnostics = 0
             o.virtual_shards = shards
             o.stream = C.c_void_p(stream_ptr)
-            if nccl is not None:  # (rank, ranks, id): the row-sharded NCCL group
+            if nccl is not None:  # (rank, ranks, id): the row-sharded group
                 self._id = C.create_string_buffer(bytes(nccl[2]), _abi.NCCL_ID_BYTES)
                 o.nccl_rank, o.nccl_ranks = nccl[0], nccl[1]
                 o.nccl_id = C.cast(self._id, C.c_void_p)
+                if transport == "peer":  # NCCL only bootstraps the IPC handles
+                    o.transport = _abi.TRANSPORT_PEER
             self.opts[memkind] = o
         self._abi = _abi
         self.msg = C.create_string_buffer(512)
@@ -420,7 +428,7 @@ def main():
     stream = torch.cuda.Stream(device=local)
     with torch.cuda.stream(stream):
         eng = Engine(problem, settings, local, stream.cuda_stream, dtype, args.mode,
-                     shards=args.shards, nccl=nccl)
+                     shards=args.shards, nccl=nccl, transport=args.transport)
         for i in range(args.warmup):
             t = time.time()
             info = eng.solve("device")
@@ -500,7 +508,7 @@ def main():
             "config": {"workload": WORKLOADS[args.config], "config_id": args.config,
                        "n": problem.n, "m": problem.m, "nnz_P_upper": problem.p_upper.nnz,
                        "nnz_A": problem.a.nnz, "settings": {"lambda_pcg": args.lambda_pcg},
-                       "parallelism": (f"rowshard{world}" if sharded else f"replicas{world}")
+                       "parallelism": (f"rowshard{world}-{args.transport}" if sharded else f"replicas{world}")
                                       if world > 1 else
                                       ("single" if args.shards <= 1 else f"virtual-rowshard{args.shards}"),
                        "l2": "inputs larger than L2 (A and A^T streams ~%.1f GB per PCG iteration)"

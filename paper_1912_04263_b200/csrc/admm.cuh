@@ -8,6 +8,7 @@
 #pragma once
 
 #include "spmv.cuh"
+#include "comm.cuh"
 
 namespace qpcg_b200 {
 
@@ -442,6 +443,29 @@ struct EpiPart {
   __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[NCOL]) const {
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) out[(size_t)r * NCOL + j] = s[j];
+  }
+};
+
+// The fused peer form of EpiPart: the row results go straight into this
+// block's slot on EVERY rank (NVLink P2P stores, overlapped with the SpMV),
+// so the reduction step is only a barrier and the ordered local sum.
+template <typename T, int NCOL>
+struct EpiPeer {
+  PeerPtrs dst;  // this block's slot in every rank's area
+  int R;
+  const Ctl<T>* ctl;
+  uint32_t gate;
+  __device__ __forceinline__ bool init() {
+    if (ctl->error) return false;
+    if (gate == 1) return ctl->pcg_active != 0;
+    return true;
+  }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[NCOL]) const {
+    for (int q = 0; q < R; ++q) {
+      T* o = reinterpret_cast<T*>(dst.p[q]) + (size_t)r * NCOL;
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) o[j] = s[j];
+    }
   }
 };
 

@@ -365,20 +365,11 @@ struct ShardComm {
       if (count > a.vcap) throw InvalidArgument("p2p: allreduce larger than the slots");
       ShardPtrs<T> src{};
       for (size_t l = 0; l < bufs.size(); ++l) src.p[l] = bufs[l];
-      const size_t set = a.off_vec + (a.parity & 1u) * a.vec_set();
-      a.parity ^= 1u;
       const uint32_t g = (uint32_t)std::min<size_t>((count + kThreads - 1) / kThreads, 4u * kNumSMs);
-      k_p2p_publish<T><<<g, kThreads, 0, s>>>(src, (int)bufs.size(), count, peers(set), a.R,
+      k_p2p_publish<T><<<g, kThreads, 0, s>>>(src, (int)bufs.size(), count, peers(p2p_set()), a.R,
                                                size_t(rank) * a.L * a.vec_slot(), a.vec_slot());
       CK_LAUNCH();
-      barrier();
-      if (max)
-        k_p2p_reduce<T, true><<<g, kThreads, 0, s>>>(a.mine + set, a.vec_slot(), a.G, count, src,
-                                                     (int)bufs.size());
-      else
-        k_p2p_reduce<T, false><<<g, kThreads, 0, s>>>(a.mine + set, a.vec_slot(), a.G, count, src,
-                                                      (int)bufs.size());
-      CK_LAUNCH();
+      p2p_reduce(bufs, count, max);
       return;
     }
     if (bufs.size() > 1) {
@@ -398,6 +389,31 @@ struct ShardComm {
       for (size_t l = 1; l < bufs.size(); ++l)
         CK(cudaMemcpyAsync(bufs[l], bufs[0], sizeof(T) * count, cudaMemcpyDeviceToDevice, s));
     }
+  }
+
+  // The fused form (the A^T SpMV epilogue stores its rows straight into every
+  // rank's slot): p2p_slot(l) is where local block l writes this time,
+  // p2p_reduce() then barriers and sums the G slots into bufs.
+  size_t p2p_set() const { return p2p->off_vec + (p2p->parity & 1u) * p2p->vec_set(); }
+  PeerPtrs p2p_slot(int l) const {
+    return peers(p2p_set() + (size_t(rank) * p2p->L + l) * p2p->vec_slot());
+  }
+  template <typename T>
+  void p2p_reduce(const std::vector<T*>& bufs, size_t count, bool max) {
+    P2PArea& a = *p2p;
+    ShardPtrs<T> out{};
+    for (size_t l = 0; l < bufs.size(); ++l) out.p[l] = bufs[l];
+    const size_t set = p2p_set();
+    a.parity ^= 1u;
+    barrier();
+    const uint32_t g = (uint32_t)std::min<size_t>((count + kThreads - 1) / kThreads, 4u * kNumSMs);
+    if (max)
+      k_p2p_reduce<T, true><<<g, kThreads, 0, s>>>(a.mine + set, a.vec_slot(), a.G, count, out,
+                                                   (int)bufs.size());
+    else
+      k_p2p_reduce<T, false><<<g, kThreads, 0, s>>>(a.mine + set, a.vec_slot(), a.G, count, out,
+                                                    (int)bufs.size());
+    CK_LAUNCH();
   }
 
   // min over every rank of one device-resident uint64 (validation keys)

@@ -222,14 +222,32 @@ class Sharded : public IEngine<T> {
   }
 
   // ------------------------------------------------------ loop pieces
+  // A^T pass of block w into the partial buffers, combined over all blocks:
+  // with the peer transport the epilogue stores into every rank's slot (the
+  // fused compute + collective), else EpiPart + the comm's allreduce.
+  template <int NCOL, class Gather>
+  void at_pass_combined(Workspace<T>& w, int li, const Gather& g, uint32_t gate) {
+    if (comm.p2p)
+      launch_spmv<T, NCOL, SumOp>(w.D.AT, w.D.pAT, g,
+                                  EpiPeer<T, NCOL>{comm.p2p_slot(li), comm.p2p->R, w.D.ctl, gate}, w.s);
+    else
+      launch_spmv<T, NCOL, SumOp>(w.D.AT, w.D.pAT, g, EpiPart<T, NCOL>{w.D.part, w.D.ctl, gate}, w.s);
+  }
+  void combine_parts(size_t count) {
+    if (comm.p2p)
+      comm.p2p_reduce(bufs<T>([](Workspace<T>& w) { return w.D.part; }), count, false);
+    else
+      allreduce_part(count);
+  }
+
   void enq_rhs() {
-    each([](Workspace<T>& w) {
+    int li = 0;
+    each([&](Workspace<T>& w) {
       k_pack_rhs<T><<<grid_for(w.D.m), kThreads, 0, w.s>>>(w.D);
       CK_LAUNCH();
-      launch_spmv<T, 2, SumOp>(w.D.AT, w.D.pAT, GatherRhs<T>{w.D.g2m},
-                               EpiPart<T, 2>{w.D.part, w.D.ctl, 0}, w.s);
+      at_pass_combined<2>(w, li++, GatherRhs<T>{w.D.g2m}, 0);
     });
-    allreduce_part(2 * size_t(n));
+    combine_parts(2 * size_t(n));
     each([](Workspace<T>& w) {
       k_rhs_finish<T><<<grid_for(w.D.n), kThreads, 0, w.s>>>(w.D);
       CK_LAUNCH();
@@ -237,12 +255,12 @@ class Sharded : public IEngine<T> {
     });
   }
   void enq_pcg_iter() {
-    each([](Workspace<T>& w) {
+    int li = 0;
+    each([&](Workspace<T>& w) {
       launch_spmv<T, 1, SumOp>(w.D.A, w.D.pA, GatherVec<T>{w.D.p}, EpiAp<T>{w.D.t, w.D.ctl, T(0)}, w.s);
-      launch_spmv<T, 1, SumOp>(w.D.AT, w.D.pAT, GatherVec<T>{w.D.t},
-                               EpiPart<T, 1>{w.D.part, w.D.ctl, 1}, w.s);
+      at_pass_combined<1>(w, li++, GatherVec<T>{w.D.t}, 1);
     });
-    allreduce_part(n);
+    combine_parts(n);
     each([](Workspace<T>& w) {
       k_pcg_dot<T><<<red_grid<T>(w.D.n), kThreads, 0, w.s>>>(w.D);
       CK_LAUNCH();
@@ -253,11 +271,9 @@ class Sharded : public IEngine<T> {
     });
   }
   void enq_check(int mode) {
-    each([](Workspace<T>& w) {
-      launch_spmv<T, 1, SumOp>(w.D.AT, w.D.pAT, GatherVec<T>{w.D.y},
-                               EpiPart<T, 1>{w.D.part, w.D.ctl, 0}, w.s);
-    });
-    allreduce_part(n);
+    int li = 0;
+    each([&](Workspace<T>& w) { at_pass_combined<1>(w, li++, GatherVec<T>{w.D.y}, 0); });
+    combine_parts(n);
     each([&](Workspace<T>& w) {
       k_dual_finish<T><<<grid_for(w.D.n), kThreads, 0, w.s>>>(w.D);
       CK_LAUNCH();
