@@ -167,7 +167,7 @@ def _views(arrs, n, m, dev):
 
 class Engine:
     def __init__(self, problem, settings, device, stream_ptr, dtype, mode, shards=1, nccl=None,
-                 transport="nccl"):
+                 transport="nccl", peer_dir=None):
         import torch
         from paper_1912_04263_b200 import _abi, solver
         self.lib = solver.load_library()
@@ -206,6 +206,11 @@ class Engine:
                 o.nccl_id = C.cast(self._id, C.c_void_p)
                 if transport == "peer":  # NCCL only bootstraps the IPC handles
                     o.transport = _abi.TRANSPORT_PEER
+            if peer_dir is not None:  # (rank, ranks, rendezvous directory)
+                self._dir = C.create_string_buffer(peer_dir[2].encode())
+                o.nccl_rank, o.nccl_ranks = peer_dir[0], peer_dir[1]
+                o.transport = _abi.TRANSPORT_PEER
+                o.rendezvous_dir = C.cast(self._dir, C.c_char_p)
             self.opts[memkind] = o
         self._abi = _abi
         self.msg = C.create_string_buffer(512)
@@ -406,17 +411,32 @@ def main():
         run_reference(args, rank)
         return
     import torch
+    # QPCG_BENCH_SAME_GPU=1: every rank on GPU 0 (a harness dry run of the
+    # multi-rank path on a one-GPU box: gloo for the host collectives, the
+    # engine's peer transport bootstrapped through a rendezvous directory)
+    same_gpu = os.environ.get("QPCG_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_1912_04263_b200 import generators, solver
     from paper_1912_04263_b200.problem import Settings
     dtype = np.float64 if args.dtype == "f64" else np.float32
     sharded = world > 1 and not args.replicas
     nccl = None
-    if sharded:  # one NCCL group for the engine, id shared over torch.distributed
+    rdir = None
+    if sharded and same_gpu:  # rendezvous directory instead of an NCCL id
+        import tempfile
+        obj = [tempfile.mkdtemp(prefix="qpcg_rdv_") if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        rdir = obj[0]
+    elif sharded:  # one NCCL group for the engine, id shared over torch.distributed
         obj = [solver.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl = (rank, world, obj[0])
@@ -428,7 +448,8 @@ def main():
     stream = torch.cuda.Stream(device=local)
     with torch.cuda.stream(stream):
         eng = Engine(problem, settings, local, stream.cuda_stream, dtype, args.mode,
-                     shards=args.shards, nccl=nccl, transport=args.transport)
+                     shards=args.shards, nccl=nccl, transport=args.transport,
+                     peer_dir=(rank, world, rdir) if rdir else None)
         for i in range(args.warmup):
             t = time.time()
             info = eng.solve("device")
@@ -468,7 +489,8 @@ def main():
         kt = eng.kernel_timing(args.kernel_reps)
         log(f"kernels: A {kt[0]:.4f} ms, A^T {kt[1]:.4f} ms, PCG iteration {kt[2]:.4f} ms")
     if dist is not None:
-        t = torch.tensor([ms, ms_e2e], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([ms, ms_e2e], device="cpu" if same_gpu else f"cuda:{local}",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, ms_e2e = float(t[0]), float(t[1])
     if rank != 0:

@@ -16,6 +16,7 @@
 #pragma once
 
 #include <dlfcn.h>
+#include <sys/stat.h>
 #include <nccl.h>  // types and enums only: every symbol is resolved through dlopen
 
 #include <chrono>
@@ -287,7 +288,18 @@ struct ShardComm {
       for (int i = 0; i < R; ++i) all[i] = buf.substr(i * sizeof(h), sizeof(h));
     } else {
       if (!dir) throw InvalidArgument("options: the peer transport needs an NCCL id or a rendezvous directory");
-      p2p_exchange_file(dir, r, R, &h, sizeof(h), all);
+      // one fresh subdirectory per setup of the group (every rank sets up the
+      // same sequence of workspaces, so the counters agree)
+      static std::mutex gmu;
+      static std::map<std::string, int> generation;
+      int k = 0;
+      {
+        std::lock_guard<std::mutex> lock(gmu);
+        k = generation[dir]++;
+      }
+      const std::string sub = std::string(dir) + "/g" + std::to_string(k);
+      mkdir(sub.c_str(), 0700);  // EEXIST from the other ranks is fine
+      p2p_exchange_file(sub, r, R, &h, sizeof(h), all);
     }
     a->peer.assign(R, nullptr);
     for (int i = 0; i < R; ++i) {
