@@ -451,18 +451,22 @@ struct EpiPart {
 // so the reduction step is only a barrier and the ordered local sum.
 template <typename T, int NCOL>
 struct EpiPeer {
-  PeerPtrs dst;  // this block's slot in every rank's area
+  PeerPtrs dst;  // this block's slot (set 0) in every rank's area
   int R;
   const Ctl<T>* ctl;
   uint32_t gate;
+  size_t set_bytes;
+  const unsigned long long* epoch;  // this rank's barrier epoch: its parity picks the set
+  size_t set;
   __device__ __forceinline__ bool init() {
     if (ctl->error) return false;
+    set = (p2p_epoch(epoch) & 1ull) * set_bytes;
     if (gate == 1) return ctl->pcg_active != 0;
     return true;
   }
   __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[NCOL]) const {
     for (int q = 0; q < R; ++q) {
-      T* o = reinterpret_cast<T*>(dst.p[q]) + (size_t)r * NCOL;
+      T* o = reinterpret_cast<T*>(dst.p[q] + set) + (size_t)r * NCOL;
 #pragma unroll
       for (int j = 0; j < NCOL; ++j) o[j] = s[j];
     }

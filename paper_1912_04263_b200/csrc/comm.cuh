@@ -138,34 +138,52 @@ struct PeerPtrs {
   char* p[kMaxLocalShards];
 };
 
+// The barrier epoch (this rank's count of barriers, in its own area) is kept
+// on the device, and the slot set of an allreduce is its parity before the
+// barrier: no host state changes between collectives, so the whole loop can
+// be captured into a CUDA graph (the set alternates every replay).
+__device__ __forceinline__ unsigned long long p2p_epoch(const unsigned long long* e) {
+  return *reinterpret_cast<const volatile unsigned long long*>(e);
+}
+
+// dst.p[r] = rank r's first slot set; set 1 starts set_bytes later
 template <typename T>
 __global__ void k_p2p_publish(ShardPtrs<T> src, int L, size_t count, PeerPtrs dst, int R,
-                              size_t off_bytes, size_t slot_bytes) {
+                              size_t off_bytes, size_t slot_bytes, size_t set_bytes,
+                              const unsigned long long* epoch) {
+  const size_t set = (p2p_epoch(epoch) & 1ull) * set_bytes;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
        i += (size_t)gridDim.x * blockDim.x) {
     for (int l = 0; l < L; ++l) {
       const T v = src.p[l][i];
       for (int r = 0; r < R; ++r)
-        reinterpret_cast<T*>(dst.p[r] + off_bytes + l * slot_bytes)[i] = v;
+        reinterpret_cast<T*>(dst.p[r] + set + off_bytes + l * slot_bytes)[i] = v;
     }
   }
 }
 
-// one thread: fence, arrive at every rank's counter, wait for my counter
-static __global__ void k_p2p_barrier(PeerPtrs area, int R, int rank, unsigned long long target) {
+// one thread: fence, arrive at every rank's counter (area offset 0), bump
+// this rank's epoch (offset 8), wait until every rank arrived this epoch
+static __global__ void k_p2p_barrier(PeerPtrs area, int R, int rank) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   __threadfence_system();
   for (int r = 0; r < R; ++r)
     atomicAdd_system(reinterpret_cast<unsigned long long*>(area.p[r]), 1ull);
+  unsigned long long* ep = reinterpret_cast<unsigned long long*>(area.p[rank] + 8);
+  const unsigned long long e = *ep + 1ull;
+  *ep = e;
   const volatile unsigned long long* mine =
       reinterpret_cast<const volatile unsigned long long*>(area.p[rank]);
-  while (*mine < target) __nanosleep(200);
+  while (*mine < e * (unsigned long long)R) __nanosleep(200);
   __threadfence_system();
 }
 
+// after the barrier: the set of the epoch just closed
 template <typename T, bool MAX>
-__global__ void k_p2p_reduce(const char* slots, size_t slot_bytes, int G, size_t count,
-                             ShardPtrs<T> out, int L) {
+__global__ void k_p2p_reduce(const char* slots0, size_t slot_bytes, size_t set_bytes, int G,
+                             size_t count, ShardPtrs<T> out, int L,
+                             const unsigned long long* epoch) {
+  const char* slots = slots0 + ((p2p_epoch(epoch) - 1ull) & 1ull) * set_bytes;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
        i += (size_t)gridDim.x * blockDim.x) {
     T a = __ldcv(reinterpret_cast<const T*>(slots) + i);
@@ -194,8 +212,6 @@ struct P2PArea {
   size_t bytes = 0, vcap = 0, m = 0, n = 0;
   size_t off_vec = 0, off_u64 = 0, off_gbuf = 0, off_chain = 0;  // (flags at 0)
   std::vector<char*> peer;
-  unsigned long long epoch = 0;  // barriers so far (identical on every rank)
-  uint32_t parity = 0;           // slot set of the next allreduce
   size_t vec_slot() const { return vcap * 8; }
   size_t vec_set() const { return vec_slot() * G; }
 };
@@ -333,9 +349,11 @@ struct ShardComm {
     return pp;
   }
   void barrier() {
-    p2p->epoch += 1;
-    k_p2p_barrier<<<1, 32, 0, s>>>(peers(0), p2p->R, p2p->rank, p2p->epoch * p2p->R);
+    k_p2p_barrier<<<1, 32, 0, s>>>(peers(0), p2p->R, p2p->rank);
     CK_LAUNCH();
+  }
+  const unsigned long long* dev_epoch() const {
+    return reinterpret_cast<const unsigned long long*>(p2p->mine + 8);
   }
 
   int global_count() const { return local * nranks; }
@@ -378,8 +396,9 @@ struct ShardComm {
       ShardPtrs<T> src{};
       for (size_t l = 0; l < bufs.size(); ++l) src.p[l] = bufs[l];
       const uint32_t g = (uint32_t)std::min<size_t>((count + kThreads - 1) / kThreads, 4u * kNumSMs);
-      k_p2p_publish<T><<<g, kThreads, 0, s>>>(src, (int)bufs.size(), count, peers(p2p_set()), a.R,
-                                               size_t(rank) * a.L * a.vec_slot(), a.vec_slot());
+      k_p2p_publish<T><<<g, kThreads, 0, s>>>(src, (int)bufs.size(), count, peers(a.off_vec), a.R,
+                                               size_t(rank) * a.L * a.vec_slot(), a.vec_slot(),
+                                               a.vec_set(), dev_epoch());
       CK_LAUNCH();
       p2p_reduce(bufs, count, max);
       return;
@@ -406,25 +425,24 @@ struct ShardComm {
   // The fused form (the A^T SpMV epilogue stores its rows straight into every
   // rank's slot): p2p_slot(l) is where local block l writes this time,
   // p2p_reduce() then barriers and sums the G slots into bufs.
-  size_t p2p_set() const { return p2p->off_vec + (p2p->parity & 1u) * p2p->vec_set(); }
+  // block l's slot in set 0 of every rank's area (set 1: + vec_set(); the
+  // epilogue picks the set from the device epoch)
   PeerPtrs p2p_slot(int l) const {
-    return peers(p2p_set() + (size_t(rank) * p2p->L + l) * p2p->vec_slot());
+    return peers(p2p->off_vec + (size_t(rank) * p2p->L + l) * p2p->vec_slot());
   }
   template <typename T>
   void p2p_reduce(const std::vector<T*>& bufs, size_t count, bool max) {
     P2PArea& a = *p2p;
     ShardPtrs<T> out{};
     for (size_t l = 0; l < bufs.size(); ++l) out.p[l] = bufs[l];
-    const size_t set = p2p_set();
-    a.parity ^= 1u;
     barrier();
     const uint32_t g = (uint32_t)std::min<size_t>((count + kThreads - 1) / kThreads, 4u * kNumSMs);
     if (max)
-      k_p2p_reduce<T, true><<<g, kThreads, 0, s>>>(a.mine + set, a.vec_slot(), a.G, count, out,
-                                                   (int)bufs.size());
+      k_p2p_reduce<T, true><<<g, kThreads, 0, s>>>(a.mine + a.off_vec, a.vec_slot(), a.vec_set(),
+                                                   a.G, count, out, (int)bufs.size(), dev_epoch());
     else
-      k_p2p_reduce<T, false><<<g, kThreads, 0, s>>>(a.mine + set, a.vec_slot(), a.G, count, out,
-                                                    (int)bufs.size());
+      k_p2p_reduce<T, false><<<g, kThreads, 0, s>>>(a.mine + a.off_vec, a.vec_slot(), a.vec_set(),
+                                                    a.G, count, out, (int)bufs.size(), dev_epoch());
     CK_LAUNCH();
   }
 

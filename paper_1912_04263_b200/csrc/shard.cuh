@@ -45,6 +45,8 @@ class Sharded : public IEngine<T> {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   ~Sharded() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
     comm.free_p2p();  // a collective: every rank tears down together
     sh.clear();  // blocks free their buffers on the shared stream
     if (full_m) {
@@ -229,7 +231,9 @@ class Sharded : public IEngine<T> {
   void at_pass_combined(Workspace<T>& w, int li, const Gather& g, uint32_t gate) {
     if (comm.p2p)
       launch_spmv<T, NCOL, SumOp>(w.D.AT, w.D.pAT, g,
-                                  EpiPeer<T, NCOL>{comm.p2p_slot(li), comm.p2p->R, w.D.ctl, gate}, w.s);
+                                  EpiPeer<T, NCOL>{comm.p2p_slot(li), comm.p2p->R, w.D.ctl, gate,
+                                                   comm.p2p->vec_set(), comm.dev_epoch(), 0},
+                                  w.s);
     else
       launch_spmv<T, NCOL, SumOp>(w.D.AT, w.D.pAT, g, EpiPart<T, NCOL>{w.D.part, w.D.ctl, gate}, w.s);
   }
@@ -240,7 +244,7 @@ class Sharded : public IEngine<T> {
       allreduce_part(count);
   }
 
-  void enq_rhs() {
+  void enq_rhs(Handles H = {}) {
     int li = 0;
     each([&](Workspace<T>& w) {
       k_pack_rhs<T><<<grid_for(w.D.m), kThreads, 0, w.s>>>(w.D);
@@ -248,29 +252,29 @@ class Sharded : public IEngine<T> {
       at_pass_combined<2>(w, li++, GatherRhs<T>{w.D.g2m}, 0);
     });
     combine_parts(2 * size_t(n));
-    each([](Workspace<T>& w) {
+    each([&](Workspace<T>& w) {
       k_rhs_finish<T><<<grid_for(w.D.n), kThreads, 0, w.s>>>(w.D);
       CK_LAUNCH();
-      w.enq_pcg_init(Handles{});
+      w.enq_pcg_init(H);
     });
   }
-  void enq_pcg_iter() {
+  void enq_pcg_iter(Handles H = {}) {
     int li = 0;
     each([&](Workspace<T>& w) {
       launch_spmv<T, 1, SumOp>(w.D.A, w.D.pA, GatherVec<T>{w.D.p}, EpiAp<T>{w.D.t, w.D.ctl, T(0)}, w.s);
       at_pass_combined<1>(w, li++, GatherVec<T>{w.D.t}, 1);
     });
     combine_parts(n);
-    each([](Workspace<T>& w) {
+    each([&](Workspace<T>& w) {
       k_pcg_dot<T><<<red_grid<T>(w.D.n), kThreads, 0, w.s>>>(w.D);
       CK_LAUNCH();
-      k_pcg_update<T><<<red_grid<T>(w.D.n), kThreads, 0, w.s>>>(w.D, Handles{});
+      k_pcg_update<T><<<red_grid<T>(w.D.n), kThreads, 0, w.s>>>(w.D, H);
       CK_LAUNCH();
       k_pcg_pupdate<T><<<grid_for(w.D.n), kThreads, 0, w.s>>>(w.D);
       CK_LAUNCH();
     });
   }
-  void enq_check(int mode) {
+  void enq_check(int mode, Handles H = {}) {
     int li = 0;
     each([&](Workspace<T>& w) { at_pass_combined<1>(w, li++, GatherVec<T>{w.D.y}, 0); });
     combine_parts(n);
@@ -282,7 +286,7 @@ class Sharded : public IEngine<T> {
     });
     allreduce_scal(14, true);
     each([&](Workspace<T>& w) {
-      k_residuals_decide<T><<<1, 32, 0, w.s>>>(w.D, mode, Handles{});
+      k_residuals_decide<T><<<1, 32, 0, w.s>>>(w.D, mode, H);
       CK_LAUNCH();
     });
   }
@@ -328,7 +332,7 @@ class Sharded : public IEngine<T> {
   }
   void enq_rho() {
     each([](Workspace<T>& w) {
-      w.enq_rho_flag(Handles{});
+      w.enq_rho_flag(Handles{});  // (no IF node: the rho kernels gate themselves)
       k_rho<T><<<red_grid<T>(w.D.m), kThreads, 0, w.s>>>(w.D);
       CK_LAUNCH();
     });
@@ -341,6 +345,73 @@ class Sharded : public IEngine<T> {
     });
   }
 
+  // ------------------------------------------------- device-driven loop
+  // The same sequence as the host loop below as one CUDA graph with
+  // conditional WHILE / IF nodes: the decisions come from the (identical)
+  // control blocks of the row blocks, the collectives are kernels (local
+  // combine, peer stores, device barriers), so nothing returns to the host
+  // until the solve ends.  Not with the NCCL transport.
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool graph_ok() const { return opt.mode == QPCG_MODE_GRAPH && (comm.p2p || !comm.comm); }
+  cudaGraph_t add_cond(cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = type;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, deps, nd, &cp));
+    CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+    return cp.conditional.phGraph_out[0];
+  }
+  void build_graph() {
+    CK(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h_admm, h_pcg, h_chk, h_inf;
+    CK(cudaGraphConditionalHandleCreate(&h_admm, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h_admm;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t n_admm;
+    CK(cudaGraphAddNode(&n_admm, graph, nullptr, 0, &cp));
+    cudaGraph_t b_admm = cp.conditional.phGraph_out[0];
+    CK(cudaGraphConditionalHandleCreate(&h_pcg, b_admm, 0, cudaGraphCondAssignDefault));
+    CK(cudaGraphConditionalHandleCreate(&h_chk, b_admm, 0, cudaGraphCondAssignDefault));
+    Handles H;
+    H.admm = (unsigned long long)h_admm;
+    H.pcg = (unsigned long long)h_pcg;
+    H.chk = (unsigned long long)h_chk;
+    cudaGraph_t b_pcg, b_chk, b_inf, g_out;
+    CK(cudaStreamBeginCaptureToGraph(s, b_admm, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    enq_rhs(H);
+    b_pcg = add_cond(h_pcg, cudaGraphCondTypeWhile);
+    each([&](Workspace<T>& w) { w.enq_post_pcg(H); });
+    b_chk = add_cond(h_chk, cudaGraphCondTypeIf);
+    enq_rho();
+    each([&](Workspace<T>& w) { w.enq_admm_cond(H); });
+    CK(cudaStreamEndCapture(s, &g_out));
+    CK(cudaStreamBeginCaptureToGraph(s, b_pcg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    enq_pcg_iter(H);
+    CK(cudaStreamEndCapture(s, &g_out));
+    CK(cudaGraphConditionalHandleCreate(&h_inf, b_chk, 0, cudaGraphCondAssignDefault));
+    H.inf = (unsigned long long)h_inf;
+    CK(cudaStreamBeginCaptureToGraph(s, b_chk, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    enq_check(0, H);
+    b_inf = add_cond(h_inf, cudaGraphCondTypeIf);
+    CK(cudaStreamEndCapture(s, &g_out));
+    CK(cudaStreamBeginCaptureToGraph(s, b_inf, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    enq_infeas();
+    CK(cudaStreamEndCapture(s, &g_out));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+  }
+
   // ------------------------------------------------------------ solve
   void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) override {
     CK(cudaSetDevice(device));
@@ -351,7 +422,11 @@ class Sharded : public IEngine<T> {
     const uint64_t l0 = g_launches;
     Workspace<T>& W = w0();
     enq_residuals_fresh(1);  // solver.hpp:436-441
-    for (;;) {
+    if (graph_ok()) {
+      if (!exec) build_graph();
+      CK(cudaGraphLaunch(exec, s));
+    }
+    for (; !graph_ok();) {
       W.pull_ctl();
       if (W.hc.done || W.hc.error || W.hc.iter >= W.hc.max_iter) break;
       enq_rhs();
@@ -410,7 +485,13 @@ class Sharded : public IEngine<T> {
       });
       info->h2d_bytes = h2d;
       info->h2d_seconds = h2ds;
-      info->kernel_launches = (g_launches - l0) + (have_counted_setup ? 0 : setup_launches);
+      uint64_t launches = g_launches - l0;
+      if (graph_ok()) {  // kernels executed inside the graph (per block L, per combine c)
+        const uint64_t L = comm.local, c = comm.p2p ? 3 : (L > 1 ? 1 : 0);
+        launches += W.hc.iter * (L * 10 + 2 * c) + W.hc.pcg_total * (L * 5 + c) +
+                    uint64_t(W.hc.n_checks) * (L * 3 + 2 * c) + uint64_t(W.hc.n_inf) * (L * 8 + 3 * c);
+      }
+      info->kernel_launches = launches + (have_counted_setup ? 0 : setup_launches);
     }
     have_counted_setup = true;
   }

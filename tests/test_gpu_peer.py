@@ -18,21 +18,21 @@ pytestmark = pytest.mark.gpu
 S = Settings(lambda_pcg=0.01)
 
 
-def _rank(rank, ranks, local, rdir, cls, scale, q):
+def _rank(rank, ranks, local, rdir, cls, scale, q, mode="graph"):
     try:
         p = G.generate(cls, scale, 0)
-        r = solver.solve(p, S, device=0, shards=local, peer=(rank, ranks, rdir))
+        r = solver.solve(p, S, device=0, shards=local, peer=(rank, ranks, rdir), mode=mode)
         q.put((rank, r.status, r.iterations, r.pcg_iterations_total, r.x, r.z, r.y, r.objective,
                r.info["kernel_launches"]))
     except Exception as e:  # reported to the parent
         q.put((rank, "exception", repr(e)))
 
 
-def run_ranks(ranks, local, cls, scale):
+def run_ranks(ranks, local, cls, scale, mode="graph"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     with tempfile.TemporaryDirectory() as rdir:
-        procs = [ctx.Process(target=_rank, args=(r, ranks, local, rdir, cls, scale, q))
+        procs = [ctx.Process(target=_rank, args=(r, ranks, local, rdir, cls, scale, q, mode))
                  for r in range(ranks)]
         for pr in procs:
             pr.start()
@@ -49,10 +49,13 @@ def run_ranks(ranks, local, cls, scale):
     return out
 
 
-@pytest.mark.parametrize("cls,scale,ranks,local", [("lasso", 4, 2, 1), ("huber", 3, 2, 2),
-                                                   ("svm", 3, 2, 1)])
-def test_peer_transport_two_processes_bitwise_equal_virtual(cls, scale, ranks, local):
-    out = run_ranks(ranks, local, cls, scale)
+@pytest.mark.parametrize("cls,scale,ranks,local,mode", [("lasso", 4, 2, 1, "graph"),
+                                                        ("huber", 3, 2, 2, "graph"),
+                                                        ("svm", 3, 2, 1, "eager")])
+def test_peer_transport_two_processes_bitwise_equal_virtual(cls, scale, ranks, local, mode):
+    """mode graph: the whole sharded loop as one CUDA graph per process, the
+    peer stores / device barriers inside it; eager: the host-driven loop."""
+    out = run_ranks(ranks, local, cls, scale, mode)
     for r in range(ranks):
         assert out[r][1] != "exception", out[r]
     p = G.generate(cls, scale, 0)

@@ -143,3 +143,15 @@ def test_sharded_warm_start_matches_oracle():
     ow = O.oracle_solve(p, S, warm=w)
     assert g.status == ow.status == "solved"
     assert rel(g.objective, ow.objective) < 1e-3
+
+
+@pytest.mark.parametrize("cls", ["lasso", "huber", "portfolio"])
+def test_sharded_graph_equals_host_loop(cls):
+    """The device-driven sharded loop (one CUDA graph, conditional nodes) is
+    bitwise identical to the host-driven one."""
+    p = G.generate(cls, 5, 0)
+    a = solver.solve(p, S, device=0, shards=3, mode="graph")
+    b = solver.solve(p, S, device=0, shards=3, mode="eager")
+    assert a.status == b.status and a.iterations == b.iterations
+    assert a.pcg_iterations_total == b.pcg_iterations_total
+    assert np.array_equal(a.x, b.x) and np.array_equal(a.z, b.z) and np.array_equal(a.y, b.y)
