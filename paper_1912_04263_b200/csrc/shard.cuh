@@ -44,16 +44,18 @@ class Sharded : public IEngine<T> {
   T* full_m = nullptr;  // gather buffer [m]
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
+  Arena arena;  // the transient setup buffers of all blocks (one shared stream)
   ~Sharded() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     comm.free_p2p();  // a collective: every rank tears down together
     sh.clear();  // blocks free their buffers on the shared stream
     if (full_m) {
-      AllocScope scope(s);
+      AllocScope scope(s, &arena);
       dfree(full_m);
-      cudaStreamSynchronize(s);
     }
+    if (s) cudaStreamSynchronize(s);
+    arena.return_all();
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (s && own_stream) cudaStreamDestroy(s);
@@ -146,7 +148,7 @@ class Sharded : public IEngine<T> {
       w.D.sh_index = g;
       w.D.sh_count = G;
       w.begin(st, op, s);
-      AllocScope scope(s);
+      AllocScope scope(s, &arena);
       if (balanced)
         w.load(Pu, q, A, l, u, cuts[g], cuts[g + 1], true);
       else if (g == 0)  // invalid row_ptr: block 0 sees A exactly as given
@@ -178,7 +180,7 @@ class Sharded : public IEngine<T> {
       if (!w.a_cols_ok) throw InvalidArgument("problem: A column count must equal n");
       if (v.k[2] != ~0ull) throw InvalidArgument(validation_message(v.k[2]));
     }
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     each([](Workspace<T>& w) { w.build_structures(); });
     // ---- Ruiz with the two maxima combined across blocks
     uint32_t passes = 0;
@@ -415,7 +417,7 @@ class Sharded : public IEngine<T> {
   // ------------------------------------------------------------ solve
   void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) override {
     CK(cudaSetDevice(device));
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     const double w0s = now_s();
     CK(cudaEventRecord(ev0, s));
     each([](Workspace<T>& w) { w.reset_solve_state(); });
@@ -535,7 +537,7 @@ class Sharded : public IEngine<T> {
   // --------------------------------------------------- OSQP-style updates
   void warm_start(const T* x, const T* z, const T* y) override {
     CK(cudaSetDevice(device));
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     std::vector<unsigned long long> keys;
     each([&](Workspace<T>& w) { keys.push_back(w.warm_stage(x, z + w.row0, y + w.row0)); });
     if (agree_min(keys) != ~0ull) throw InvalidArgument("solve: warm start must be finite");
@@ -546,7 +548,7 @@ class Sharded : public IEngine<T> {
   }
   void update_vectors(const T* q, const T* l, const T* u) override {
     CK(cudaSetDevice(device));
-    AllocScope scope(s);
+    AllocScope scope(s, &arena);
     std::vector<unsigned long long> keys;
     each([&](Workspace<T>& w) {
       keys.push_back(w.vectors_stage(q, l ? l + w.row0 : nullptr, u ? u + w.row0 : nullptr));
