@@ -155,3 +155,14 @@ def test_sharded_graph_equals_host_loop(cls):
     assert a.status == b.status and a.iterations == b.iterations
     assert a.pcg_iterations_total == b.pcg_iterations_total
     assert np.array_equal(a.x, b.x) and np.array_equal(a.z, b.z) and np.array_equal(a.y, b.y)
+
+
+def test_peer_transport_nccl_bootstrap_single_rank():
+    """The peer transport bootstrapped over NCCL (ncclAllGather of the IPC
+    handles), one rank x 2 blocks: bitwise equal to the 2 virtual blocks."""
+    uid = solver.nccl_unique_id()
+    p = G.generate("control", 5, 0)
+    g = solver.solve(p, S, device=0, shards=2, nccl=(0, 1, uid), peer=(0, 1, None))
+    v = solver.solve(p, S, device=0, shards=2)
+    assert g.status == v.status and g.iterations == v.iterations
+    assert np.array_equal(g.x, v.x) and np.array_equal(g.z, v.z)
