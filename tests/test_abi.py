@@ -105,3 +105,22 @@ def test_settings_json_loader():
     assert s.lambda_pcg == 0.01 and s.max_admm_iter == 10 and s.alpha == 1.6
     with pytest.raises(RuntimeError, match="unknown key"):
         Settings.from_json('{"lambda": 0.01}')  # io.hpp:201
+
+
+def test_null_and_wrong_precision_arguments_fail_cleanly():
+    """Argument errors surface as return codes + messages, with no GPU needed."""
+    lib = solver.load_library()
+    ws = C.c_void_p()
+    s = _abi.default_settings()
+    rc = lib.qpcg_f64_setup(C.byref(ws), None, None, None, None, None, C.byref(s), None)
+    assert rc == _abi.QPCG_ERR_INVALID and not ws.value
+    assert b"null" in lib.qpcg_last_error(None)
+    lib.qpcg_cleanup(None)  # no-op
+    assert lib.qpcg_get_pcg_calls(None, None, 0) == 0
+    assert lib.qpcg_get_rho_updates(None, None, 0) == 0
+    assert lib.qpcg_get_check_iterations(None, None, 0) == 0
+    lib.qpcg_f64_update_rho.argtypes = [C.c_void_p, C.c_double]
+    assert lib.qpcg_f64_update_rho(None, 1.0) == _abi.QPCG_ERR_INVALID
+    lib.qpcg_shard_cuts.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p]
+    assert lib.qpcg_shard_cuts(None, 3, 3, 2, None) == 0
+    assert lib.qpcg_validate_settings(C.byref(s), None, 0) == 0
