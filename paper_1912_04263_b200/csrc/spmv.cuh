@@ -212,28 +212,46 @@ __device__ __forceinline__ void spmv_item(const DevCsr<T>& M, const SpmvPlan<T>&
                                                                   CMP ? P.c0[it] : 0u, lane, acc);
 #pragma unroll
   for (int j = 0; j < NCOL; ++j) acc[j] = Op::warp(acc[j]);
-  if (lane != 0) return;
   if (item.lr == 0xffffffffu) {
-    epi(item.row, acc);
+    if (lane == 0) epi(item.row, acc);
     return;
   }
+  // publish the partial; the release/acquire counter increment orders it
+  // before the last arriver's reads
+  uint32_t prev = 0;
   const uint2 info = P.lrinfo[item.lr];
-  const uint32_t chunk = (item.beg - M.rp[item.row]) / kChunk;
-  T* part = P.partials + (size_t)(info.x + chunk) * kMaxCols;
+  if (lane == 0) {
+    const uint32_t chunk = (item.beg - M.rp[item.row]) / kChunk;
+    T* part = P.partials + (size_t)(info.x + chunk) * kMaxCols;
 #pragma unroll
-  for (int j = 0; j < NCOL; ++j) part[j] = acc[j];
-  __threadfence();
-  const uint32_t prev = atomicAdd(P.counters + item.lr, 1u);
+    for (int j = 0; j < NCOL; ++j) part[j] = acc[j];
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(prev) : "l"(P.counters + item.lr) : "memory");
+  }
+  prev = __shfl_sync(0xffffffffu, prev, 0);
   if (prev != info.y - 1) return;
-  __threadfence();
+  __syncwarp();
+  // last arriver: the lanes load the partials in parallel, lane 0 joins them
+  // in item order (the same order as a sequential loop: bitwise stable)
   T tot[NCOL];
 #pragma unroll
   for (int j = 0; j < NCOL; ++j) tot[j] = T(0);
-  for (uint32_t q = 0; q < info.y; ++q) {
+  for (uint32_t q0 = 0; q0 < info.y; q0 += 32) {
+    T pv[NCOL];
+    const uint32_t q = q0 + lane;
     const T* pp = P.partials + (size_t)(info.x + q) * kMaxCols;
 #pragma unroll
-    for (int j = 0; j < NCOL; ++j) tot[j] = Op::join(tot[j], __ldcg(pp + j));
+    for (int j = 0; j < NCOL; ++j) pv[j] = q < info.y ? __ldcg(pp + j) : T(0);
+    const uint32_t cnt = min(32u, info.y - q0);
+    for (uint32_t t = 0; t < cnt; ++t) {
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) {
+        const T v = __shfl_sync(0xffffffffu, pv[j], t);
+        tot[j] = Op::join(tot[j], v);
+      }
+    }
   }
+  if (lane != 0) return;
   P.counters[item.lr] = 0u;
   epi(item.row, tot);
 }
