@@ -196,20 +196,11 @@ __device__ __forceinline__ void item_loop(const DevCsr<T>& M, const SpmvPlan<T>&
 }
 
 // --------------------------------------------------------------- kernel
-// One work item (one warp; lane 0 runs the epilogue).  Multi-item rows
-// publish a partial; the last item to arrive combines them in item order
-// (deterministic).
-template <typename T, int NCOL, class Op, class Gather, class Epi, int U, bool CMP,
-          bool L1 = false>
-__device__ __forceinline__ void spmv_item(const DevCsr<T>& M, const SpmvPlan<T>& P,
-                                          const Gather& gather, const Epi& epi, uint32_t it,
-                                          uint32_t lane) {
-  const WorkItem item = P.items[it];
-  T acc[NCOL];
-#pragma unroll
-  for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
-  item_loop<T, NCOL, Op, Gather, U, CMP && Op::kNeedsGather, L1>(M, P, gather, item,
-                                                                  CMP ? P.c0[it] : 0u, lane, acc);
+// End of a work item: warp-reduce the lane sums, then the epilogue (single
+// item) or the deterministic combine of a multi-item row.
+template <typename T, int NCOL, class Op, class Epi>
+__device__ __forceinline__ void item_finish(const DevCsr<T>& M, const SpmvPlan<T>& P, const Epi& epi,
+                                            const WorkItem& item, uint32_t lane, T (&acc)[NCOL]) {
 #pragma unroll
   for (int j = 0; j < NCOL; ++j) acc[j] = Op::warp(acc[j]);
   if (item.lr == 0xffffffffu) {
@@ -254,6 +245,23 @@ __device__ __forceinline__ void spmv_item(const DevCsr<T>& M, const SpmvPlan<T>&
   if (lane != 0) return;
   P.counters[item.lr] = 0u;
   epi(item.row, tot);
+}
+
+// One work item (one warp; lane 0 runs the epilogue).  Multi-item rows
+// publish a partial; the last item to arrive combines them in item order
+// (deterministic).
+template <typename T, int NCOL, class Op, class Gather, class Epi, int U, bool CMP,
+          bool L1 = false>
+__device__ __forceinline__ void spmv_item(const DevCsr<T>& M, const SpmvPlan<T>& P,
+                                          const Gather& gather, const Epi& epi, uint32_t it,
+                                          uint32_t lane) {
+  const WorkItem item = P.items[it];
+  T acc[NCOL];
+#pragma unroll
+  for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
+  item_loop<T, NCOL, Op, Gather, U, CMP && Op::kNeedsGather, L1>(M, P, gather, item,
+                                                                  CMP ? P.c0[it] : 0u, lane, acc);
+  item_finish<T, NCOL, Op, Epi>(M, P, epi, item, lane, acc);
 }
 
 // One short row (<= kShortRowMax nnz), one thread, left to right: bit-exact.
