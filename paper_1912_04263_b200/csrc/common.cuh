@@ -212,7 +212,10 @@ constexpr int kNumSMs = 148;           // B200
 constexpr int kThreads = 256;          // default block size
 constexpr int kWarpsPerBlock = kThreads / 32;
 constexpr uint32_t kShortRowMax = 8;   // rows with <= 8 nnz: one thread per row
-constexpr uint32_t kChunk = 2048;      // nnz per warp work item (long rows split)
+#ifndef QPCG_CHUNK
+#define QPCG_CHUNK 4096
+#endif
+constexpr uint32_t kChunk = QPCG_CHUNK;  // nnz per warp work item (long rows split)
 constexpr int kRedBlocks = 2 * kNumSMs;  // fixed grid of reduction kernels (deterministic)
 
 __host__ __device__ inline uint32_t ceil_div(uint32_t a, uint32_t b) { return (a + b - 1) / b; }

@@ -252,16 +252,22 @@ __device__ __forceinline__ void item_finish(const DevCsr<T>& M, const SpmvPlan<T
 // (deterministic).
 template <typename T, int NCOL, class Op, class Gather, class Epi, int U, bool CMP,
           bool L1 = false>
-__device__ __forceinline__ void spmv_item(const DevCsr<T>& M, const SpmvPlan<T>& P,
-                                          const Gather& gather, const Epi& epi, uint32_t it,
-                                          uint32_t lane) {
-  const WorkItem item = P.items[it];
+__device__ __forceinline__ void spmv_item_run(const DevCsr<T>& M, const SpmvPlan<T>& P,
+                                              const Gather& gather, const Epi& epi,
+                                              const WorkItem& item, uint32_t c0, uint32_t lane) {
   T acc[NCOL];
 #pragma unroll
   for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
-  item_loop<T, NCOL, Op, Gather, U, CMP && Op::kNeedsGather, L1>(M, P, gather, item,
-                                                                  CMP ? P.c0[it] : 0u, lane, acc);
+  item_loop<T, NCOL, Op, Gather, U, CMP && Op::kNeedsGather, L1>(M, P, gather, item, c0, lane, acc);
   item_finish<T, NCOL, Op, Epi>(M, P, epi, item, lane, acc);
+}
+template <typename T, int NCOL, class Op, class Gather, class Epi, int U, bool CMP,
+          bool L1 = false>
+__device__ __forceinline__ void spmv_item(const DevCsr<T>& M, const SpmvPlan<T>& P,
+                                          const Gather& gather, const Epi& epi, uint32_t it,
+                                          uint32_t lane) {
+  spmv_item_run<T, NCOL, Op, Gather, Epi, U, CMP, L1>(M, P, gather, epi, P.items[it],
+                                                      CMP ? P.c0[it] : 0u, lane);
 }
 
 // One short row (<= kShortRowMax nnz), one thread, left to right: bit-exact.
@@ -287,6 +293,10 @@ __device__ __forceinline__ void spmv_short(const DevCsr<T>& M, const SpmvPlan<T>
 // kernels rather than branches): U = 8 strides in flight with the compressed
 // index for plans of long items (the latency-bound streams of A / A^T), and
 // U = 4 with uint32 columns for plans of short items, where occupancy wins.
+// One item per warp, blocks handed out in item order by the hardware: a
+// grid-stride walk of resident warps over the items (descriptor prefetch)
+// measured 1.6x slower on the lasso A pass — the warps drift apart and the
+// in-flight rows stop sharing column windows and DRAM pages.
 template <typename T, int NCOL, class Op, class Gather, class Epi, int U, bool CMP>
 __global__ void __launch_bounds__(kThreads) spmv_kernel(DevCsr<T> M, SpmvPlan<T> P, Gather gather,
                                                        Epi epi) {
