@@ -4,7 +4,8 @@
 
 * libqpcg_b200.so : CUDA engine + C-ABI, sm_100a only, --fmad=false (see
                     csrc/common.cuh for why), -lineinfo for ncu source pages.
-* libqpcg_gen.so  : host C++ instance generators (counter RNG, parallel).
+* libqpcg_gen.so  : host C++ instance generators (counter RNG, parallel) and the
+                    reference's text problem format (textio.cpp).
 """
 from __future__ import annotations
 
@@ -60,12 +61,12 @@ def build_engine(force: bool = False) -> str:
 
 
 def build_gen(force: bool = False) -> str:
-    src = os.path.join(CSRC, "gen.cpp")
-    if not os.path.exists(src):
+    srcs = [os.path.join(CSRC, f) for f in ("gen.cpp", "textio.cpp")]
+    if not os.path.exists(srcs[0]):
         return ""
-    if force or _stale(GEN_SO, [src]):
+    if force or _stale(GEN_SO, srcs):
         cmd = ["g++", "-std=c++17", "-O3", "-ffp-contract=off", "-fPIC", "-shared", "-pthread",
-               "-o", GEN_SO, src]
+               "-o", GEN_SO, *srcs]
         print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
     return GEN_SO

@@ -251,10 +251,24 @@ class Workspace : public IEngine<T> {
       const char* e = std::getenv("QPCG_NO_DEFER");
       defer_values = op.input_memory == QPCG_MEM_HOST && !(e && e[0] == '1');
     }
+    // QPCG_SETUP_TRACE=1: host time at each phase boundary (stream synced)
+    static const bool trace = [] {
+      const char* e = std::getenv("QPCG_SETUP_TRACE");
+      return e && e[0] == '1';
+    }();
+    auto mark = [&](const char* what) {
+      if (!trace) return;
+      CK(cudaStreamSynchronize(s));
+      std::fprintf(stderr, "[setup] %-16s %8.3f ms  launches %llu\n", what, (now_s() - w0) * 1e3,
+                   (unsigned long long)(g_launches - l0));
+    };
     load(Pu, q, A, l, u, 0, A.rows, false);
+    mark("load");
     ValKeys k = validate_keys();
     raise_first(k);
+    mark("validate");
     build_structures();
+    mark("structures");
     uint32_t passes = 0;
     T deviation = T(0);
     if (set.scaling_enabled) {
@@ -268,10 +282,13 @@ class Workspace : public IEngine<T> {
         deviation = read_scalar(ruiz_scal + 4);
       }
     }
+    mark("ruiz");
     finish_scaling(passes, deviation);
     diag_ata_kernel<T><<<grid_for(uint64_t(D.n) * 32), kThreads, 0, s>>>(D.AT, D.diag_ata, nullptr);
     CK_LAUNCH();
+    mark("finish_scaling");
     finish_setup();
+    mark("finish_setup");
     CK(cudaEventRecord(ev1, s));
     CK(cudaEventSynchronize(ev1));
     float ms = 0;
