@@ -178,7 +178,11 @@ typedef struct {
                               its device, combined in block order */
   int32_t nccl_rank;       /* rank of this process in the NCCL group */
   int32_t nccl_ranks;      /* processes (one per GPU) in the NCCL group */
-  int32_t reserved_;
+  int32_t sm_budget;       /* 0: the persistent driver may use the whole
+                              device.  k > 0: at most k SMs (a cooperative
+                              grid of k SMs, one 16-SM cluster, or one block),
+                              so that many small solves share one GPU
+                              (batching); results are unchanged */
   void* stream;            /* cudaStream_t to run on (NULL: the workspace
                               creates its own non-blocking stream) */
   const void* nccl_id;     /* NULL: no NCCL.  Else the QPCG_NCCL_ID_BYTES-byte

@@ -78,7 +78,7 @@ class RhoUpdate(C.Structure):
 class Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("input_memory", C.c_int32), ("mode", C.c_int32),
                 ("record_diagnostics", C.c_int32), ("virtual_shards", C.c_int32),
-                ("nccl_rank", C.c_int32), ("nccl_ranks", C.c_int32), ("reserved_", C.c_int32),
+                ("nccl_rank", C.c_int32), ("nccl_ranks", C.c_int32), ("sm_budget", C.c_int32),
                 ("stream", C.c_void_p), ("nccl_id", C.c_void_p), ("transport", C.c_int32),
                 ("reserved2_", C.c_int32), ("rendezvous_dir", C.c_char_p)]
 

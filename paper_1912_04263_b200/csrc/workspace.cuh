@@ -927,13 +927,15 @@ class Workspace : public IEngine<T> {
       }
       cudaGetLastError();
     }
-    if (work <= block_max_nnz()) {
-      // tiny problem: one block, __syncthreads barriers, matrices held in its L1
+    const int budget = std::max(0, opt.sm_budget);  // SMs this solve may hold (0: all)
+    if (work <= block_max_nnz() || budget == 1) {
+      // tiny problem (or a one-SM budget): one block, __syncthreads barriers,
+      // matrices held in its L1
       k_admm_persistent<T, BlockSync><<<1, kThreads, 0, s>>>(D, B);
       CK_LAUNCH();
       return;
     }
-    if (cluster > 0 && work <= cluster_max_nnz()) {
+    if (cluster > 0 && (work <= cluster_max_nnz() || (budget >= cluster && budget < 2 * cluster))) {
       // tiny problem: one cluster, hardware barriers
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute at[1];
@@ -950,15 +952,19 @@ class Workspace : public IEngine<T> {
       CK_LAUNCH();
       return;
     }
-    static int max_grid = 0;  // co-resident blocks (same device model for every workspace)
+    static int max_grid = 0, grid_per_sm = 0;  // co-resident blocks (same device model)
     if (max_grid == 0) {
       int per_sm = 0, sms = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_admm_persistent<T, GridSync>,
                                                        kThreads, 0));
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-      max_grid = std::max(1, per_sm) * sms;
+      grid_per_sm = std::max(1, per_sm);
+      max_grid = grid_per_sm * sms;
     }
-    const int grid = max_grid;  // measured: more co-resident blocks is faster at every size
+    // measured: more co-resident blocks is faster at every size; a budget
+    // caps the grid (the reductions emulate a fixed geometry, so any grid
+    // gives the same bits)
+    const int grid = budget > 0 ? std::min(max_grid, grid_per_sm * budget) : max_grid;
     CK(cudaLaunchCooperativeKernel((const void*)k_admm_persistent<T, GridSync>, dim3(grid),
                                    dim3(kThreads), args, 0, s));
     CK_LAUNCH();

@@ -79,8 +79,10 @@ def _pre(dtype) -> str:
 
 def make_options(device: int = -1, mode: str = "graph", record_diagnostics: bool = False,
                  device_memory: bool = False, shards: int = 1,
-                 nccl: tuple | None = None, peer: tuple | None = None) -> _abi.Options:
-    """shards: row blocks of A held on this device (virtual shards);
+                 nccl: tuple | None = None, peer: tuple | None = None,
+                 sm_budget: int = 0) -> _abi.Options:
+    """sm_budget: SMs the persistent driver may hold (0: the whole device);
+    shards: row blocks of A held on this device (virtual shards);
     nccl: (rank, ranks, id_bytes) to join the row-sharded NCCL group
     (SURVEY.md §8(e); id_bytes from nccl_unique_id() on rank 0);
     peer: (rank, ranks, rendezvous_dir) for the peer-memory transport."""
@@ -90,6 +92,7 @@ def make_options(device: int = -1, mode: str = "graph", record_diagnostics: bool
     o.mode = {"eager": _abi.MODE_EAGER, "persistent": _abi.MODE_PERSISTENT}.get(mode, _abi.MODE_GRAPH)
     o.record_diagnostics = 1 if record_diagnostics else 0
     o.virtual_shards = max(1, int(shards))
+    o.sm_budget = max(0, int(sm_budget))
     if nccl is not None:
         rank, ranks, uid = nccl
         buf = C.create_string_buffer(bytes(uid), _abi.NCCL_ID_BYTES)
@@ -214,9 +217,11 @@ def fetch_diagnostics(lib, ws, diag: SolveDiagnostics):
 
 def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | None = None,
           diag: SolveDiagnostics | None = None, device: int = -1, mode: str = "graph",
-          shards: int = 1, nccl: tuple | None = None, peer: tuple | None = None):
+          shards: int = 1, nccl: tuple | None = None, peer: tuple | None = None,
+          sm_budget: int = 0):
     """Drop-in for qpcg::solve (solver.hpp:386-541) on the B200 engine.
-    shards > 1 / nccl / peer: the row-sharded engine."""
+    shards > 1 / nccl / peer: the row-sharded engine (SURVEY.md §8(e));
+    sm_budget: cap on the SMs of the persistent driver (see solve_batch)."""
     if diag is not None:
         with Workspace(p, settings, device, mode, record_diagnostics=True, shards=shards,
                        nccl=nccl, peer=peer) as ws:
@@ -228,7 +233,7 @@ def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | N
     n, m = p.n, p.m
     dt = p.dtype
     s = (settings or Settings()).to_c()
-    o = make_options(device, mode, shards=shards, nccl=nccl, peer=peer)
+    o = make_options(device, mode, shards=shards, nccl=nccl, peer=peer, sm_budget=sm_budget)
     x, z, y = np.zeros(n, dt), np.zeros(m, dt), np.zeros(m, dt)
     cert = np.zeros(max(n, m), dt)
     info = _abi.Info()
@@ -243,3 +248,36 @@ def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | N
     if rc != _abi.QPCG_OK:
         _raise(rc, msg.value.decode())
     return outcome_from_c(info, x, z, y, cert)
+
+
+def solve_batch(problems, settings: Settings | None = None, device: int = -1,
+                concurrency: int = 8, small_nnz: int = 30000) -> list:
+    """Many independent problems on one GPU.
+    Problems with nnz(A) + nnz(P_upper) <= small_nnz run `concurrency` at a
+    time, each on its own workspace and stream with its persistent driver
+    capped at one 16-SM thread-block cluster (sm_budget = 16), so they share
+    the GPU instead of each holding all of it; larger problems run one after
+    another with the whole device (measured: side-by-side solves only pay off
+    below ~3e4 nonzeros, scripts/batch_throughput.py).  Outcomes in input
+    order, bitwise equal to solve()."""
+    from concurrent.futures import ThreadPoolExecutor
+    problems = list(problems)
+    out = [None] * len(problems)
+    small = [i for i, p in enumerate(problems) if p.nnz_total() <= small_nnz]
+    k = max(1, min(int(concurrency), len(small) or 1))
+    if small:
+        with ThreadPoolExecutor(max_workers=k) as ex:
+            budget = 16 if k > 1 else 0
+            for i, o in zip(small, ex.map(lambda i: solve(problems[i], settings, device=device,
+                                                          sm_budget=budget), small)):
+                out[i] = o
+    for i, p in enumerate(problems):
+        if out[i] is None:
+            out[i] = solve(p, settings, device=device)
+    return out
+
+
+def device_sm_count(device: int = -1) -> int:
+    import torch  # plumbing only: the device's SM count
+    d = torch.cuda.current_device() if device < 0 else device
+    return torch.cuda.get_device_properties(d).multi_processor_count
