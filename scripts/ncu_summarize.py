@@ -1,6 +1,7 @@
 """Summarise an ncu --set full capture of the SpMV passes into profiles/.
 
     python scripts/ncu_summarize.py gpurun_out/prof.ncu-rep <config> <source note>
+    python scripts/ncu_summarize.py a.csv,b.csv <config> <note>   (ncu --page raw --csv exports)
 
 Writes profiles/ncu_summary.json[<config>] (read by bench.py for roofline.traffic)."""
 import csv
@@ -11,8 +12,15 @@ import subprocess
 import sys
 
 rep, cfg, note = sys.argv[1], sys.argv[2], " ".join(sys.argv[3:])
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(raw)))
+if rep.endswith(".csv"):
+    rows = []
+    for i, f in enumerate(rep.split(",")):
+        part = list(csv.reader(open(f)))
+        rows += part if i == 0 else part[2:]  # one header + unit row (same metric set)
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
 hdr = rows[0]
 keys = {"gpu__time_duration.sum": "ncu_us", "dram__bytes_read.sum": "dram_read",
         "dram__bytes_write.sum": "dram_write",
