@@ -206,7 +206,7 @@ inline void transpose_structure(const uint32_t* ci, const uint32_t* row_of, uint
   CK(cub::DeviceRadixSort::SortPairs(tmp.ptr, b, ci, keys_out, idx, perm, nnz, 0, nb, s));
   const uint32_t* perm_c = perm;
   for_n(nnz, [=] __device__(uint32_t i) { out_ci[i] = row_of[perm_c[i]]; }, s);
-  CK(cudaStreamSynchronize(s));
+  // (frees are ordered on s: dmalloc / dfree follow the caller's AllocScope(s))
   CK(dfree(cnt));
   CK(dfree(keys_out));
   CK(dfree(idx));
@@ -279,7 +279,6 @@ uint32_t symmetrize_upper_dev(const DevCsr<T>& up, const uint32_t* up_row_of, De
     oci[dst] = ci[k];
     ov[dst] = uv[k];
   }, s);
-  CK(cudaStreamSynchronize(s));
   for (void* p : {(void*)flags, (void*)pos, (void*)sel, (void*)sel_cols, (void*)lower_rp,
                   (void*)lower_ci, (void*)lower_perm, (void*)sel_rows, (void*)cnt})
     CK(dfree(p));

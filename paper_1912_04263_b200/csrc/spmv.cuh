@@ -412,6 +412,22 @@ inline uint32_t grid_for(uint64_t n, int threads = kThreads) {
 }
 
 // Total of an exclusive scan: last exclusive value + last input.
+// Totals of K exclusive scans of length n with one stream synchronisation.
+template <int K>
+inline void scan_totals(const uint32_t* const (&in)[K], const uint32_t* const (&ex)[K], uint32_t n,
+                        uint32_t (&out)[K], cudaStream_t s) {
+  if (n == 0) {
+    for (int i = 0; i < K; ++i) out[i] = 0;
+    return;
+  }
+  uint32_t h[2 * K];
+  for (int i = 0; i < K; ++i) {
+    CK(cudaMemcpyAsync(h + 2 * i, ex[i] + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h + 2 * i + 1, in[i] + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < K; ++i) out[i] = h[2 * i] + h[2 * i + 1];
+}
 inline uint32_t scan_total(const uint32_t* in, const uint32_t* ex, uint32_t n, cudaStream_t s) {
   if (n == 0) return 0;
   uint32_t a = 0, b = 0;
@@ -497,8 +513,6 @@ void plan_compress(SpmvPlan<T>& P, const uint32_t* ci, uint32_t nnz, uint32_t co
   chunk_count_kernel<<<grid_for(P.n_items), kThreads, 0, s>>>(P.items, P.n_items, nch);
   CK_LAUNCH();
   exclusive_scan_u32(nch, P.c0, P.n_items, tmp, s);
-  P.n_chunks = scan_total(nch, P.c0, P.n_items, s);
-  CK(dfree(nch));
   uint32_t* cnt;
   CK(dmalloc(&cnt, sizeof(uint32_t)));
   CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), s));
@@ -506,8 +520,15 @@ void plan_compress(SpmvPlan<T>& P, const uint32_t* ci, uint32_t nnz, uint32_t co
   compress_kernel<<<g, kThreads, 0, s>>>(ci, P.items, P.n_items, P.c0, nullptr, nullptr, nullptr,
                                           cnt, 0);
   CK_LAUNCH();
-  CK(cudaMemcpyAsync(&P.n_wide, cnt, 4, cudaMemcpyDeviceToHost, s));
+  // chunk total and wide-chunk count with one synchronisation
+  uint32_t h[3];
+  CK(cudaMemcpyAsync(h, P.c0 + P.n_items - 1, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h + 1, nch + P.n_items - 1, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h + 2, cnt, 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  CK(dfree(nch));
+  P.n_chunks = h[0] + h[1];
+  P.n_wide = h[2];
   // (+32: the per-stride base load of a warp may read up to U - 1 ids past
   // the item's last chunk)
   CK(dmalloc(&P.off16, sizeof(uint16_t) * (size_t(nnz) + 1)));
@@ -544,10 +565,13 @@ SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaSt
   exclusive_scan_u32(nch, item_off, rows, tmp, s);
   exclusive_scan_u32(is_multi, lr_idx, rows, tmp, s);
   exclusive_scan_u32(multi_nch, pbase, rows, tmp, s);
-  P.n_short = scan_total(is_short, short_pos, rows, s);
-  P.n_items = scan_total(nch, item_off, rows, s);
-  P.n_long = scan_total(is_multi, lr_idx, rows, s);
-  P.n_partials = scan_total(multi_nch, pbase, rows, s);
+  uint32_t tot[4];
+  scan_totals<4>({is_short, nch, is_multi, multi_nch}, {short_pos, item_off, lr_idx, pbase}, rows,
+                 tot, s);
+  P.n_short = tot[0];
+  P.n_items = tot[1];
+  P.n_long = tot[2];
+  P.n_partials = tot[3];
   CK(dmalloc(&P.short_rows, sizeof(uint32_t) * (P.n_short ? P.n_short : 1)));
   CK(dmalloc(&P.items, sizeof(WorkItem) * (P.n_items ? P.n_items : 1)));
   CK(dmalloc(&P.lrinfo, sizeof(uint2) * (P.n_long ? P.n_long : 1)));

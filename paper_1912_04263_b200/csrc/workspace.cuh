@@ -492,6 +492,9 @@ class Workspace : public IEngine<T> {
 
   // symmetrize_upper, transpose_csr, plans, the original and scaled copies
   void build_structures() {
+    // this workspace's stream and arena for the transient buffers too (the
+    // helpers free them stream-ordered, without a synchronisation)
+    AllocScope scope(s, &arena);
     const uint32_t n = D.n, m = D.m, annz = D.A.nnz;
     DevCsr<T> Pup{n, n, pu_nnz, pu_v, pu_rp, pu_ci};
     SpmvPlan<T> pPu = plan_build<T>(pu_rp, n, tmp, s);
