@@ -31,6 +31,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/qpcg_b200.h"
@@ -39,6 +40,7 @@
 #include "comm.cuh"
 #include "persist.cuh"
 #include "setup.cuh"
+#include "upload.cuh"
 
 namespace qpcg_b200 {
 
@@ -165,6 +167,7 @@ class Workspace : public IEngine<T> {
   bool have_counted_setup = false;
 
   ~Workspace() {
+    if (up_thread.joinable()) up_thread.join();  // (a setup that failed before wait_values)
     if (s_up) {
       cudaStreamSynchronize(s_up);
       cudaStreamDestroy(s_up);
@@ -210,9 +213,12 @@ class Workspace : public IEngine<T> {
   }
   void upload(void* dst, const void* src, size_t bytes) {
     if (bytes == 0) return;
-    const bool host = opt.input_memory == QPCG_MEM_HOST;
-    CK(cudaMemcpyAsync(dst, src, bytes, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
-    if (host) h2d_bytes += bytes;
+    if (opt.input_memory == QPCG_MEM_HOST) {
+      CK(h2d(dst, src, bytes, s, device));  // pageable sources through the pinned stager
+      h2d_bytes += bytes;
+    } else {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+    }
   }
   void download(void* dst, const void* src, size_t bytes) {
     if (bytes == 0 || dst == nullptr) return;
@@ -374,9 +380,23 @@ class Workspace : public IEngine<T> {
       }
       CK(cudaEventRecord(ev_vals, s));  // a_v is allocated on s
       CK(cudaStreamWaitEvent(s_up, ev_vals, 0));
-      CK(cudaMemcpyAsync(a_v, A.values + e0, sizeof(T) * annz, cudaMemcpyHostToDevice, s_up));
-      h2d_bytes += sizeof(T) * annz;
-      CK(cudaEventRecord(ev_vals, s_up));
+      // a background host thread feeds the copy (a pageable source is staged
+      // by host threads; cudaMemcpyAsync would block this thread until done)
+      // while this one enqueues the structural setup
+      const void* src = A.values + e0;
+      const size_t nb = sizeof(T) * annz;
+      T* dst = a_v;
+      const int dev = device;
+      cudaStream_t su = s_up;
+      cudaEvent_t ev = ev_vals;
+      up_err = cudaSuccess;
+      up_thread = std::thread([this, src, nb, dst, dev, su, ev] {
+        cudaError_t e = cudaSetDevice(dev);
+        if (e == cudaSuccess) e = h2d(dst, src, nb, su, dev);
+        if (e == cudaSuccess) e = cudaEventRecord(ev, su);
+        up_err = e;
+      });
+      h2d_bytes += nb;
       values_pending = true;
     } else {
       upload(a_v, A.values + e0, sizeof(T) * annz);
@@ -400,8 +420,12 @@ class Workspace : public IEngine<T> {
   cudaStream_t s_up = nullptr;
   cudaEvent_t ev_vals = nullptr;
   double h2d_t0 = 0;
+  std::thread up_thread;
+  cudaError_t up_err = cudaSuccess;
   void wait_values() {
     if (!values_pending) return;
+    if (up_thread.joinable()) up_thread.join();
+    CK(up_err);
     CK(cudaStreamWaitEvent(s, ev_vals, 0));
     CK(cudaEventSynchronize(ev_vals));
     h2d_seconds = now_s() - h2d_t0;  // upload wall time, overlapped with the structural setup
