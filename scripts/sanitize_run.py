@@ -1,4 +1,5 @@
-"""Small solves through every driver, for compute-sanitizer (memcheck /
+"""Small solves through every driver (plus one staged-upload solve and a
+solve_batch), for compute-sanitizer (memcheck /
 racecheck / synccheck / initcheck):
     compute-sanitizer --tool memcheck python scripts/sanitize_run.py"""
 import sys
@@ -26,4 +27,12 @@ for p in probs:
         ws.update_rho(0.5)
         ws.update_vectors(q=p.q * 1.0)
         ws.solve()
+# staged pageable upload (A's values > 8 MB) with the background feed
+big = G.generate("lasso", 8, 0)
+r = solver.solve(big, S, device=0)
+print("staged", big.a.nnz, r.status, r.iterations, flush=True)
+# many small solves side by side with a capped persistent driver
+outs = solver.solve_batch([G.generate("random", 2, s) for s in range(4)], S, device=0,
+                          concurrency=2)
+print("batch", [o.iterations for o in outs], flush=True)
 print("done")
