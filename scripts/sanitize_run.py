@@ -28,7 +28,7 @@ for p in probs:
         ws.update_vectors(q=p.q * 1.0)
         ws.solve()
 # staged pageable upload (A's values > 8 MB) with the background feed
-big = G.generate("lasso", 8, 0)
+big = G.generate_explicit("lasso", 1000, 20000, 0, 3)  # 24 MB of values: staged
 r = solver.solve(big, S, device=0)
 print("staged", big.a.nnz, r.status, r.iterations, flush=True)
 # many small solves side by side with a capped persistent driver
