@@ -929,9 +929,10 @@ class Workspace : public IEngine<T> {
     PersistBufs<T> B{persist_part, D.ctl};
     void* args[] = {(void*)&D, (void*)&B};
     const uint64_t work = uint64_t(D.A.nnz) + D.P.nnz;
-    static int cluster = -1;  // largest cluster the kernel can run as (same device model)
-    if (cluster < 0) {
-      cluster = 0;
+    // largest cluster the kernel can run as (same device model); thread-safe
+    // one-time probe (solve_batch runs workspaces from several threads)
+    static const int cluster = [] {
+      int c_ok = 0;
       auto* kc = k_admm_persistent<T, ClusterSync>;
       if (cudaFuncSetAttribute(kc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
         for (int c : {16, 8}) {
@@ -947,13 +948,14 @@ class Workspace : public IEngine<T> {
           cfg.numAttrs = 1;
           int nc = 0;
           if (cudaOccupancyMaxActiveClusters(&nc, kc, &cfg) == cudaSuccess && nc > 0) {
-            cluster = c;
+            c_ok = c;
             break;
           }
         }
       }
       cudaGetLastError();
-    }
+      return c_ok;
+    }();
     const int budget = std::max(0, opt.sm_budget);  // SMs this solve may hold (0: all)
     if (work <= block_max_nnz() || budget == 1) {
       // tiny problem (or a one-SM budget): one block, __syncthreads barriers,
@@ -975,19 +977,23 @@ class Workspace : public IEngine<T> {
       cfg.stream = s;
       cfg.attrs = at;
       cfg.numAttrs = 1;
+      // (the attribute is per device: set it for this one too)
+      CK(cudaFuncSetAttribute(k_admm_persistent<T, ClusterSync>,
+                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       CK(cudaLaunchKernelExC(&cfg, (const void*)k_admm_persistent<T, ClusterSync>, args));
       CK_LAUNCH();
       return;
     }
-    static int max_grid = 0, grid_per_sm = 0;  // co-resident blocks (same device model)
-    if (max_grid == 0) {
-      int per_sm = 0, sms = 0;
+    // co-resident blocks (same device model; thread-safe one-time probe)
+    static const int grid_per_sm = [] {
+      int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_admm_persistent<T, GridSync>,
                                                        kThreads, 0));
-      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-      grid_per_sm = std::max(1, per_sm);
-      max_grid = grid_per_sm * sms;
-    }
+      return std::max(1, per_sm);
+    }();
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const int max_grid = grid_per_sm * sms;
     // measured: more co-resident blocks is faster at every size; a budget
     // caps the grid (the reductions emulate a fixed geometry, so any grid
     // gives the same bits)
