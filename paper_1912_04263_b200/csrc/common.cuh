@@ -212,10 +212,19 @@ constexpr int kNumSMs = 148;           // B200
 constexpr int kThreads = 256;          // default block size
 constexpr int kWarpsPerBlock = kThreads / 32;
 constexpr uint32_t kShortRowMax = 8;   // rows with <= 8 nnz: one thread per row
-#ifndef QPCG_CHUNK
-#define QPCG_CHUNK 4096
+// nnz per warp work item (long rows split): 2^chunk_log2<T>().  4096 for
+// both precisions (DESIGN.md §4 item-size sweep).  fp32 passes run 2-4 %
+// faster with 8192, but the changed rounding of the long rows moved the
+// config-2 fp32 trajectory from 110 / 433 to 120 / 466 iterations (a slower
+// solve), so it stays at 4096.  -DQPCG_CHUNK_LOG2=n forces a size (A/B builds).
+template <typename T>
+__host__ __device__ constexpr uint32_t chunk_log2() {
+#ifdef QPCG_CHUNK_LOG2
+  return QPCG_CHUNK_LOG2;
+#else
+  return 12u;
 #endif
-constexpr uint32_t kChunk = QPCG_CHUNK;  // nnz per warp work item (long rows split)
+}
 constexpr int kRedBlocks = 2 * kNumSMs;  // fixed grid of reduction kernels (deterministic)
 
 __host__ __device__ inline uint32_t ceil_div(uint32_t a, uint32_t b) { return (a + b - 1) / b; }

@@ -4,7 +4,7 @@
 // x[col[k]].  The reference sums each row left to right; here:
 //   * rows with <= kShortRowMax nnz ("S bin") run one thread per row and sum
 //     left to right — bit-identical to the reference for those rows;
-//   * longer rows are cut into work items of <= kChunk nnz ("W bin"), one
+//   * longer rows are cut into work items of <= 2^chunk_log2<T>() nnz ("W bin"), one
 //     warp per item, lanes striding the item with coalesced loads; lanes
 //     combine with a fixed xor-butterfly and multi-item rows combine their
 //     per-item partials in item order.  The order is fixed per matrix, so
@@ -212,7 +212,7 @@ __device__ __forceinline__ void item_finish(const DevCsr<T>& M, const SpmvPlan<T
   uint32_t prev = 0;
   const uint2 info = P.lrinfo[item.lr];
   if (lane == 0) {
-    const uint32_t chunk = (item.beg - M.rp[item.row]) / kChunk;
+    const uint32_t chunk = (item.beg - M.rp[item.row]) >> chunk_log2<T>();
     T* part = P.partials + (size_t)(info.x + chunk) * kMaxCols;
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) part[j] = acc[j];
@@ -326,12 +326,13 @@ void launch_spmv(const DevCsr<T>& M, const SpmvPlan<T>& P, const Gather& g, cons
 
 // ------------------------------------------------------------ plan build
 static __global__ void plan_classify_kernel(const uint32_t* __restrict__ rp, uint32_t rows,
+                                            uint32_t chunk,
                                      uint32_t* is_short, uint32_t* nch, uint32_t* is_multi,
                                      uint32_t* multi_nch) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
     const uint32_t len = rp[r + 1] - rp[r];
     const uint32_t s = len <= kShortRowMax;
-    const uint32_t c = s ? 0u : ceil_div(len, kChunk);
+    const uint32_t c = s ? 0u : ceil_div(len, chunk);
     is_short[r] = s;
     nch[r] = c;
     is_multi[r] = c > 1;
@@ -340,6 +341,7 @@ static __global__ void plan_classify_kernel(const uint32_t* __restrict__ rp, uin
 }
 
 static __global__ void plan_emit_kernel(const uint32_t* __restrict__ rp, uint32_t rows,
+                                        uint32_t chunk,
                                  const uint32_t* is_short, const uint32_t* short_pos,
                                  const uint32_t* nch, const uint32_t* item_off,
                                  const uint32_t* lr_idx, const uint32_t* pbase,
@@ -356,8 +358,8 @@ static __global__ void plan_emit_kernel(const uint32_t* __restrict__ rp, uint32_
     for (uint32_t q = 0; q < c; ++q) {
       WorkItem w;
       w.row = r;
-      w.beg = b + q * kChunk;
-      w.end = min(e, w.beg + kChunk);
+      w.beg = b + q * chunk;
+      w.end = min(e, w.beg + chunk);
       w.lr = lr;
       items[item_off[r] + q] = w;
       // sort key.  by_chunk: the q-th chunks of all rows first, in row order,
@@ -365,7 +367,7 @@ static __global__ void plan_emit_kernel(const uint32_t* __restrict__ rp, uint32_
       // about the same column window in every row of similar density, so the
       // warps resident on an SM gather from one window (L1 reuse).  Else:
       // longest first (balanced tail).
-      item_len[item_off[r] + q] = by_chunk ? q : kChunk - (w.end - w.beg);
+      item_len[item_off[r] + q] = by_chunk ? q : chunk - (w.end - w.beg);
     }
   }
 }
@@ -558,7 +560,8 @@ SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaSt
   CK(dmalloc(&item_off, bytes));
   CK(dmalloc(&lr_idx, bytes));
   CK(dmalloc(&pbase, bytes));
-  plan_classify_kernel<<<grid_for(rows), kThreads, 0, s>>>(d_rp, rows, is_short, nch, is_multi,
+  const uint32_t chunk = 1u << chunk_log2<T>();
+  plan_classify_kernel<<<grid_for(rows), kThreads, 0, s>>>(d_rp, rows, chunk, is_short, nch, is_multi,
                                                           multi_nch);
   CK_LAUNCH();
   exclusive_scan_u32(is_short, short_pos, rows, tmp, s);
@@ -586,7 +589,7 @@ SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaSt
   CK(dmalloc(&keys_out, sizeof(uint32_t) * ni));
   CK(dmalloc(&order, sizeof(uint32_t) * ni));
   CK(dmalloc(&order_out, sizeof(uint32_t) * ni));
-  plan_emit_kernel<<<grid_for(rows), kThreads, 0, s>>>(d_rp, rows, is_short, short_pos, nch,
+  plan_emit_kernel<<<grid_for(rows), kThreads, 0, s>>>(d_rp, rows, chunk, is_short, short_pos, nch,
                                                       item_off, lr_idx, pbase, P.short_rows,
                                                       items_tmp, keys, P.lrinfo, by_chunk);
   CK_LAUNCH();
@@ -595,7 +598,7 @@ SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaSt
     iota_kernel<<<grid_for(P.n_items), kThreads, 0, s>>>(order, P.n_items);
     CK_LAUNCH();
     size_t b = 0;
-    const int kbits = by_chunk ? 20 : 12;
+    const int kbits = by_chunk ? 20 : int(chunk_log2<T>()) + 1;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, b, keys, keys_out, order, order_out, P.n_items, 0,
                                        kbits, s));
     tmp.ensure(b);
