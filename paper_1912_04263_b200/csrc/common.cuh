@@ -212,17 +212,18 @@ constexpr int kNumSMs = 148;           // B200
 constexpr int kThreads = 256;          // default block size
 constexpr int kWarpsPerBlock = kThreads / 32;
 constexpr uint32_t kShortRowMax = 8;   // rows with <= 8 nnz: one thread per row
-// nnz per warp work item (long rows split): 2^chunk_log2<T>().  4096 for
-// both precisions (DESIGN.md §4 item-size sweep).  fp32 passes run 2-4 %
-// faster with 8192, but the changed rounding of the long rows moved the
-// config-2 fp32 trajectory from 110 / 433 to 120 / 466 iterations (a slower
-// solve), so it stays at 4096.  -DQPCG_CHUNK_LOG2=n forces a size (A/B builds).
-template <typename T>
-__host__ __device__ constexpr uint32_t chunk_log2() {
+// nnz per warp work item (long rows split): 2^plan_chunk_log2(nnz) per
+// matrix (DESIGN.md §4 item-size sweep).  4096 for the 1e8-nnz class, where
+// the passes are throughput-bound and every item pays a two-round-trip head;
+// 2048 below 2^25 nnz, where a pass lasts a few item latencies and a few long
+// rows cut into 4096-nnz items set its tail (portfolio at N = 1e6: 256 ms
+// with 2048, 359 ms with 4096).  -DQPCG_CHUNK_LOG2=n forces a size.
+inline uint32_t plan_chunk_log2(uint64_t nnz) {
 #ifdef QPCG_CHUNK_LOG2
+  (void)nnz;
   return QPCG_CHUNK_LOG2;
 #else
-  return 12u;
+  return nnz >= (uint64_t(1) << 25) ? 12u : 11u;
 #endif
 }
 constexpr int kRedBlocks = 2 * kNumSMs;  // fixed grid of reduction kernels (deterministic)

@@ -40,7 +40,7 @@ void op_spmv<double>(const HostCsr<double>& mv, const double* x, double* y, int 
   CK(cudaMemcpyAsync(M.ci, mv.col_indices, 4 * size_t(M.nnz), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(M.rp, mv.row_ptr, 4 * (size_t(M.rows) + 1), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(dx, x, sizeof(T) * M.cols, cudaMemcpyHostToDevice, s));
-  SpmvPlan<T> P = plan_build<T>(M.rp, M.rows, tmp, s);
+  SpmvPlan<T> P = plan_build<T>(M.rp, M.rows, M.nnz, tmp, s);
   if (Workspace<T>::compress_indices()) plan_compress(P, M.ci, M.nnz, M.cols, tmp, s);  // as the workspace
   launch_spmv<T, 1, SumOp>(M, P, GatherVec<T>{dx}, EpiStore<T>{dy}, s);
   CK(cudaMemcpyAsync(y, dy, sizeof(T) * M.rows, cudaMemcpyDeviceToHost, s));

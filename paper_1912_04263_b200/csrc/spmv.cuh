@@ -4,7 +4,7 @@
 // x[col[k]].  The reference sums each row left to right; here:
 //   * rows with <= kShortRowMax nnz ("S bin") run one thread per row and sum
 //     left to right — bit-identical to the reference for those rows;
-//   * longer rows are cut into work items of <= 2^chunk_log2<T>() nnz ("W bin"), one
+//   * longer rows are cut into work items of <= 2^P.chunk_log2 nnz ("W bin"), one
 //     warp per item, lanes striding the item with coalesced loads; lanes
 //     combine with a fixed xor-butterfly and multi-item rows combine their
 //     per-item partials in item order.  The order is fixed per matrix, so
@@ -57,6 +57,7 @@ struct SpmvPlan {
   uint32_t* c0 = nullptr;
   uint32_t* wide = nullptr;
   uint32_t n_chunks = 0, n_wide = 0;
+  uint32_t chunk_log2 = 12;  // work items hold <= 2^chunk_log2 nnz (plan_chunk_log2)
   uint32_t grid() const { return nb_items + nb_short; }
 };
 
@@ -212,7 +213,7 @@ __device__ __forceinline__ void item_finish(const DevCsr<T>& M, const SpmvPlan<T
   uint32_t prev = 0;
   const uint2 info = P.lrinfo[item.lr];
   if (lane == 0) {
-    const uint32_t chunk = (item.beg - M.rp[item.row]) >> chunk_log2<T>();
+    const uint32_t chunk = (item.beg - M.rp[item.row]) >> P.chunk_log2;
     T* part = P.partials + (size_t)(info.x + chunk) * kMaxCols;
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) part[j] = acc[j];
@@ -545,8 +546,10 @@ void plan_compress(SpmvPlan<T>& P, const uint32_t* ci, uint32_t nnz, uint32_t co
 
 // Build the plan for a CSR structure whose row_ptr lives on the device.
 template <typename T>
-SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaStream_t s) {
+SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, uint64_t nnz, CubTemp& tmp,
+                       cudaStream_t s) {
   SpmvPlan<T> P;
+  P.chunk_log2 = plan_chunk_log2(nnz);
   const char* ord = std::getenv("QPCG_ITEM_ORDER");
   const int by_chunk = !(ord && ord[0] == 'l');  // "len": longest first
   if (rows == 0) return P;
@@ -560,7 +563,7 @@ SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaSt
   CK(dmalloc(&item_off, bytes));
   CK(dmalloc(&lr_idx, bytes));
   CK(dmalloc(&pbase, bytes));
-  const uint32_t chunk = 1u << chunk_log2<T>();
+  const uint32_t chunk = 1u << P.chunk_log2;
   plan_classify_kernel<<<grid_for(rows), kThreads, 0, s>>>(d_rp, rows, chunk, is_short, nch, is_multi,
                                                           multi_nch);
   CK_LAUNCH();
@@ -598,7 +601,7 @@ SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, CubTemp& tmp, cudaSt
     iota_kernel<<<grid_for(P.n_items), kThreads, 0, s>>>(order, P.n_items);
     CK_LAUNCH();
     size_t b = 0;
-    const int kbits = by_chunk ? 20 : int(chunk_log2<T>()) + 1;
+    const int kbits = by_chunk ? 20 : int(P.chunk_log2) + 1;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, b, keys, keys_out, order, order_out, P.n_items, 0,
                                        kbits, s));
     tmp.ensure(b);

@@ -521,8 +521,8 @@ class Workspace : public IEngine<T> {
     AllocScope scope(s, &arena);
     const uint32_t n = D.n, m = D.m, annz = D.A.nnz;
     DevCsr<T> Pup{n, n, pu_nnz, pu_v, pu_rp, pu_ci};
-    SpmvPlan<T> pPu = plan_build<T>(pu_rp, n, tmp, s);
-    D.pA = plan_build<T>(a_rp, m, tmp, s);
+    SpmvPlan<T> pPu = plan_build<T>(pu_rp, n, pu_nnz, tmp, s);
+    D.pA = plan_build<T>(a_rp, m, annz, tmp, s);
     uint32_t* row_of = alloc<uint32_t>(std::max(pu_nnz, annz));
     plan_visit(Pup, pPu, RowOfFn{row_of}, s);
     // symmetrize_upper (solver.hpp:397)
@@ -532,7 +532,7 @@ class Workspace : public IEngine<T> {
     allocs.push_back(Pfull.ci);
     allocs.push_back(Pfull.val);
     plan_free(pPu);
-    D.pP = plan_build<T>(Pfull.rp, n, tmp, s);
+    D.pP = plan_build<T>(Pfull.rp, n, Pfull.nnz, tmp, s);
     D.Po = Pfull;
     // transpose_csr (solver.hpp:398)
     plan_visit(D.A, D.pA, RowOfFn{row_of}, s);
@@ -540,7 +540,7 @@ class Workspace : public IEngine<T> {
     uint32_t* at_ci = alloc<uint32_t>(annz);
     permA = alloc<uint32_t>(annz);
     transpose_structure(a_ci, row_of, n, annz, at_rp, at_ci, permA, tmp, s);
-    D.pAT = plan_build<T>(at_rp, n, tmp, s);
+    D.pAT = plan_build<T>(at_rp, n, annz, tmp, s);
     if (compress_indices()) {  // 16-bit column offsets for the A / A^T streams
       plan_compress(D.pA, a_ci, annz, n, tmp, s);
       plan_compress(D.pAT, at_ci, annz, m, tmp, s);
@@ -1348,9 +1348,9 @@ class Workspace : public IEngine<T> {
     D.P = up(Pf);
     D.A = up(A);
     D.AT = up(AT);
-    D.pP = plan_build<T>(D.P.rp, n, tmp, s);
-    D.pA = plan_build<T>(D.A.rp, m, tmp, s);
-    D.pAT = plan_build<T>(D.AT.rp, n, tmp, s);
+    D.pP = plan_build<T>(D.P.rp, n, D.P.nnz, tmp, s);
+    D.pA = plan_build<T>(D.A.rp, m, D.A.nnz, tmp, s);
+    D.pAT = plan_build<T>(D.AT.rp, n, D.AT.nnz, tmp, s);
     // linsys.hpp:54-58: a_t must be transpose_csr(a) bit for bit
     {
       uint32_t* row_of = alloc<uint32_t>(A.nnz);
