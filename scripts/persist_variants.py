@@ -1,3 +1,5 @@
+"""Loop time of the persistent driver's barrier variants (one block / one
+16-SM cluster / cooperative grid) on tiny instances: python scripts/persist_variants.py"""
 import os, sys
 sys.path.insert(0, "/root/repo")
 from paper_1912_04263_b200 import generators as G, solver

@@ -1,3 +1,5 @@
+"""Setup phase trace of a tiny instance (lasso scale 2):
+    QPCG_SETUP_TRACE=1 python scripts/tiny_setup_trace.py"""
 import sys, os
 sys.path.insert(0, "/root/repo")
 from paper_1912_04263_b200 import generators as G, solver
