@@ -391,6 +391,9 @@ class Sharded : public IEngine<T> {
     H.pcg = (unsigned long long)h_pcg;
     H.chk = (unsigned long long)h_chk;
     cudaGraph_t b_pcg, b_chk, b_inf, g_out;
+    // kernels per execution of each body, counted as they are captured
+    const uint64_t b0 = g_launches;
+    uint64_t c0 = g_launches;
     CK(cudaStreamBeginCaptureToGraph(s, b_admm, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     enq_rhs(H);
     b_pcg = add_cond(h_pcg, cudaGraphCondTypeWhile);
@@ -399,20 +402,30 @@ class Sharded : public IEngine<T> {
     enq_rho();
     each([&](Workspace<T>& w) { w.enq_admm_cond(H); });
     CK(cudaStreamEndCapture(s, &g_out));
+    body_kernels[0] = g_launches - c0;
+    c0 = g_launches;
     CK(cudaStreamBeginCaptureToGraph(s, b_pcg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     enq_pcg_iter(H);
     CK(cudaStreamEndCapture(s, &g_out));
+    body_kernels[1] = g_launches - c0;
     CK(cudaGraphConditionalHandleCreate(&h_inf, b_chk, 0, cudaGraphCondAssignDefault));
     H.inf = (unsigned long long)h_inf;
+    c0 = g_launches;
     CK(cudaStreamBeginCaptureToGraph(s, b_chk, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     enq_check(0, H);
     b_inf = add_cond(h_inf, cudaGraphCondTypeIf);
     CK(cudaStreamEndCapture(s, &g_out));
+    body_kernels[2] = g_launches - c0;
+    c0 = g_launches;
     CK(cudaStreamBeginCaptureToGraph(s, b_inf, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     enq_infeas();
     CK(cudaStreamEndCapture(s, &g_out));
+    body_kernels[3] = g_launches - c0;
+    graph_build = g_launches - b0;  // captured, not launched
     CK(cudaGraphInstantiate(&exec, graph, 0));
   }
+  uint64_t body_kernels[4] = {};  // per execution: ADMM step, PCG iteration, check, infeas
+  uint64_t graph_build = 0;
 
   // ------------------------------------------------------------ solve
   void solve(qpcg_info* info, T* x, T* z, T* y, T* cert) override {
@@ -424,8 +437,12 @@ class Sharded : public IEngine<T> {
     const uint64_t l0 = g_launches;
     Workspace<T>& W = w0();
     enq_residuals_fresh(1);  // solver.hpp:436-441
+    uint64_t graph_built_now = 0;
     if (graph_ok()) {
-      if (!exec) build_graph();
+      if (!exec) {
+        build_graph();
+        graph_built_now = graph_build;
+      }
       CK(cudaGraphLaunch(exec, s));
     }
     for (; !graph_ok();) {
@@ -487,12 +504,10 @@ class Sharded : public IEngine<T> {
       });
       info->h2d_bytes = h2d;
       info->h2d_seconds = h2ds;
-      uint64_t launches = g_launches - l0;
-      if (graph_ok()) {  // kernels executed inside the graph (per block L, per combine c)
-        const uint64_t L = comm.local, c = comm.p2p ? 3 : (L > 1 ? 1 : 0);
-        launches += W.hc.iter * (L * 10 + 2 * c) + W.hc.pcg_total * (L * 5 + c) +
-                    uint64_t(W.hc.n_checks) * (L * 3 + 2 * c) + uint64_t(W.hc.n_inf) * (L * 8 + 3 * c);
-      }
+      uint64_t launches = g_launches - l0 - graph_built_now;
+      if (graph_ok())  // kernels executed inside the graph
+        launches += W.hc.iter * body_kernels[0] + W.hc.pcg_total * body_kernels[1] +
+                    uint64_t(W.hc.n_checks) * body_kernels[2] + uint64_t(W.hc.n_inf) * body_kernels[3];
       info->kernel_launches = launches + (have_counted_setup ? 0 : setup_launches);
     }
     have_counted_setup = true;

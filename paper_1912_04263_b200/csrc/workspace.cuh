@@ -788,10 +788,11 @@ class Workspace : public IEngine<T> {
   void enq_post_pcg(const Handles& H) {
     k_pcg_fin<T><<<grid_for(D.n), kThreads, 0, s>>>(D);
     CK_LAUNCH();
-    launch_spmv<T, 2, SumOp>(D.A, D.pA, GatherAdmm<T>{D.g2n},
-                             EpiAdmm<T, 2>{D, T(0), T(0), T(0), false}, s);
-    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.xt},
-                             EpiAdmm<T, 1>{D, T(0), T(0), T(0), false}, s);
+    // z~ = A x~ with the m-side update: the 2-column build on check
+    // iterations (col 1 = A x_new), else the 1-column one; one launch
+    launch_spmv_select<T, 1, GatherVec<T>, EpiAdmm<T, 1>, 2, GatherAdmm<T>, EpiAdmm<T, 2>>(
+        D.A, D.pA, GatherVec<T>{D.xt}, EpiAdmm<T, 1>{D, T(0), T(0), T(0), false},
+        GatherAdmm<T>{D.g2n}, EpiAdmm<T, 2>{D, T(0), T(0), T(0), false}, s);
     k_xupdate<T><<<grid_for(D.n), kThreads, 0, s>>>(D, H);
     CK_LAUNCH();
   }
@@ -854,6 +855,7 @@ class Workspace : public IEngine<T> {
     return cp.conditional.phGraph_out[0];
   }
 
+  uint64_t body_kernels[5] = {};  // per execution: ADMM step, PCG iteration, check, infeas, rho
   void build_graph() {
     CK(cudaGraphCreate(&graph, 0));
     cudaGraphConditionalHandle h_admm, h_pcg, h_chk, h_inf, h_rho;
@@ -875,6 +877,9 @@ class Workspace : public IEngine<T> {
     H.chk = (unsigned long long)h_chk;
     H.rho = (unsigned long long)h_rho;
     cudaGraph_t b_pcg, b_chk, b_rho, b_inf, g_out;
+    // kernels per execution of each body, counted as they are captured
+    // (the solve's launch count multiplies them by the executions)
+    uint64_t c0 = g_launches;
     CK(cudaStreamBeginCaptureToGraph(s, b_admm, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     enq_rhs(H);
     enq_pcg_init(H);
@@ -885,21 +890,30 @@ class Workspace : public IEngine<T> {
     b_rho = add_cond_in_capture(h_rho, cudaGraphCondTypeIf);
     enq_admm_cond(H);
     CK(cudaStreamEndCapture(s, &g_out));
+    body_kernels[0] = g_launches - c0;
+    c0 = g_launches;
     CK(cudaStreamBeginCaptureToGraph(s, b_pcg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     enq_pcg_iter(H);
     CK(cudaStreamEndCapture(s, &g_out));
+    body_kernels[1] = g_launches - c0;
     CK(cudaGraphConditionalHandleCreate(&h_inf, b_chk, 0, cudaGraphCondAssignDefault));
     H.inf = (unsigned long long)h_inf;
+    c0 = g_launches;
     CK(cudaStreamBeginCaptureToGraph(s, b_chk, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     enq_check(H, 0);
     b_inf = add_cond_in_capture(h_inf, cudaGraphCondTypeIf);
     CK(cudaStreamEndCapture(s, &g_out));
+    body_kernels[2] = g_launches - c0;
+    c0 = g_launches;
     CK(cudaStreamBeginCaptureToGraph(s, b_inf, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     enq_infeas(H);
     CK(cudaStreamEndCapture(s, &g_out));
+    body_kernels[3] = g_launches - c0;
+    c0 = g_launches;
     CK(cudaStreamBeginCaptureToGraph(s, b_rho, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     enq_rho(H);
     CK(cudaStreamEndCapture(s, &g_out));
+    body_kernels[4] = g_launches - c0;
     CK(cudaGraphInstantiate(&exec, graph, 0));
   }
 
@@ -1122,8 +1136,9 @@ class Workspace : public IEngine<T> {
     const bool has_cert = hc.status == 1 || hc.status == 2;
     uint64_t launches = g_launches - l0 - graph_build;
     if (opt.mode != QPCG_MODE_EAGER && !use_persistent())  // kernels executed inside the graph
-      launches += 9ull * hc.iter + 5ull * hc.pcg_total + 2ull * hc.n_checks + 6ull * hc.n_inf +
-                  2ull * hc.n_rho_branch;
+      launches += body_kernels[0] * hc.iter + body_kernels[1] * hc.pcg_total +
+                  body_kernels[2] * hc.n_checks + body_kernels[3] * hc.n_inf +
+                  body_kernels[4] * hc.n_rho_branch;
     if (has_cert) download(cert, D.cert, sizeof(T) * (hc.status == 1 ? D.m : D.n));
     CK(cudaStreamSynchronize(s));
     const double d2h = now_s() - td;
