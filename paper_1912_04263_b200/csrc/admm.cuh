@@ -314,8 +314,9 @@ struct GatherAdmm {  // {x~, x_new} packed by k_pcg_fin
   }
 };
 // NCOL 2 on check iterations (col 1 = A x_new for the residuals), NCOL 1 (x~
-// only, an 8-byte gather) otherwise.  Both builds are launched; each returns
-// at init() unless it is the one this iteration needs (gate: the pass's NCOL).
+// only, an 8-byte gather) otherwise.  init() is true only for the build this
+// iteration needs: the stand-alone path runs both in one launch
+// (spmv_select_kernel), the persistent loop calls both phases.
 template <typename T, int NCOL = 2>
 struct EpiAdmm {
   Dev<T> D;
