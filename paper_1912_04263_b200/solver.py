@@ -275,9 +275,3 @@ def solve_batch(problems, settings: Settings | None = None, device: int = -1,
         if out[i] is None:
             out[i] = solve(p, settings, device=device)
     return out
-
-
-def device_sm_count(device: int = -1) -> int:
-    import torch  # plumbing only: the device's SM count
-    d = torch.cuda.current_device() if device < 0 else device
-    return torch.cuda.get_device_properties(d).multi_processor_count
