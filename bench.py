@@ -20,9 +20,12 @@ RNG and recipes; fp64; settings {"lambda_pcg": 1e-3} (0.01, the survey's choice,
 * cpu_baseline  the reference itself (oracle/_ref, unmodified headers) on the
               same instance, 1 core (it is single threaded): its setup
               phases and hot-path operators are timed on a bounded sample and
-              the solve time is extrapolated with the solve's iteration counts.
+              the solve time is extrapolated with the REFERENCE's own iteration
+              counts (its committed complete solve of the instance).
 
---impl reference runs only the reference CPU arm (rank 0), same metric/config.
+--impl reference runs only the reference CPU arm (rank 0): the instance built by
+the reference's own generators, then ONE complete qpcg::solve of it (minutes on
+one core; value = its runtime_seconds), same metric and config dict.
 Multi-GPU (torchrun, N > 1): the ROW-SHARDED engine — every
 rank holds an nnz-balanced block of A's rows (+ its own A_g^T), and the A^T
 partials are combined once per operator apply: by default the SpMV epilogue
@@ -59,7 +62,6 @@ WORKLOADS = {
     "5a": "portfolio N~1e8 (n=142835, m=142836, nnz(A)=1.0e8)",
     "5b": "control/MPC gen_control scale 13 (nnz(A)=1.39e8)",
 }
-COUNTS_FILE = os.path.join(ROOT, "profiles", "solve_counts.json")
 
 
 def log(*a):
@@ -344,7 +346,8 @@ def cpu_baseline(problem, counts: dict, budget_reps: int = 1, cfg: str = "", lam
                        f"{t_trans:.2f}s, 1-pass Ruiz {t_ruiz1:.2f}s, operator build {t_op:.2f}s, "
                        f"K-apply {t_k:.3f}s, A^T spmv {t_at:.3f}s, A spmv {t_a:.3f}s, residuals "
                        f"{t_res:.3f}s ({wall:.1f}s of CPU); solve time EXTRAPOLATED to {passes} "
-                       f"Ruiz passes, {iters} ADMM / {pcg} PCG iterations, {checks} checks"
+                       f"Ruiz passes, {iters} ADMM / {pcg} PCG iterations, {checks} checks "
+                       f"(counts: {counts.get('source', 'given')})"
                        + (f"; the reference's complete solve of this instance took {full:.0f} s on one "
                           f"core of the build container (profiles/ref_solve_config{cfg}_*.json)"
                           if full else "")),
@@ -355,31 +358,20 @@ def cpu_baseline(problem, counts: dict, budget_reps: int = 1, cfg: str = "", lam
                              "loop_est": loop}}
 
 
-def load_counts(config: str) -> dict:
+def reference_counts(config: str, lam: float):
+    """The REFERENCE's own iteration counts for this instance: its complete
+    solve, committed as a golden anchor (tests/golden/config*_reference_solve.json,
+    scripts/ref_solve_config.py).  None when no such run exists."""
     try:
-        with open(COUNTS_FILE) as f:
-            return json.load(f)[config]
+        with open(os.path.join(ROOT, "tests", "golden", f"config{config}_reference_solve.json")) as f:
+            d = json.load(f)
     except Exception:
-        return {"iterations": 300, "pcg_iterations_total": 1500, "equil_passes": 10,
-                "source": "default guess (no recorded B200 solve)"}
-
-
-def save_counts(config: str, info) -> None:
-    try:
-        data = {}
-        if os.path.exists(COUNTS_FILE):
-            with open(COUNTS_FILE) as f:
-                data = json.load(f)
-        data[config] = {"iterations": int(info.iterations),
-                        "pcg_iterations_total": int(info.pcg_iterations_total),
-                        "equil_passes": int(info.equil_passes), "status": int(info.status),
-                        "objective": float(info.objective),
-                        "source": "B200 engine solve of the same instance (bench.py)"}
-        os.makedirs(os.path.dirname(COUNTS_FILE), exist_ok=True)
-        with open(COUNTS_FILE, "w") as f:
-            json.dump(data, f, indent=1, sort_keys=True)
-    except Exception:
-        pass
+        return None
+    if abs(float(d.get("lambda_pcg", -1.0)) - lam) > 1e-15:
+        return None
+    return {"iterations": int(d["iterations"]), "pcg_iterations_total": int(d["pcg_iterations_total"]),
+            "equil_passes": int(d["equil_passes"]), "runtime_seconds": float(d["runtime_seconds"]),
+            "source": f"the reference's complete solve (tests/golden/config{config}_reference_solve.json)"}
 
 
 def peaks() -> dict:
@@ -400,27 +392,75 @@ def ncu_traffic(config: str):
         return None
 
 
+def config_dict(args, problem, world: int, sharded: bool) -> dict:
+    """The workload description both arms print (identical dicts)."""
+    S = 8 if args.dtype == "f64" else 4
+    a_bytes = problem.a.nnz * (S + 4) * 2
+    return {"workload": WORKLOADS[args.config], "config_id": args.config,
+            "n": problem.n, "m": problem.m, "nnz_P_upper": problem.p_upper.nnz,
+            "nnz_A": problem.a.nnz, "settings": {"lambda_pcg": args.lambda_pcg},
+            "parallelism": (f"rowshard{world}-{args.transport}" if sharded else f"replicas{world}")
+                           if world > 1 else
+                           ("single" if args.shards <= 1 else f"virtual-rowshard{args.shards}"),
+            "l2": ("inputs larger than L2 (A and A^T streams ~%.1f GB per PCG iteration)"
+                   % (a_bytes / 1e9)) if a_bytes >= (256 << 20) else
+                  "matrices fit in L2: a 512 MB buffer is overwritten before every timed step",
+            "mode": args.mode}
+
+
+def reference_problem(config: str):
+    """The instance generated by the REFERENCE's own generators (oracle/_ref:
+    bench::detail recipes / bench::generate, generators.hpp) — bit-identical to
+    the engine arm's native generator (tests/test_generators.py)."""
+    from oracle import oracle as O  # reference arm only
+    from paper_1912_04263_b200.generators import CONFIGS
+    spec = CONFIGS[config]
+    if spec[0] == "class":
+        return O.ref_generate(spec[1], spec[2], 0)
+    return O.ref_generate_explicit(*spec, seed=0)
+
+
 # --------------------------------------------------------------- arms
-def run_reference(args, rank: int) -> None:
+def run_reference(args, rank: int, world: int) -> None:
+    """The reference's own CPU implementation of the path: ONE complete
+    qpcg::solve (solver.hpp:386-541, oracle/_ref = the unmodified headers) of
+    the instance the reference's own generators build.  value = the solve's
+    runtime_seconds (its own timed region, solver.hpp:392 -> :539).  A full
+    solve of a BASELINE config takes minutes on one core, so exactly one step
+    is run whatever --steps / --warmup say (both printed as requested_*)."""
     if rank != 0:
         return
-    from paper_1912_04263_b200 import generators
-    problem = generators.config(args.config, seed=0)
-    counts = load_counts(args.config)
-    vals = []
-    for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(problem, counts, cfg=args.config, lam=args.lambda_pcg)
-        if i >= args.warmup:
-            vals.append(cb["value"])
-    v = float(np.mean(vals))
-    cb["value"] = v
+    from oracle import oracle as O  # reference arm only
+    from paper_1912_04263_b200.problem import Settings
+    tg = time.time()
+    problem = reference_problem(args.config)
+    if args.dtype == "f32":
+        problem = problem.astype(np.float32)
+    gen_s = time.time() - tg
+    log(f"reference generated config {args.config}: nnz(A)={problem.a.nnz} in {gen_s:.1f}s")
+    t0 = time.time()
+    r = O.ref_solve(problem, Settings(lambda_pcg=args.lambda_pcg))
+    wall = time.time() - t0
+    v = float(r.runtime_seconds)
+    log(f"reference solve: {r.status} {r.iterations} ADMM / {r.pcg_iterations_total} PCG, "
+        f"runtime {v:.1f}s (wall {wall:.1f}s)")
+    cb = {"value": v, "unit": "s", "cores": 1, "kind": "reference", "extrapolated": False,
+          "sample": (f"one complete qpcg::solve (oracle/_ref: the unmodified reference headers, "
+                     f"g++ -O3 -ffp-contract=off, single-threaded as the reference is) of the "
+                     f"whole config-{args.config} instance, generated by the reference's own "
+                     f"generators; runtime_seconds = its own timed region"),
+          "nproc": os.cpu_count(), "wall_s": wall}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference RNG + recipes, SURVEY.md §8(d))",
-            "config": {"workload": WORKLOADS[args.config], "config_id": args.config,
-                       "settings": {"lambda_pcg": args.lambda_pcg}, "iteration_counts": counts},
-            "cpu_baseline": cb,
+            "steps": 1, "warmup": 0, "requested_steps": args.steps,
+            "requested_warmup": args.warmup, "ms_per_step": v * 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.dtype, "data": "synthetic (reference RNG + recipes, SURVEY.md §8(d))",
+            "config": config_dict(args, problem, world, world > 1 and not args.replicas),
+            "solve": {"status": r.status, "iterations": int(r.iterations),
+                      "pcg_iterations_total": int(r.pcg_iterations_total),
+                      "objective": float(r.objective), "r_prim_inf": float(r.r_prim_inf),
+                      "r_dual_inf": float(r.r_dual_inf), "equil_passes": int(r.equil_passes)},
+            "generation_s": gen_s, "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -451,7 +491,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, rank, world)
         return
     import torch
     # QPCG_BENCH_SAME_GPU=1: every rank on GPU 0 (a harness dry run of the
@@ -553,7 +593,6 @@ def main():
             dist.destroy_process_group()
         return
     last = infos[-1]
-    save_counts(args.config, last)
     pk = peaks()
     S = 8 if dtype == np.float64 else 4
     at_ms, pcg_ms = kt[1], kt[2]
@@ -582,16 +621,7 @@ def main():
             "higher_is_better": False, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic (reference RNG + recipes, SURVEY.md §8(d))",
-            "config": {"workload": WORKLOADS[args.config], "config_id": args.config,
-                       "n": problem.n, "m": problem.m, "nnz_P_upper": problem.p_upper.nnz,
-                       "nnz_A": problem.a.nnz, "settings": {"lambda_pcg": args.lambda_pcg},
-                       "parallelism": (f"rowshard{world}-{args.transport}" if sharded else f"replicas{world}")
-                                      if world > 1 else
-                                      ("single" if args.shards <= 1 else f"virtual-rowshard{args.shards}"),
-                       "l2": ("inputs larger than L2 (A and A^T streams ~%.1f GB per PCG iteration)"
-                              % (kt[5] / 1e9)) if flush is None else
-                             "matrices fit in L2: a 512 MB buffer is overwritten before every timed step",
-                       "mode": args.mode},
+            "config": config_dict(args, problem, world, sharded),
             "solve": {"status": int(last.status), "iterations": int(last.iterations),
                       "pcg_iterations_total": int(last.pcg_iterations_total),
                       "objective": last.objective, "r_prim_inf": last.r_prim_inf,
@@ -608,10 +638,14 @@ def main():
             "generation_s": gen_s}
     if not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline(problem, {
+            counts = reference_counts(args.config, args.lambda_pcg) or {
                 "iterations": int(last.iterations),
                 "pcg_iterations_total": int(last.pcg_iterations_total),
-                "equil_passes": int(last.equil_passes)}, cfg=args.config, lam=args.lambda_pcg)
+                "equil_passes": int(last.equil_passes),
+                "source": "this engine's solve (no complete reference solve of this instance "
+                          "is committed)"}
+            line["cpu_baseline"] = cpu_baseline(problem, counts, cfg=args.config,
+                                                lam=args.lambda_pcg)
         except Exception as e:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "error": repr(e)}
     print(json.dumps(line), flush=True)

@@ -270,6 +270,13 @@ int qpcg_nccl_unique_id(void* out);
 
 /* ---- common to both precisions ------------------------------------------ */
 void qpcg_cleanup(qpcg_workspace* ws);
+/* Hands the engine's idle device memory back to the driver: the process-wide
+ * cache of released workspace blocks (at most QPCG_CACHE_MAX_GB, default 32)
+ * and the unused part of the engine's own per-device memory pools (the
+ * devices' default pools are never modified).  Live workspaces keep theirs.
+ * Synchronises every device the engine has used.  No reference counterpart
+ * (the reference frees its std::vectors on return). */
+void qpcg_release_cached_memory(void);
 const char* qpcg_last_error(const qpcg_workspace* ws);
 /* copies up to `cap` records; returns the total number recorded */
 uint32_t qpcg_get_pcg_calls(const qpcg_workspace* ws, qpcg_pcg_call* out,

@@ -13,7 +13,7 @@
 namespace qpcg_b200 {
 
 enum PcgExit : uint32_t { kPcgConverged = 0, kPcgCap = 1, kPcgZeroRhs = 2 };
-enum ErrCode : uint32_t { kErrNone = 0, kErrInvalid = 1, kErrNotPD = 2 };
+enum ErrCode : uint32_t { kErrNone = 0, kErrInvalid = 1, kErrNotPD = 2, kErrRho = 3 };
 
 // Device-resident control block (one per workspace).
 template <typename T>
@@ -1014,7 +1014,7 @@ __device__ void rho_decide(Dev<T> D, T z_inf, bool record = true) {
   }
   C->n_rho += 1;
   if (!(next > T(0))) {
-    C->error = kErrInvalid;  // kkt operator: rho must be positive
+    C->error = kErrRho;  // kkt operator: rho must be positive
     C->done = 1;
     return;
   }

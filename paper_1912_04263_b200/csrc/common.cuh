@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -50,16 +51,50 @@ inline thread_local uint64_t g_launches = 0;
   } while (0)
 
 // ------------------------------------------------------- device memory
-// All engine allocations are stream-ordered from the device's default memory
-// pool with an unbounded release threshold: a solve's ~9 GB (config 2) is
-// recycled from the pool by the next workspace instead of being unmapped and
-// re-mapped (cudaMalloc/cudaFree of multi-GB buffers costs ~100 ms per solve).
+// All engine allocations are stream-ordered from the engine's OWN memory pool
+// per device (cudaMemPoolCreate; the device's default pool, which other
+// cudaMallocAsync users of the process share, is left untouched) with an
+// unbounded release threshold: a solve's ~9 GB (config 2) is recycled from the
+// pool by the next workspace instead of being unmapped and re-mapped
+// (cudaMalloc/cudaFree of multi-GB buffers costs ~100 ms per solve).
+// qpcg_release_cached_memory() hands everything idle back to the driver.
 inline thread_local cudaStream_t g_alloc_stream = nullptr;
-inline void configure_pool(int device) {
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
-  uint64_t thr = ~0ull;
-  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+constexpr int kMaxDevices = 64;
+struct EnginePools {
+  std::mutex mu;
+  cudaMemPool_t pool[kMaxDevices] = {};
+};
+inline EnginePools& engine_pools() {
+  static EnginePools p;
+  return p;
+}
+inline cudaMemPool_t engine_pool(int device) {
+  if (device < 0 || device >= kMaxDevices) return nullptr;
+  EnginePools& P = engine_pools();
+  std::lock_guard<std::mutex> g(P.mu);
+  if (!P.pool[device]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    P.pool[device] = pool;
+  }
+  return P.pool[device];
+}
+inline void configure_pool(int device) { (void)engine_pool(device); }
+inline cudaError_t pool_malloc(void** p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool = engine_pool(dev);
+  if (!pool) return cudaMallocAsync(p, bytes ? bytes : 1, g_alloc_stream);
+  return cudaMallocFromPoolAsync(p, bytes ? bytes : 1, pool, g_alloc_stream);
 }
 // A workspace's long-lived buffers (its matrices, scaled copies and vectors;
 // ~9 GB at config 2) are recycled through a process-wide cache keyed by
@@ -78,7 +113,14 @@ inline BlockCache& block_cache() {
   return c;
 }
 constexpr size_t kCacheMin = size_t(1) << 20;     // smaller buffers: the pool
-constexpr size_t kCacheMax = size_t(96) << 30;    // idle bytes kept at most
+// idle bytes kept at most: 32 GB, or QPCG_CACHE_MAX_GB (0 disables the cache)
+inline size_t cache_max_bytes() {
+  static const size_t v = [] {
+    const char* e = std::getenv("QPCG_CACHE_MAX_GB");
+    return e ? size_t(std::strtoull(e, nullptr, 10)) << 30 : size_t(32) << 30;
+  }();
+  return v;
+}
 inline void cache_flush_idle() {
   BlockCache& c = block_cache();
   std::lock_guard<std::mutex> g(c.mu);
@@ -90,7 +132,7 @@ inline void cache_flush_idle() {
   c.idle_bytes = 0;
 }
 inline cudaError_t cache_get(void** p, size_t bytes) {
-  if (bytes < kCacheMin) return cudaMallocAsync(p, bytes ? bytes : 1, g_alloc_stream);
+  if (bytes < kCacheMin) return pool_malloc(p, bytes);
   int dev = 0;
   cudaGetDevice(&dev);
   BlockCache& c = block_cache();
@@ -104,11 +146,11 @@ inline cudaError_t cache_get(void** p, size_t bytes) {
       return cudaSuccess;
     }
   }
-  cudaError_t e = cudaMallocAsync(p, bytes, g_alloc_stream);
+  cudaError_t e = pool_malloc(p, bytes);
   if (e == cudaErrorMemoryAllocation) {  // idle blocks first, then retry once
     cudaGetLastError();
     cache_flush_idle();
-    e = cudaMallocAsync(p, bytes, g_alloc_stream);
+    e = pool_malloc(p, bytes);
   }
   if (e == cudaSuccess) {
     std::lock_guard<std::mutex> g(c.mu);
@@ -124,7 +166,7 @@ inline void cache_put(void* p) {
     std::lock_guard<std::mutex> g(c.mu);
     auto it = c.owned.find(p);
     if (it != c.owned.end()) {
-      if (c.idle_bytes + it->second.second <= kCacheMax) {
+      if (c.idle_bytes + it->second.second <= cache_max_bytes()) {
         c.idle.emplace(it->second, p);
         c.idle_bytes += it->second.second;
         return;
@@ -142,6 +184,23 @@ inline bool cache_owned(void* p, size_t* bytes) {
   if (it == c.owned.end()) return false;
   *bytes = it->second.second;
   return true;
+}
+
+// qpcg_release_cached_memory(): the idle cached blocks are freed, then every
+// engine pool is trimmed to what live workspaces still hold.
+inline void release_cached_memory() {
+  cache_flush_idle();
+  EnginePools& P = engine_pools();
+  std::lock_guard<std::mutex> g(P.mu);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  for (int d = 0; d < kMaxDevices; ++d) {
+    if (!P.pool[d]) continue;
+    cudaSetDevice(d);
+    cudaDeviceSynchronize();  // frees enqueued on any stream have completed
+    cudaMemPoolTrimTo(P.pool[d], 0);
+  }
+  cudaSetDevice(prev);
 }
 
 // A workspace's arena: every cached block it took, and the ones it already
@@ -181,7 +240,7 @@ inline cudaError_t dmalloc(U** p, size_t bytes) {
     *p = static_cast<U*>(q);
     return cudaSuccess;
   }
-  return cudaMallocAsync(reinterpret_cast<void**>(p), bytes ? bytes : 1, g_alloc_stream);
+  return pool_malloc(reinterpret_cast<void**>(p), bytes);
 }
 inline cudaError_t dfree(void* p) {
   if (!p) return cudaSuccess;

@@ -231,6 +231,7 @@ int qpcg_f32_solve_problem(const qpcg_csr_f32* p, const float* q, const qpcg_csr
                                    msg_len);
 }
 void qpcg_cleanup(qpcg_workspace* ws) { delete ws; }
+void qpcg_release_cached_memory(void) { release_cached_memory(); }
 
 int qpcg_shard_cuts(const uint32_t* row_ptr, uint32_t rows, uint32_t nnz, uint32_t blocks,
                     uint32_t* cuts) {

@@ -1062,10 +1062,8 @@ class Workspace : public IEngine<T> {
   void raise_device_error() {
     if (hc.error == kErrNotPD)
       throw NotPositiveDefinite("pcg: encountered direction of nonpositive curvature");
-    if (hc.error == kErrInvalid) {
-      if (hc.n_rho > 0 && !(hc.rho > T(0))) throw InvalidArgument("kkt operator: rho must be positive");
-      throw InvalidArgument("pcg: warm start must be finite");
-    }
+    if (hc.error == kErrRho) throw InvalidArgument("kkt operator: rho must be positive");
+    if (hc.error == kErrInvalid) throw InvalidArgument("pcg: warm start must be finite");
   }
   void fill_info(qpcg_info* info, double solve_s, double d2h, uint32_t n, uint32_t m) const {
     const bool has_cert = hc.status == 1 || hc.status == 2;
@@ -1460,6 +1458,7 @@ class Workspace : public IEngine<T> {
     }
     if (hc.error == kErrNotPD)
       throw NotPositiveDefinite("pcg: encountered direction of nonpositive curvature");
+    if (hc.error == kErrRho) throw InvalidArgument("kkt operator: rho must be positive");
     if (hc.error == kErrInvalid) throw InvalidArgument("pcg: warm start must be finite");
     k_pcg_fin<T><<<grid_for(n), kThreads, 0, s>>>(D);
     CK_LAUNCH();
@@ -1524,15 +1523,27 @@ class Workspace : public IEngine<T> {
     if (k != ~0ull) throw InvalidArgument(validation_message(k));
     vectors_apply();
   }
+  // Uploads into scratch (the vectors not given are copied from the current
+  // data) and validates there: a rejected update leaves q_o / l_o / u_o and
+  // their scaled copies untouched.  The scratch lives until vectors_apply in
+  // the caller's AllocScope.
+  T *v_q = nullptr, *v_l = nullptr, *v_u = nullptr;
   unsigned long long vectors_stage(const T* q, const T* l, const T* u) {
     const uint32_t n = D.n, m = D.m;
-    if (q) upload(D.q_o, q, sizeof(T) * n);
-    if (l) upload(D.l_o, l, sizeof(T) * m);
-    if (u) upload(D.u_o, u, sizeof(T) * m);
+    v_q = vec(n, false);
+    v_l = vec(m, false);
+    v_u = vec(m, false);
+    auto stage = [&](T* dst, const T* src, const T* cur, uint32_t len) {
+      if (src) upload(dst, src, sizeof(T) * len);
+      else if (len) CK(cudaMemcpyAsync(dst, cur, sizeof(T) * len, cudaMemcpyDeviceToDevice, s));
+    };
+    stage(v_q, q, D.q_o, n);
+    stage(v_l, l, D.l_o, m);
+    stage(v_u, u, D.u_o, m);
     unsigned long long* key = alloc<unsigned long long>(1);
     CK(cudaMemsetAsync(key, 0xff, 8, s));
-    validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(D.q_o, n, kValQFinite, key);
-    validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(D.l_o, D.u_o, m, key, row0);
+    validate_values_kernel<T><<<grid_for(n), kThreads, 0, s>>>(v_q, n, kValQFinite, key);
+    validate_bounds_kernel<T><<<grid_for(m), kThreads, 0, s>>>(v_l, v_u, m, key, row0);
     CK_LAUNCH();
     unsigned long long k;
     CK(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, s));
@@ -1542,6 +1553,9 @@ class Workspace : public IEngine<T> {
   void vectors_apply() {
     const uint32_t n = D.n, m = D.m;
     const T c = hc.c;
+    if (n) CK(cudaMemcpyAsync(D.q_o, v_q, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
+    if (m) CK(cudaMemcpyAsync(D.l_o, v_l, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
+    if (m) CK(cudaMemcpyAsync(D.u_o, v_u, sizeof(T) * m, cudaMemcpyDeviceToDevice, s));
     T *qs = D.q, *qo = D.q_o, *d = D.d, *e = D.e, *ls = D.l, *us = D.u, *lo = D.l_o, *uo = D.u_o;
     for_n(n, [=] __device__(uint32_t i) { qs[i] = c * (d[i] * qo[i]); }, s);
     for_n(m, [=] __device__(uint32_t j) {

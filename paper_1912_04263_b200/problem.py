@@ -45,6 +45,19 @@ class CsrMatrix:
     def view(self) -> _abi.CsrF64:
         return _abi.csr_view(self.values, self.row_ptr, self.col_indices, self.rows, self.cols)
 
+    def checked(self, dtype) -> "CsrMatrix":
+        """The array-length rules of validate(CsrMatrix) (sparse.hpp:100-106)
+        that the C-ABI cannot see (it receives rows / nnz only), with every
+        array coerced to its C type right before a call."""
+        rp = np.ascontiguousarray(self.row_ptr, dtype=np.uint32)
+        ci = np.ascontiguousarray(self.col_indices, dtype=np.uint32)
+        v = np.ascontiguousarray(self.values, dtype=dtype)
+        if rp.ndim != 1 or rp.shape[0] != int(self.rows) + 1:
+            raise ValueError("csr: row_ptr must have rows + 1 entries")
+        if ci.ndim != 1 or v.ndim != 1 or ci.shape[0] != v.shape[0]:
+            raise ValueError("csr: col_indices/value length mismatch")
+        return CsrMatrix(int(self.rows), int(self.cols), v, rp, ci)
+
     def to_scipy(self):
         import scipy.sparse as sp
         return sp.csr_matrix((self.values, self.col_indices.astype(np.int64),
@@ -106,6 +119,32 @@ class QpProblem:
         """runner.hpp:81  N = nnz(P upper) + nnz(A)."""
         return self.p_upper.nnz + self.a.nnz
 
+    def checked(self) -> "QpProblem":
+        """A copy (views where possible) whose arrays all have the problem's
+        dtype and whose lengths satisfy problem.hpp:47-70 / sparse.hpp:100-106,
+        in the reference's order, so that the C-ABI (which receives n, m and
+        nnz only) never reads past a caller's buffer.  The remaining rules
+        (values, bounds, structure) are the engine's and raise the same
+        messages there."""
+        dt = self.dtype
+        if dt not in (np.float64, np.float32):
+            raise TypeError(f"unsupported dtype {dt}")
+        P = self.p_upper.checked(dt)
+        A = self.a.checked(dt)
+        q = np.ascontiguousarray(self.q, dtype=dt)
+        l = np.ascontiguousarray(self.l, dtype=dt)
+        u = np.ascontiguousarray(self.u, dtype=dt)
+        if P.rows == P.cols and P.rows > 0 and A.cols == P.cols:
+            if q.ndim != 1 or q.shape[0] != P.rows:
+                raise ValueError("problem: q length must equal n")
+            if l.ndim != 1 or u.ndim != 1 or l.shape[0] != A.rows or u.shape[0] != A.rows:
+                raise ValueError("problem: bound lengths must equal m")
+        else:  # the engine reports the shape error; keep its reads in bounds
+            q = np.resize(q, max(P.rows, 1)).astype(dt)
+            l = np.resize(l, max(A.rows, 1)).astype(dt)
+            u = np.resize(u, max(A.rows, 1)).astype(dt)
+        return QpProblem(P, q, A, l, u)
+
 
 @dataclass
 class Settings:
@@ -141,9 +180,38 @@ class Settings:
                                                    "scaling_enabled") else float(v))
         return s
 
+    _FLOATS = ("alpha", "sigma", "rho_bar_init", "eps_abs", "eps_rel", "eps_pinf", "eps_dinf",
+               "lambda_pcg", "eps_pcg_min", "eps_equil")
+    _INDICES = ("max_admm_iter", "check_interval", "rho_update_interval", "equil_max_passes")
+
+    def validate(self) -> "Settings":
+        """settings.hpp:44-75 (qpcg_validate_settings): ValueError with the
+        reference's message."""
+        import ctypes as C
+        from .solver import load_library
+        msg = C.create_string_buffer(256)
+        if load_library().qpcg_validate_settings(C.byref(self.to_c()), msg, 256) != _abi.QPCG_OK:
+            raise ValueError(msg.value.decode())
+        return self
+
+    @staticmethod
+    def _json_type(v) -> str:
+        if v is None:
+            return "null"
+        if isinstance(v, bool):
+            return "boolean"
+        if isinstance(v, (int, float)):
+            return "number"
+        if isinstance(v, str):
+            return "string"
+        return "array" if isinstance(v, list) else "object"
+
     @classmethod
     def from_json(cls, obj) -> "Settings":
-        """io.hpp:175-205 settings_from_json: flat keys, unknown key is an error."""
+        """io.hpp:175-205 settings_from_json: flat keys, an unknown key is an
+        error, each value converted as nlohmann's get<T> / get<index_t> /
+        get<bool> / get<std::string> does (a wrong JSON type raises its
+        type_error text), then validate(s) (:203)."""
         import json
         if isinstance(obj, (str, bytes)):
             obj = json.loads(obj)
@@ -151,8 +219,24 @@ class Settings:
         for k, v in obj.items():
             if k not in cls._KEYS:
                 raise RuntimeError(f"settings: unknown key '{k}'")
+            t = cls._json_type(v)
+            if k in cls._FLOATS or k in cls._INDICES:
+                if t != "number":
+                    raise RuntimeError(f"[json.exception.type_error.302] type must be number, "
+                                       f"but is {t}")
+                if k in cls._FLOATS:
+                    v = float(v)
+                else:  # static_cast<uint32_t> of the stored integer / truncated float
+                    v = int(v) & 0xFFFFFFFF
+            elif k == "scaling_enabled":
+                if t != "boolean":
+                    raise RuntimeError(f"[json.exception.type_error.302] type must be boolean, "
+                                       f"but is {t}")
+            elif t != "string":  # precision_note
+                raise RuntimeError(f"[json.exception.type_error.302] type must be string, "
+                                   f"but is {t}")
             setattr(s, k, v)
-        return s
+        return s.validate()
 
 
 @dataclass

@@ -44,6 +44,8 @@ def load_library() -> C.CDLL:
         getattr(lib, f"qpcg_{pre}_solve").argtypes = [vp, vp, vp, vp, vp, vp]
         getattr(lib, f"qpcg_{pre}_solve_problem").argtypes = [vp] * 15 + [C.c_char_p, C.c_size_t]
     lib.qpcg_cleanup.argtypes = [vp]
+    lib.qpcg_release_cached_memory.argtypes = []
+    lib.qpcg_release_cached_memory.restype = None
     lib.qpcg_last_error.argtypes = [vp]
     lib.qpcg_last_error.restype = C.c_char_p
     lib.qpcg_version.restype = C.c_char_p
@@ -57,6 +59,12 @@ def load_library() -> C.CDLL:
     lib.qpcg_nccl_unique_id.argtypes = [vp]
     _lib = lib
     return lib
+
+
+def release_cached_memory() -> None:
+    """Return the engine's idle device memory (released workspaces' cached
+    blocks, unused pool memory) to the driver; live workspaces keep theirs."""
+    load_library().qpcg_release_cached_memory()
 
 
 def _raise(rc: int, msg: str):
@@ -135,6 +143,7 @@ class Workspace:
                  mode: str = "graph", record_diagnostics: bool = False, shards: int = 1,
                  nccl: tuple | None = None, peer: tuple | None = None):
         self.lib = load_library()
+        problem = problem.checked()  # lengths + dtype before any pointer crosses the ABI
         self.problem = problem
         self.dtype = problem.dtype
         self.pre = _pre(self.dtype)
@@ -157,14 +166,19 @@ class Workspace:
             _raise(rc, self.lib.qpcg_last_error(self.ws).decode())
 
     def warm_start(self, x, z, y):
-        a = [np.ascontiguousarray(v, self.dtype) for v in (x, z, y)]
+        a = _warm_arrays(x, z, y, self.problem.n, self.problem.m, self.dtype)
         self._check(getattr(self.lib, f"qpcg_{self.pre}_warm_start")(self.ws, *[_abi.ptr(v) for v in a]))
 
     def update_rho(self, rho: float):
         self._check(getattr(self.lib, f"qpcg_{self.pre}_update_rho")(self.ws, C.c_double(rho)))
 
     def update_vectors(self, q=None, l=None, u=None):
-        a = [None if v is None else np.ascontiguousarray(v, self.dtype) for v in (q, l, u)]
+        a = [None if v is None else np.ascontiguousarray(v, self.dtype).reshape(-1)
+             for v in (q, l, u)]
+        if a[0] is not None and a[0].shape[0] != self.problem.n:
+            raise ValueError("update_vectors: q length must equal n")
+        if any(v is not None and v.shape[0] != self.problem.m for v in a[1:]):
+            raise ValueError("update_vectors: bound lengths must equal m")
         self._check(getattr(self.lib, f"qpcg_{self.pre}_update_vectors")(self.ws, *[_abi.ptr(v) for v in a]))
 
     def solve(self, diag: SolveDiagnostics | None = None):
@@ -194,6 +208,15 @@ class Workspace:
 
     def __exit__(self, *a):
         self.close()
+
+
+def _warm_arrays(x, z, y, n: int, m: int, dtype):
+    """solver.hpp:414-417: a warm start of the wrong size is rejected before
+    any pointer reaches the ABI (finiteness is checked by the engine)."""
+    a = [np.ascontiguousarray(v, dtype).reshape(-1) for v in (x, z, y)]
+    if a[0].shape[0] != n or a[1].shape[0] != m or a[2].shape[0] != m:
+        raise ValueError("solve: warm start dimension mismatch")
+    return a
 
 
 def fetch_diagnostics(lib, ws, diag: SolveDiagnostics):
@@ -229,6 +252,7 @@ def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | N
                 ws.warm_start(initial.x, initial.z, initial.y)
             return ws.solve(diag)
     lib = load_library()
+    p = p.checked()  # lengths + dtype before any pointer crosses the ABI
     pre = _pre(p.dtype)
     n, m = p.n, p.m
     dt = p.dtype
@@ -238,8 +262,8 @@ def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | N
     cert = np.zeros(max(n, m), dt)
     info = _abi.Info()
     pv, av = p.p_upper.view(), p.a.view()
-    w = [None, None, None] if initial is None else [np.ascontiguousarray(v, dt) for v in
-                                                      (initial.x, initial.z, initial.y)]
+    w = [None, None, None] if initial is None else _warm_arrays(initial.x, initial.z, initial.y,
+                                                                  n, m, dt)
     msg = C.create_string_buffer(512)
     rc = getattr(lib, f"qpcg_{pre}_solve_problem")(
         C.addressof(pv), _abi.ptr(p.q), C.addressof(av), _abi.ptr(p.l), _abi.ptr(p.u),

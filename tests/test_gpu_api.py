@@ -40,20 +40,26 @@ def test_repeated_solve_continues_from_state():
 
 def test_update_rho_and_vectors():
     p = G.generate("control", 4, 0)
-    with solver.Workspace(p, S, device=0) as ws:
+    # eps = 1e-5 so that "equals a fresh solve within KKT tolerance" (SURVEY
+    # §8(f) rank 1: the update is not bit-equal to a fresh solve, Ruiz's gamma
+    # depends on q) is held to the north star's 1e-3
+    S5 = Settings(lambda_pcg=0.01, eps_abs=1e-5, eps_rel=1e-5)
+    with solver.Workspace(p, S5, device=0) as ws:
         a = ws.solve()
         ws.update_rho(1.0)
         b = ws.solve()
-        assert b.status == "solved" and kkt_ok(p, b, S)
+        assert b.status == "solved" and kkt_ok(p, b, S5)
         # receding-horizon style update of the bounds
         l2, u2 = p.l * 0.9, p.u * 0.9
         ws.update_vectors(l=l2, u=u2)
         c = ws.solve()
     from paper_1912_04263_b200.problem import QpProblem
     p2 = QpProblem(p.p_upper, p.q, p.a, l2, u2)
-    assert c.status == "solved" and kkt_ok(p2, c, S)
-    fresh = O.oracle_solve(p2, S)
-    assert rel(c.objective, fresh.objective) < 1e-2
+    assert c.status == "solved" and kkt_ok(p2, c, S5)
+    fresh = O.oracle_solve(p2, S5)
+    assert rel(c.objective, fresh.objective) < 1e-3
+    scale = max(1.0, float(np.max(np.abs(fresh.x))))
+    assert float(np.max(np.abs(c.x - fresh.x))) / scale < 1e-3
     with pytest.raises(ValueError, match="rho must be positive"):
         with solver.Workspace(p, S, device=0) as ws:
             ws.update_rho(-1.0)
@@ -102,3 +108,53 @@ def test_reentrant_workspaces():
     a2 = solver.solve(p1, S, device=0)
     assert np.array_equal(a.x, a2.x) and b.status == "solved"
     w1.close(); w2.close()
+
+
+def test_rejected_update_vectors_leaves_the_workspace_unchanged():
+    """A rejected update (l > u) must not leak into the original-data
+    buffers: the next solve equals one on the untouched workspace bit for bit,
+    and a later valid q-only update is accepted."""
+    p = G.generate("control", 4, 0)
+    with solver.Workspace(p, S, device=0) as ws:
+        ws.solve()
+        bad_l = p.u + 1.0
+        with pytest.raises(ValueError, match="l must not exceed u"):
+            ws.update_vectors(l=bad_l)
+        b1 = ws.solve()
+        ws.update_vectors(q=p.q * 1.0)
+        c1 = ws.solve()
+    with solver.Workspace(p, S, device=0) as ws:
+        ws.solve()
+        b2 = ws.solve()
+        ws.update_vectors(q=p.q * 1.0)
+        c2 = ws.solve()
+    assert np.array_equal(b1.x, b2.x) and b1.objective == b2.objective
+    assert np.array_equal(c1.x, c2.x) and c1.status == c2.status
+
+
+def test_update_vectors_length_checked():
+    p = G.generate("lasso", 3, 0)
+    with solver.Workspace(p, S, device=0) as ws:
+        with pytest.raises(ValueError, match="q length must equal n"):
+            ws.update_vectors(q=np.zeros(p.n + 1))
+        with pytest.raises(ValueError, match="bound lengths must equal m"):
+            ws.update_vectors(u=np.zeros(p.m - 1))
+        with pytest.raises(ValueError, match="warm start dimension mismatch"):
+            ws.warm_start(np.zeros(p.n), np.zeros(p.m), np.zeros(p.m + 2))
+        assert ws.solve().status == "solved"
+
+
+def test_release_cached_memory_returns_device_memory():
+    import torch
+    p = G.config("1")
+    solver.solve(p, S, device=0)
+    solver.release_cached_memory()
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info(0)
+    for _ in range(2):
+        solver.solve(p, S, device=0)
+    free1, _ = torch.cuda.mem_get_info(0)
+    solver.release_cached_memory()
+    free2, _ = torch.cuda.mem_get_info(0)
+    assert free2 >= free1
+    assert free2 >= free0 - (64 << 20)  # nothing of the finished solves is kept
