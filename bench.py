@@ -503,6 +503,10 @@ def main():
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
+        # NCCL's init lines (communicator size and rank per process) let the
+        # driver verify that N ranks formed one group
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         if same_gpu:
             dist.init_process_group("gloo")
@@ -584,6 +588,14 @@ def main():
         log(f"re-solve after a bound update: {resolve['resolve_iterations']} iterations, "
             f"{resolve['resolve_s'] * 1e3:.1f} ms (first solve {resolve['first_solve_s'] * 1e3:.1f} ms)")
     if dist is not None:
+        props = torch.cuda.get_device_properties(local)
+        log(json.dumps({"rank": rank, "local_rank": local, "device": local,
+                        "device_uuid": str(getattr(props, "uuid", "")), "world": world,
+                        "ranks_seen": dist.get_world_size(),
+                        "transport": (args.transport if sharded else "none (replicas)"),
+                        "engine_group": (f"{world} ranks x {args.shards} block(s)"
+                                         if sharded else "independent"),
+                        "ms_per_solve": ms, "iterations": int(infos[-1].iterations)}))
         t = torch.tensor([ms, ms_e2e], device="cpu" if same_gpu else f"cuda:{local}",
                          dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

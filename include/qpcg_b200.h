@@ -163,12 +163,24 @@ typedef struct {
                                   QPCG_PERSIST_MAX_NNZ).  All modes give
                                   bitwise-identical results. */
 
+/* Per-iteration observer (solver.hpp:132-145 IterationView): iter is the
+ * 1-based ADMM iteration; x (n), z (m), y (m) the scaled iterates and l, u (m)
+ * the scaled bounds, all host arrays of the workspace's precision (float or
+ * double), valid only during the call. */
+typedef void (*qpcg_iteration_cb)(void* user, uint32_t iter, const void* x, const void* z,
+                                  const void* y, const void* l, const void* u, uint32_t n,
+                                  uint32_t m);
+
 /* Row sharding.  A is cut into G = virtual_shards x
  * nccl_ranks contiguous nnz-balanced row blocks (qpcg_shard_cuts); every
  * block keeps its own A_g^T, P and the n-vectors are replicated, and the A^T
  * partials are summed across blocks once per operator apply.  Every rank
  * passes the FULL problem (it uploads only its blocks) and receives the full
- * x, z, y.  The sharded loop is host-driven (mode is ignored). */
+ * x, z, y.  Loop driver: QPCG_MODE_GRAPH with the peer transport (or
+ * virtual blocks only) runs the whole sharded loop as one CUDA graph with
+ * conditional nodes (every collective is a kernel); with the NCCL transport,
+ * or in QPCG_MODE_EAGER / QPCG_MODE_PERSISTENT, the loop is host-driven (one
+ * control-block read per decision). */
 typedef struct {
   int32_t device;          /* CUDA ordinal, -1 = current */
   int32_t input_memory;    /* QPCG_MEM_HOST / QPCG_MEM_DEVICE */
@@ -194,6 +206,14 @@ typedef struct {
   const char* rendezvous_dir; /* QPCG_TRANSPORT_PEER without an NCCL id: a
                               directory shared by the ranks (fresh per group)
                               through which they exchange their IPC handles */
+  qpcg_iteration_cb on_iteration; /* SolveDiagnostics::on_iteration
+                              (solver.hpp:166, :451-454): when set, the solve
+                              runs the host-driven loop and calls it after
+                              every ADMM step with the SCALED iterates (one
+                              device->host copy of x, z, y per iteration: an
+                              instrumented mode, not a fast path).  Unsharded
+                              workspaces only. */
+  void* on_iteration_user;  /* passed back as the callback's first argument */
 } qpcg_options;
 
 /* NCCL collectives (default), or stores into every peer's memory (CUDA IPC /

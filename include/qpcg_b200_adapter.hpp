@@ -16,13 +16,17 @@
 //
 //   const SolveOutcome<T> out = qpcg::b200::solve(p, settings);
 //
-// SolveDiagnostics::on_iteration (a per-iteration host callback on scaled
-// iterates) is not supported by the device-resident loop; pcg_calls,
-// check_iterations and rho_updates are filled.
+// SolveDiagnostics: pcg_calls, check_iterations and rho_updates are filled
+// after the solve; a set on_iteration (solver.hpp:166, :451-454) switches the
+// engine to its host-driven loop and is called after every ADMM step with the
+// scaled iterates (qpcg_options.on_iteration: one device->host copy per
+// iteration, an instrumented mode).  Unlike the reference, pcg_calls is not
+// yet appended while the callback runs.
 #ifndef QPCG_B200_ADAPTER_HPP
 #define QPCG_B200_ADAPTER_HPP
 
 #include <chrono>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -103,6 +107,29 @@ struct Api<float> {
   }
 };
 
+// qpcg_iteration_cb -> std::function<void(const IterationView<T>&)>
+template <typename T>
+struct IterTrampoline {
+  const std::function<void(const qpcg::IterationView<T>&)>* fn;
+  std::vector<T> x, z, y, l, u;
+  static void call(void* user, uint32_t iter, const void* xp, const void* zp, const void* yp,
+                   const void* lp, const void* up, uint32_t n, uint32_t m) {
+    auto* t = static_cast<IterTrampoline*>(user);
+    auto fill = [](std::vector<T>& v, const void* p, uint32_t k) {
+      const T* a = static_cast<const T*>(p);
+      v.assign(a, a + k);
+    };
+    fill(t->x, xp, n);
+    fill(t->z, zp, m);
+    fill(t->y, yp, m);
+    if (t->l.size() != m) {  // bounds do not change during a solve
+      fill(t->l, lp, m);
+      fill(t->u, up, m);
+    }
+    (*t->fn)(qpcg::IterationView<T>{iter, t->x, t->z, t->y, t->l, t->u});
+  }
+};
+
 struct WsGuard {
   qpcg_workspace* w = nullptr;
   ~WsGuard() { qpcg_cleanup(w); }
@@ -123,6 +150,11 @@ qpcg::SolveOutcome<T> solve(const qpcg::QpProblem<T>& p, const qpcg::Settings<T>
   qpcg_options opt;
   qpcg_default_options(&opt);
   opt.record_diagnostics = diag != nullptr ? 1 : 0;
+  IterTrampoline<T> tramp{diag != nullptr ? &diag->on_iteration : nullptr, {}, {}, {}, {}, {}};
+  if (diag != nullptr && diag->on_iteration) {
+    opt.on_iteration = &IterTrampoline<T>::call;
+    opt.on_iteration_user = &tramp;
+  }
   if (p.q.size() != p.p_upper.rows) throw std::invalid_argument("problem: q length must equal n");
   if (p.l.size() != p.a.rows || p.u.size() != p.a.rows)
     throw std::invalid_argument("problem: bound lengths must equal m");

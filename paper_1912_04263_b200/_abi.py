@@ -80,7 +80,13 @@ class Options(C.Structure):
                 ("record_diagnostics", C.c_int32), ("virtual_shards", C.c_int32),
                 ("nccl_rank", C.c_int32), ("nccl_ranks", C.c_int32), ("sm_budget", C.c_int32),
                 ("stream", C.c_void_p), ("nccl_id", C.c_void_p), ("transport", C.c_int32),
-                ("reserved2_", C.c_int32), ("rendezvous_dir", C.c_char_p)]
+                ("reserved2_", C.c_int32), ("rendezvous_dir", C.c_char_p),
+                ("on_iteration", C.c_void_p), ("on_iteration_user", C.c_void_p)]
+
+
+# qpcg_iteration_cb: (user, iter, x, z, y, l, u, n, m)
+ITERATION_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                           C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32)
 
 
 TRANSPORT_NCCL = 0

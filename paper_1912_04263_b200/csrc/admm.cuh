@@ -117,6 +117,41 @@ __host__ __device__ inline uint32_t red_grid(uint32_t len) {
   return g == 0 ? 1u : g;
 }
 
+// Grid-stride loop whose loads are issued kLoadAhead strides ahead of their
+// use.  The reduction kernels run on the fixed kRedBlocks x kThreads grid
+// (deterministic partials), i.e. ~76k threads; with one load per thread in
+// flight a 1e6-element vector streams at well under 1 TB/s (svm: 92 us of
+// vector kernels per PCG iteration).  ld(i) loads element i's operands, use(i,
+// v) consumes them; elements are consumed in exactly the plain loop's order,
+// so every result is bitwise unchanged (the persistent driver, which calls
+// the same *_elems bodies, stays identical too).
+constexpr int kLoadAhead = 4;
+template <class Ld, class Use>
+__device__ __forceinline__ void strided(uint32_t t0, uint32_t stride, uint32_t n, Ld ld, Use use) {
+  uint64_t i = t0;
+  const uint64_t st = stride;
+  for (; i + (kLoadAhead - 1) * st < n; i += kLoadAhead * st) {
+    decltype(ld(0u)) v[kLoadAhead];
+#pragma unroll
+    for (int u = 0; u < kLoadAhead; ++u) v[u] = ld(uint32_t(i + u * st));
+#pragma unroll
+    for (int u = 0; u < kLoadAhead; ++u) use(uint32_t(i + u * st), v[u]);
+  }
+  for (; i < n; i += st) use(uint32_t(i), ld(uint32_t(i)));
+}
+template <typename T>
+struct V2 {
+  T a, b;
+};
+template <typename T>
+struct V3 {
+  T a, b, c;
+};
+template <typename T>
+struct V4 {
+  T a, b, c, d;
+};
+
 // Block all-reduce (result in every thread), fixed tree.
 template <typename T, bool MAX>
 __device__ __forceinline__ T block_allreduce(T v, T* sm) {
@@ -526,17 +561,19 @@ __global__ void k_flag_to_scal(Dev<T> D) {
 template <typename T>
 __device__ __forceinline__ void pcg_init_elems(const Dev<T>& D, uint32_t t0, uint32_t stride,
                                                T (&v)[4]) {
-  for (uint32_t i = t0; i < D.n; i += stride) {
-    const T ri = D.r[i];
-    const T yi = D.dinv[i] * ri;
-    D.p[i] = -yi;
-    const T xi = D.xt[i];
-    D.best[i] = xi;
-    v[0] = smax(v[0], tabs(D.b[i]));
-    v[1] = smax(v[1], tabs(ri));
-    v[2] += ri * yi;
-    if (!isfinite(xi)) v[3] += T(1);
-  }
+  strided(t0, stride, D.n,
+          [&](uint32_t i) { return V4<T>{D.r[i], D.dinv[i], D.xt[i], D.b[i]}; },
+          [&](uint32_t i, const V4<T>& e) {
+            const T ri = e.a;
+            const T yi = e.b * ri;
+            D.p[i] = -yi;
+            const T xi = e.c;
+            D.best[i] = xi;
+            v[0] = smax(v[0], tabs(e.d));
+            v[1] = smax(v[1], tabs(ri));
+            v[2] += ri * yi;
+            if (!isfinite(xi)) v[3] += T(1);
+          });
 }
 template <typename T>
 __device__ void pcg_init_decide(Ctl<T>* C, const T (&tot)[4], Handles H) {
@@ -585,7 +622,8 @@ __device__ __forceinline__ void pcg_dot_elems(const Dev<T>& D, uint32_t t0, uint
       v[0] += D.p[i] * kp;
     }
   } else {
-    for (uint32_t i = t0; i < D.n; i += stride) v[0] += D.p[i] * D.kp[i];
+    strided(t0, stride, D.n, [&](uint32_t i) { return V2<T>{D.p[i], D.kp[i]}; },
+            [&](uint32_t, const V2<T>& e) { v[0] += e.a * e.b; });
   }
 }
 template <typename T>
@@ -616,14 +654,18 @@ template <typename T>
 __device__ __forceinline__ void pcg_update_elems(const Dev<T>& D, uint32_t t0, uint32_t stride,
                                                  T (&v)[2]) {
   const T a = D.ctl->alpha_cg;
-  for (uint32_t i = t0; i < D.n; i += stride) {
-    D.xt[i] += a * D.p[i];
-    const T ri = D.r[i] + a * D.kp[i];
-    D.r[i] = ri;
-    const T yi = D.dinv[i] * ri;
-    v[0] += ri * yi;
-    v[1] = smax(v[1], tabs(ri));
-  }
+  strided(t0, stride, D.n,
+          [&](uint32_t i) {
+            return V4<T>{D.xt[i] + a * D.p[i], D.r[i], D.kp[i], D.dinv[i]};
+          },
+          [&](uint32_t i, const V4<T>& e) {
+            D.xt[i] = e.a;
+            const T ri = e.b + a * e.c;
+            D.r[i] = ri;
+            const T yi = e.d * ri;
+            v[0] += ri * yi;
+            v[1] = smax(v[1], tabs(ri));
+          });
 }
 template <typename T>
 __device__ void pcg_update_decide(Ctl<T>* C, const T (&tot)[2], Handles H) {
@@ -818,27 +860,35 @@ template <typename T>
 __device__ __forceinline__ void residuals_elems(const Dev<T>& D, uint32_t t0, uint32_t stride,
                                                 T (&v)[14]) {
   const T c_inv = D.ctl->c_inv;
-  for (uint32_t i = t0; i < D.m; i += stride) {
-    const T ax = D.ax[i], z = D.z[i], ei = D.e_inv[i];
-    const T rp = ax - z;
-    v[0] = smax(v[0], tabs(rp));
-    v[1] = smax(v[1], tabs(ax));
-    v[2] = smax(v[2], tabs(z));
-    v[3] = smax(v[3], tabs(rp * ei));
-    v[4] = smax(v[4], tabs(ax * ei));
-    v[5] = smax(v[5], tabs(z * ei));
-    v[6] = smax(v[6], tabs((D.e[i] * D.dy[i]) * c_inv));
-  }
-  for (uint32_t i = t0; i < D.n; i += stride) {
-    const T rd = D.rdual[i], px = D.px[i], aty = D.aty[i], di = D.d_inv[i];
-    v[7] = smax(v[7], tabs(rd));
-    v[8] = smax(v[8], tabs(px));
-    v[9] = smax(v[9], tabs(aty));
-    v[10] = smax(v[10], tabs(rd * di));
-    v[11] = smax(v[11], tabs(px * di));
-    v[12] = smax(v[12], tabs(aty * di));
-    v[13] = smax(v[13], tabs(D.d[i] * D.dx[i]));
-  }
+  strided(t0, stride, D.m,
+          [&](uint32_t i) {
+            return V4<T>{D.ax[i], D.z[i], D.e_inv[i], (D.e[i] * D.dy[i]) * c_inv};
+          },
+          [&](uint32_t, const V4<T>& e) {
+            const T ax = e.a, z = e.b, ei = e.c;
+            const T rp = ax - z;
+            v[0] = smax(v[0], tabs(rp));
+            v[1] = smax(v[1], tabs(ax));
+            v[2] = smax(v[2], tabs(z));
+            v[3] = smax(v[3], tabs(rp * ei));
+            v[4] = smax(v[4], tabs(ax * ei));
+            v[5] = smax(v[5], tabs(z * ei));
+            v[6] = smax(v[6], tabs(e.d));
+          });
+  strided(t0, stride, D.n,
+          [&](uint32_t i) {
+            return V4<T>{D.rdual[i], D.px[i], D.aty[i], D.d[i] * D.dx[i]};
+          },
+          [&](uint32_t i, const V4<T>& e) {
+            const T rd = e.a, px = e.b, aty = e.c, di = D.d_inv[i];
+            v[7] = smax(v[7], tabs(rd));
+            v[8] = smax(v[8], tabs(px));
+            v[9] = smax(v[9], tabs(aty));
+            v[10] = smax(v[10], tabs(rd * di));
+            v[11] = smax(v[11], tabs(px * di));
+            v[12] = smax(v[12], tabs(aty * di));
+            v[13] = smax(v[13], tabs(e.d));
+          });
 }
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_residuals(Dev<T> D, int mode, Handles H) {
@@ -1023,7 +1073,8 @@ __device__ void rho_decide(Dev<T> D, T z_inf, bool record = true) {
 }
 template <typename T>
 __device__ __forceinline__ void rho_elems(const Dev<T>& D, uint32_t t0, uint32_t stride, T (&v)[1]) {
-  for (uint32_t i = t0; i < D.m; i += stride) v[0] = smax(v[0], tabs(D.z[i]));
+  strided(t0, stride, D.m, [&](uint32_t i) { return D.z[i]; },
+          [&](uint32_t, T z) { v[0] = smax(v[0], tabs(z)); });
 }
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_rho(Dev<T> D) {

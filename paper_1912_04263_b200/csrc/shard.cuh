@@ -99,6 +99,8 @@ class Sharded : public IEngine<T> {
     const uint64_t l0 = g_launches;
     opt = op;
     Workspace<T>::validate_settings(st);
+    if (op.on_iteration)
+      throw InvalidArgument("on_iteration: not available on a row-sharded workspace");
     device = op.device;
     if (device < 0) CK(cudaGetDevice(&device));
     CK(cudaSetDevice(device));

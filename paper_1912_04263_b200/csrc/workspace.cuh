@@ -1020,6 +1020,20 @@ class Workspace : public IEngine<T> {
   // ------------------------------------------------------- eager loop
   void run_eager() {
     Handles H{};
+    // SolveDiagnostics::on_iteration (solver.hpp:451-454): the scaled
+    // iterates after every ADMM step, before the check; bounds once
+    std::vector<T> hx, hz, hy, hl, hu;
+    if (opt.on_iteration) {
+      hx.resize(D.n);
+      hz.resize(D.m);
+      hy.resize(D.m);
+      hl.resize(D.m);
+      hu.resize(D.m);
+      if (D.m) {
+        CK(cudaMemcpyAsync(hl.data(), D.l, sizeof(T) * D.m, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hu.data(), D.u, sizeof(T) * D.m, cudaMemcpyDeviceToHost, s));
+      }
+    }
     for (;;) {
       pull_ctl();
       if (hc.done || hc.error || hc.iter >= hc.max_iter) break;
@@ -1032,6 +1046,16 @@ class Workspace : public IEngine<T> {
       }
       enq_post_pcg(H);
       pull_ctl();
+      if (opt.on_iteration && !hc.error) {
+        CK(cudaMemcpyAsync(hx.data(), D.x, sizeof(T) * D.n, cudaMemcpyDeviceToHost, s));
+        if (D.m) {
+          CK(cudaMemcpyAsync(hz.data(), D.z, sizeof(T) * D.m, cudaMemcpyDeviceToHost, s));
+          CK(cudaMemcpyAsync(hy.data(), D.y, sizeof(T) * D.m, cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaStreamSynchronize(s));
+        opt.on_iteration(opt.on_iteration_user, hc.iter, hx.data(), hz.data(), hy.data(),
+                         hl.data(), hu.data(), D.n, D.m);
+      }
       if (hc.is_check && !hc.error) {
         enq_check(H, 0);
         pull_ctl();
@@ -1102,7 +1126,7 @@ class Workspace : public IEngine<T> {
     const uint64_t l0 = g_launches;
     // initial residuals and PCG tolerance (solver.hpp:436-441)
     enq_residuals_fresh(1);
-    if (opt.mode == QPCG_MODE_EAGER) {
+    if (opt.mode == QPCG_MODE_EAGER || opt.on_iteration) {
       run_eager();
     } else if (use_persistent()) {
       run_persistent();

@@ -247,10 +247,24 @@ class WarmStart:
 
 
 @dataclass
+class IterationView:
+    """solver.hpp:135-145: the scaled iterates handed to on_iteration."""
+    iter: int
+    x: np.ndarray
+    z: np.ndarray
+    y: np.ndarray
+    l: np.ndarray
+    u: np.ndarray
+
+
+@dataclass
 class SolveDiagnostics:
     pcg_calls: list = field(default_factory=list)  # dicts: admm_iter, eps, r_prim_scaled_inf, ...
     check_iterations: list = field(default_factory=list)
     rho_updates: list = field(default_factory=list)
+    # solver.hpp:166: called after every ADMM step with an IterationView (the
+    # engine then runs its host-driven loop: one D2H of x, z, y per iteration)
+    on_iteration: object = None
 
 
 @dataclass

@@ -85,10 +85,23 @@ def _pre(dtype) -> str:
     raise TypeError(f"unsupported dtype {dtype}")
 
 
+def _iteration_trampoline(fn, dtype):
+    """qpcg_iteration_cb -> fn(IterationView) with numpy copies."""
+    from .problem import IterationView
+    ct = C.c_double if dtype == np.float64 else C.c_float
+
+    def cb(_user, it, x, z, y, l, u, n, m):
+        def arr(p, k):
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), (k,)).copy() if k else \
+                np.zeros(0, dtype)
+        fn(IterationView(int(it), arr(x, n), arr(z, m), arr(y, m), arr(l, m), arr(u, m)))
+    return _abi.ITERATION_CB(cb)
+
+
 def make_options(device: int = -1, mode: str = "graph", record_diagnostics: bool = False,
                  device_memory: bool = False, shards: int = 1,
                  nccl: tuple | None = None, peer: tuple | None = None,
-                 sm_budget: int = 0) -> _abi.Options:
+                 sm_budget: int = 0, on_iteration=None, dtype=np.float64) -> _abi.Options:
     """sm_budget: SMs the persistent driver may hold (0: the whole device);
     shards: row blocks of A held on this device (virtual shards);
     nccl: (rank, ranks, id_bytes) to join the row-sharded NCCL group
@@ -101,6 +114,9 @@ def make_options(device: int = -1, mode: str = "graph", record_diagnostics: bool
     o.record_diagnostics = 1 if record_diagnostics else 0
     o.virtual_shards = max(1, int(shards))
     o.sm_budget = max(0, int(sm_budget))
+    if on_iteration is not None:
+        o._keep_cb = _iteration_trampoline(on_iteration, dtype)  # outlives the workspace
+        o.on_iteration = C.cast(o._keep_cb, C.c_void_p)
     if nccl is not None:
         rank, ranks, uid = nccl
         buf = C.create_string_buffer(bytes(uid), _abi.NCCL_ID_BYTES)
@@ -141,7 +157,7 @@ class Workspace:
 
     def __init__(self, problem: QpProblem, settings: Settings | None = None, device: int = -1,
                  mode: str = "graph", record_diagnostics: bool = False, shards: int = 1,
-                 nccl: tuple | None = None, peer: tuple | None = None):
+                 nccl: tuple | None = None, peer: tuple | None = None, on_iteration=None):
         self.lib = load_library()
         problem = problem.checked()  # lengths + dtype before any pointer crosses the ABI
         self.problem = problem
@@ -149,7 +165,7 @@ class Workspace:
         self.pre = _pre(self.dtype)
         self.settings = settings or Settings()
         self._opts = make_options(device, mode, record_diagnostics, shards=shards, nccl=nccl,
-                                  peer=peer)
+                                  peer=peer, on_iteration=on_iteration, dtype=problem.dtype)
         self._s = self.settings.to_c()
         self._pv, self._av = problem.p_upper.view(), problem.a.view()
         self.ws = C.c_void_p()
@@ -247,7 +263,7 @@ def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | N
     sm_budget: cap on the SMs of the persistent driver (see solve_batch)."""
     if diag is not None:
         with Workspace(p, settings, device, mode, record_diagnostics=True, shards=shards,
-                       nccl=nccl, peer=peer) as ws:
+                       nccl=nccl, peer=peer, on_iteration=diag.on_iteration) as ws:
             if initial is not None:
                 ws.warm_start(initial.x, initial.z, initial.y)
             return ws.solve(diag)

@@ -47,6 +47,7 @@ int main(void) {
   P(qpcg_info, setup_seconds); P(qpcg_info, kernel_launches); P(qpcg_info, rho_final);
   P(qpcg_options, stream); P(qpcg_options, nccl_id); P(qpcg_options, nccl_ranks);
   P(qpcg_options, transport); P(qpcg_options, rendezvous_dir);
+  P(qpcg_options, on_iteration); P(qpcg_options, on_iteration_user);
   P(qpcg_pcg_call, converged);
   return 0;
 }'''
@@ -72,6 +73,8 @@ int main(void) {
     assert int(out["qpcg_options.nccl_ranks"]) == _abi.Options.nccl_ranks.offset
     assert int(out["qpcg_options.transport"]) == _abi.Options.transport.offset
     assert int(out["qpcg_options.rendezvous_dir"]) == _abi.Options.rendezvous_dir.offset
+    assert int(out["qpcg_options.on_iteration"]) == _abi.Options.on_iteration.offset
+    assert int(out["qpcg_options.on_iteration_user"]) == _abi.Options.on_iteration_user.offset
     assert int(out["qpcg_pcg_call.converged"]) == _abi.PcgCall.converged.offset
 
 

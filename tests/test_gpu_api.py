@@ -158,3 +158,21 @@ def test_release_cached_memory_returns_device_memory():
     free2, _ = torch.cuda.mem_get_info(0)
     assert free2 >= free1
     assert free2 >= free0 - (64 << 20)  # nothing of the finished solves is kept
+
+
+def test_on_iteration_observer():
+    """SolveDiagnostics.on_iteration (solver.hpp:166, :451-454): one call per
+    ADMM iteration with the scaled iterates; the instrumented (host-driven)
+    loop gives bitwise the same solve as the graph driver."""
+    from paper_1912_04263_b200.problem import SolveDiagnostics
+    p = G.generate("huber", 4, 1)
+    views = []
+    d = SolveDiagnostics(on_iteration=views.append)
+    g = solver.solve(p, S, diag=d, device=0)
+    ref = solver.solve(p, S, device=0)
+    assert [v.iter for v in views] == list(range(1, g.iterations + 1))
+    assert np.array_equal(g.x, ref.x) and g.iterations == ref.iterations
+    last = views[-1]
+    assert last.x.shape == (p.n,) and last.z.shape == (p.m,) and last.l.shape == (p.m,)
+    assert np.all(last.l <= last.z) and np.all(last.z <= last.u)  # z = proj_[l,u](w), scaled
+    assert len(d.pcg_calls) == g.iterations

@@ -39,8 +39,12 @@ def check_parity(p, s, g, o, tol=1e-3):
             g5, o5 = solver.solve(p, s5, device=0), O.oracle_solve(p, s5)
             assert g5.status == o5.status, (g5.status, o5.status, ro, no, rx, nx)
             if o5.status == "solved":
-                assert rel(g5.objective, o5.objective) <= tol, (rel(g5.objective, o5.objective), ro, no)
-                assert xrel(g5.x, o5.x) <= 10 * tol, (xrel(g5.x, o5.x), rx, nx)
+                ro5, rx5 = rel(g5.objective, o5.objective), xrel(g5.x, o5.x)
+                if ro5 > tol or rx5 > tol:  # the oracle's own noise at eps = 1e-5
+                    t5 = O.oracle_solve(reversed_twin(p), s5)
+                    no5, nx5 = rel(t5.objective, o5.objective), xrel(t5.x, o5.x)
+                    assert ro5 <= max(tol, 2 * no5), (ro5, no5, ro, no)
+                    assert rx5 <= max(tol, 2 * nx5), (rx5, nx5, rx, nx)
     elif o.status in ("primal_infeasible", "dual_infeasible"):
         assert g.objective == o.objective
         assert np.allclose(g.certificate, o.certificate, atol=1e-6)
@@ -58,14 +62,16 @@ def test_classes_f64(cls, scale):
 
 
 @pytest.mark.parametrize("cls", G.CLASSES)
-def test_classes_f32(cls):
-    p = G.generate(cls, 4, 0).astype(np.float32)
-    s = Settings(lambda_pcg=0.01, eps_abs=3e-3, eps_rel=3e-3)  # SPEC acceptance 10
-    g = solver.solve(p, s, device=0)
-    o = O.oracle_solve(p, s)
-    assert g.status == o.status
-    if o.status == "solved":
-        assert rel(g.objective, o.objective) < 3e-2
+@pytest.mark.parametrize("scale", [3, 5, 7])
+def test_classes_f32(cls, scale):
+    """fp32 engine against the fp32 oracle (SPEC acceptance 10; fp32 is
+    compared with fp32) under the same protocol as fp64:
+    objective and x within 1e-3, or within 2x the fp32 oracle's reorder noise,
+    KKT re-check on the original data."""
+    p = G.generate(cls, scale, 0).astype(np.float32)
+    g = solver.solve(p, S, device=0)
+    o = O.oracle_solve(p, S)
+    check_parity(p, S, g, o)
 
 
 @pytest.mark.parametrize("cls", ["lasso", "svm", "random", "control"])
@@ -136,17 +142,54 @@ GOLD_CONFIGS = sorted(f[len("config"):-len("_reference_solve.json")]
 
 @pytest.mark.parametrize("cfg", GOLD_CONFIGS)
 def test_full_size_config_against_reference_run(cfg):
-    """BASELINE configs at full size (1.4e8-1.5e8 nnz) against the reference's own
+    """BASELINE configs at full size (1.0e8-1.5e8 nnz) against the reference's own
     completed solve of the identical instance (tests/golden/config*_reference_solve.json,
-    produced by scripts/ref_solve_config.py: 5-6 minutes on one CPU core each)."""
+    produced by scripts/ref_solve_config.py: minutes on one CPU core each; the
+    _f32 anchors are the reference instantiated with T = float)."""
     ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
                                       f"config{cfg}_reference_solve.json")))
-    p = G.config(cfg)
+    f32 = cfg.endswith("_f32")
+    p = G.config(cfg[:-4] if f32 else cfg, dtype=np.float32 if f32 else np.float64)
     s = Settings(lambda_pcg=ref["lambda_pcg"])
     g = solver.solve(p, s, device=0)
     assert g.status == ref["status"] == "solved"
+    xs = g.x[::ref["x_sample_stride"]].astype(np.float64)
+    xdiff = np.max(np.abs(xs - np.array(ref["x_sample"]))) / max(1.0, ref["x_inf"])
+    if f32:  # north-star tolerance: objective and x within 1e-3
+        assert rel(g.objective, ref["objective"]) < 1e-3
+        assert xdiff <= 1e-3
+        assert kkt_ok(p, g, s, 2.0)
+        return
     assert abs(g.iterations - ref["iterations"]) <= 5
     assert rel(g.objective, ref["objective"]) < 1e-6
-    xs = g.x[::ref["x_sample_stride"]]
-    assert np.max(np.abs(xs - np.array(ref["x_sample"]))) <= 1e-4 * max(1.0, ref["x_inf"])
+    assert xdiff <= 1e-4
     assert kkt_ok(p, g, s)
+
+
+DEFAULT_CONFIGS = sorted(f[len("config"):-len("_reference_defaults.json")]
+                         for f in os.listdir(os.path.join(os.path.dirname(__file__), "golden"))
+                         if f.startswith("config") and f.endswith("_reference_defaults.json"))
+
+
+@pytest.mark.parametrize("cfg", DEFAULT_CONFIGS)
+def test_full_size_defaults_against_reference(cfg):
+    """every config also at PURE DEFAULT settings (lambda_pcg =
+    0.15, where the reference diverges), against the reference's own
+    run of the identical full-size instance with the loop capped
+    (tests/golden/config*_reference_defaults.json, scripts/ref_defaults_trajectory.py):
+    same status and iteration count, the same PCG iteration counts for the
+    first calls, the same adaptive tolerances until the trajectory turns
+    chaotic."""
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                      f"config{cfg}_reference_defaults.json")))
+    p = G.config(cfg)
+    s = Settings(max_admm_iter=ref["max_admm_iter"])
+    d = SolveDiagnostics()
+    g = solver.solve(p, s, device=0, diag=d)
+    assert g.status == ref["status"]
+    assert g.iterations == ref["iterations"]
+    rc = ref["pcg_calls"]
+    k = min(len(rc), len(d.pcg_calls), 10)
+    assert [c["iterations"] for c in d.pcg_calls[:k]] == [c["iterations"] for c in rc[:k]]
+    for a, b in zip(d.pcg_calls[:3], rc[:3]):
+        assert a["eps"] == pytest.approx(b["eps"], rel=1e-6)
