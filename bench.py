@@ -244,7 +244,7 @@ class Engine:
         if rc != 0:
             raise RuntimeError(self.lib.qpcg_last_error(None).decode())
         try:
-            out = np.zeros(9)
+            out = np.zeros(12)
             self.lib.qpcg_bench_kernels.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
             rc = self.lib.qpcg_bench_kernels(ws, reps, out.ctypes.data)
             if rc != 0:
@@ -383,41 +383,18 @@ def peaks() -> dict:
         return {"hbm_gbs": 6650.0, "source": "fallback"}
 
 
-def ncu_traffic(config: str):
+def ncu_traffic(config: str, dtype: str = "f64", kernel: str = "EpiKp"):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu capture of this config (profiles/ncu_summary.json, written by
+    scripts/ncu_summarize.py; key <config> or <config>_f32)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        return d.get(config, {}).get("at_pass_dram_bytes")
+        rec = d.get(config if dtype == "f64" else f"{config}_f32", {})
+        k = rec.get("kernels", {}).get(kernel)
+        return k.get("dram_bytes") if k else None
     except Exception:
         return None
-
-
-def config_dict(args, problem, world: int, sharded: bool) -> dict:
-    """The workload description both arms print (identical dicts)."""
-    S = 8 if args.dtype == "f64" else 4
-    a_bytes = problem.a.nnz * (S + 4) * 2
-    return {"workload": WORKLOADS[args.config], "config_id": args.config,
-            "n": problem.n, "m": problem.m, "nnz_P_upper": problem.p_upper.nnz,
-            "nnz_A": problem.a.nnz, "settings": {"lambda_pcg": args.lambda_pcg},
-            "parallelism": (f"rowshard{world}-{args.transport}" if sharded else f"replicas{world}")
-                           if world > 1 else
-                           ("single" if args.shards <= 1 else f"virtual-rowshard{args.shards}"),
-            "l2": ("inputs larger than L2 (A and A^T streams ~%.1f GB per PCG iteration)"
-                   % (a_bytes / 1e9)) if a_bytes >= (256 << 20) else
-                  "matrices fit in L2: a 512 MB buffer is overwritten before every timed step",
-            "mode": args.mode}
-
-
-def reference_problem(config: str):
-    """The instance generated by the REFERENCE's own generators (oracle/_ref:
-    bench::detail recipes / bench::generate, generators.hpp) — bit-identical to
-    the engine arm's native generator (tests/test_generators.py)."""
-    from oracle import oracle as O  # reference arm only
-    from paper_1912_04263_b200.generators import CONFIGS
-    spec = CONFIGS[config]
-    if spec[0] == "class":
-        return O.ref_generate(spec[1], spec[2], 0)
-    return O.ref_generate_explicit(*spec, seed=0)
 
 
 # --------------------------------------------------------------- arms
@@ -608,25 +585,50 @@ def main():
     pk = peaks()
     S = 8 if dtype == np.float64 else 4
     at_ms, pcg_ms = kt[1], kt[2]
-    achieved = kt[4] / (at_ms * 1e-3) / 1e9
+    gram = kt[9] > 0  # the one-pass operator apply (csrc/gram.cuh) runs the PCG iterations
+    hbm = pk["hbm_gbs"]
+    rate = lambda b, t_ms: b / (t_ms * 1e-3) / 1e9  # noqa: E731
+    if gram:
+        # dominant kernel: k_gram (t = rho A p and the partial windows of A^T t
+        # in one pass over A).  Algorithmic bytes (§8(d) style, 4-byte
+        # indices): MB(A) + S n (p) + S m (t) + S G W (partial windows) =
+        # kt[10] with the index bytes at 4 instead of the 2 streamed
+        S_ = 8 if dtype == np.float64 else 4
+        nnz_a = problem.a.nnz
+        alg = kt[10] + 2.0 * nnz_a  # 16-bit in-window offsets counted at 4 bytes
+        kern = {"kernel": "k_gram: one pass over A forming t = rho A p and A^T t's window "
+                          "partials (PCG operator apply, csrc/gram.cuh)",
+                "achieved": rate(alg, kt[9]), "algorithmic_bytes_per_launch": alg,
+                "launch_ms": kt[9]}
+    else:
+        kern = {"kernel": "spmv A^T pass of the PCG operator (Kp = P p + sigma p + A^T t)"
+                          + (" on rank 0's row block" if sharded or args.shards > 1 else ""),
+                "achieved": rate(kt[4], at_ms), "algorithmic_bytes_per_launch": kt[4],
+                "launch_ms": at_ms}
+    achieved = kern["achieved"]
     loop_s = last.solve_seconds
-    roofline = {"bound": "hbm", "kernel": "spmv A^T pass of the PCG operator (Kp = P p + sigma p + A^T t)"
-                + (" on rank 0's row block" if sharded or args.shards > 1 else ""),
-                "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "peak_source": pk["source"],
-                "traffic": None if (sharded or args.shards > 1) else ncu_traffic(args.config),
-                "algorithmic_bytes_per_launch": kt[4], "launch_ms": at_ms,
-                "a_pass": {"ms": kt[0], "bytes": kt[3], "achieved": kt[3] / (kt[0] * 1e-3) / 1e9},
+    roofline = {"bound": "hbm", **kern, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "peak_source": pk["source"],
+                "traffic": None if (sharded or args.shards > 1) else
+                           ncu_traffic(args.config, args.dtype, "k_gram" if gram else "EpiKp"),
+                "operator_path": "one-pass (k_gram)" if gram else "two-pass (A, A^T SpMV)",
+                "a_pass": {"ms": kt[0], "bytes": kt[3], "achieved": rate(kt[3], kt[0])},
+                "at_pass": {"ms": at_ms, "bytes": kt[4], "achieved": rate(kt[4], at_ms)},
+                # SURVEY §8(d)'s B_pcg counts BOTH matrix streams; on the one-pass
+                # path A^T's window rows are never read, so this is an
+                # EFFECTIVE rate (it may exceed the peak); format_bytes has the
+                # bytes actually streamed
                 "pcg_iteration": {"ms": pcg_ms, "bytes": kt[5],
-                                  "achieved": kt[5] / (pcg_ms * 1e-3) / 1e9,
-                                  "frac": kt[5] / (pcg_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
-                # the engine streams 16-bit compressed column offsets: the bytes
-                # of the formats actually read (achieved/frac above use SURVEY
-                # §8(d)'s 4-byte-index formula, i.e. effective bandwidth)
-                "format_bytes": {"a_pass": kt[6], "at_pass": kt[7], "pcg_iteration": kt[8],
-                                 "at_pass_achieved": kt[7] / (at_ms * 1e-3) / 1e9,
-                                 "at_pass_frac": kt[7] / (at_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
-                                 "pcg_iteration_frac": kt[8] / (pcg_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
+                                  "achieved": rate(kt[5], pcg_ms),
+                                  "frac": rate(kt[5], pcg_ms) / hbm,
+                                  "effective": gram},
+                "format_bytes": {"a_pass": kt[6], "at_pass": kt[7],
+                                 "pcg_iteration": kt[11] if gram else kt[8],
+                                 "at_pass_frac": rate(kt[7], at_ms) / hbm,
+                                 "k_gram": kt[10] if gram else None,
+                                 "k_gram_frac": rate(kt[10], kt[9]) / hbm if gram else None,
+                                 "pcg_iteration_frac":
+                                     rate(kt[11] if gram else kt[8], pcg_ms) / hbm},
                 "frac_of_nominal_8TBs": achieved / 8000.0}
     line = {"metric": METRIC, "value": ms * 1e-3, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -643,6 +645,7 @@ def main():
                       if loop_s > 0 else None},
             "workspace_reuse": resolve,
             "gpu_launches": int(sum(i.kernel_launches for i in infos)),
+            "engine_flags": int(last.engine_flags),
             "clocks": clk, "roofline": roofline,
             "e2e": {"value": ms_e2e * 1e-3, "unit": "s",
                     "h2d_bytes_per_step": int(einfos[-1].h2d_bytes),

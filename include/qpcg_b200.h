@@ -116,7 +116,7 @@ typedef struct {
   double rho_final;
   uint32_t certificate_valid;    /* 1 when a certificate was written */
   uint32_t n, m;
-  uint32_t reserved_;
+  uint32_t engine_flags;         /* QPCG_ENGINE_*: which engine paths ran */
   /* engine-side measurements (device-timed with CUDA events) */
   double setup_seconds;          /* device setup: symmetrize/transpose/Ruiz/operator */
   double solve_seconds;          /* ADMM loop + unscale + objective */
@@ -147,6 +147,11 @@ typedef struct {
 } qpcg_rho_update;
 
 /* ---- engine options (not part of the reference's Settings) ------------- */
+/* qpcg_info.engine_flags */
+#define QPCG_ENGINE_ONE_PASS_OPERATOR 1u /* PCG operator apply with A streamed
+                                            once (csrc/gram.cuh) */
+#define QPCG_ENGINE_PERSISTENT 2u        /* the whole loop as one kernel */
+
 #define QPCG_MEM_HOST 0   /* caller arrays are host memory (copied in setup) */
 #define QPCG_MEM_DEVICE 1 /* caller arrays are device memory on `device` */
 

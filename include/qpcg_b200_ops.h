@@ -59,7 +59,11 @@ int qpcg_debug_operator(qpcg_workspace* ws, const void* x, void* kx, void* diag_
  * (5 kernels), out[3..5] algorithmic bytes of each (4-byte
  * column indices), out[6..8] the same with the bytes of the matrix formats
  * actually streamed (16-bit compressed column offsets where used).
- * out must hold 9 doubles. */
+ * out[9] ms per one-pass kernel k_gram (the operator apply with A streamed
+ * once, csrc/gram.cuh; 0 when the workspace runs the two-pass path),
+ * out[10] its bytes, out[11] the bytes of a whole PCG iteration on that path.
+ * The A / A^T pass timings are taken either way; out[2] times the path the
+ * solve uses.  out must hold 12 doubles. */
 int qpcg_bench_kernels(qpcg_workspace* ws, uint32_t reps, double* out);
 
 #ifdef __cplusplus

@@ -54,7 +54,7 @@ class Info(C.Structure):
                 ("runtime_seconds", C.c_double), ("equil_passes", C.c_uint32),
                 ("rho_update_count", C.c_uint32), ("equil_residual", C.c_double),
                 ("rho_final", C.c_double), ("certificate_valid", C.c_uint32),
-                ("n", C.c_uint32), ("m", C.c_uint32), ("reserved_", C.c_uint32),
+                ("n", C.c_uint32), ("m", C.c_uint32), ("engine_flags", C.c_uint32),
                 ("setup_seconds", C.c_double), ("solve_seconds", C.c_double),
                 ("h2d_seconds", C.c_double), ("d2h_seconds", C.c_double),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),

@@ -38,6 +38,7 @@
 #include "../../include/qpcg_b200_ops.h"
 #include "admm.cuh"
 #include "comm.cuh"
+#include "gram.cuh"
 #include "persist.cuh"
 #include "setup.cuh"
 #include "upload.cuh"
@@ -165,6 +166,7 @@ class Workspace : public IEngine<T> {
   bool own_stream = true;
   uint64_t setup_launches = 0;
   bool have_counted_setup = false;
+  bool ran_persistent = false;
 
   ~Workspace() {
     if (up_thread.joinable()) up_thread.join();  // (a setup that failed before wait_values)
@@ -185,7 +187,7 @@ class Workspace : public IEngine<T> {
       AllocScope scope(s, &arena);
       if (s) cudaStreamSynchronize(s);  // every stream that used the buffers is idle now
       for (void* p : allocs) dfree(p);  // arena blocks: back to the arena; others: the pool
-      for (SpmvPlan<T>* p : {&D.pP, &D.pA, &D.pAT}) plan_free(*p);
+      for (SpmvPlan<T>* p : {&D.pP, &D.pA, &D.pAT, &gLo, &gHi}) plan_free(*p);
       if (tmp.ptr) dfree(tmp.ptr);
       tmp.ptr = nullptr;
       tmp.bytes = 0;
@@ -295,6 +297,8 @@ class Workspace : public IEngine<T> {
     mark("finish_scaling");
     finish_setup();
     mark("finish_setup");
+    build_gram();
+    mark("gram");
     CK(cudaEventRecord(ev1, s));
     CK(cudaEventSynchronize(ev1));
     float ms = 0;
@@ -765,6 +769,237 @@ class Workspace : public IEngine<T> {
       bad("settings: bad equilibration parameters");
   }
 
+  // ------------------------------------------------ one-pass operator apply
+  // (gram.cuh): K p with A streamed once; built at the end of setup when A
+  // has a dense column window, else the two-pass SpMV path runs.
+  GramDev<T> gram{};
+  bool gram_on = false;
+  size_t gram_smem = 0;
+  uint32_t gram_threads = 0;
+  DevCsr<T> atLo{}, atHi{};  // row-range views of A^T outside the window
+  SpmvPlan<T> gLo{}, gHi{};
+  uint32_t gram_hi0 = 0;
+  uint64_t gram_nnz_g = 0;  // padded in-window entries of the row-pass rows
+  uint32_t gram_nnz_out = 0, gram_ng = 0, gram_nthin = 0, gram_thin_nnz = 0;
+  static constexpr size_t kGramSmemBudget = 225u << 10;
+
+  void enq_gram_kernel_only() {
+    k_gram<T><<<gram.G, gram_threads, gram_smem, s>>>(D, gram);
+    CK_LAUNCH();
+  }
+  void enq_gram() {
+    enq_gram_kernel_only();
+    if (gram.n_trows) {
+      k_gram_thin<T><<<grid_for(gram.n_trows), kThreads, 0, s>>>(D, gram);
+      CK_LAUNCH();
+    }
+    k_gram_reduce<T><<<ceil_div(gram.W, 32u), 32 * kGramRedGroups, 0, s>>>(D, gram);
+    CK_LAUNCH();
+    if (gLo.grid())
+      launch_spmv<T, 1, SumOp>(atLo, gLo, GatherVec<T>{D.t}, EpiKpOff<T>{D, T(0), 0u}, s);
+    if (gHi.grid())
+      launch_spmv<T, 1, SumOp>(atHi, gHi, GatherVec<T>{D.t}, EpiKpOff<T>{D, T(0), gram_hi0}, s);
+  }
+
+  void build_gram() {
+    // opt-in (QPCG_GRAM=1): measured slower than the two-pass SpMV on B200 at
+    // every eligible BASELINE config (profiles/r02_gram_experiment.txt)
+    const char* env = std::getenv("QPCG_GRAM");
+    const bool force = env && env[0] == '1';
+    if (!force || D.split || D.A.nnz == 0 || D.n == 0 || D.m == 0) return;
+    const uint32_t n = D.n, m = D.m, nnz = D.A.nnz;
+    // the dense column window from the column counts (A^T's row_ptr): the
+    // smallest range holding every column with >= min(512, max count / 4)
+    // entries (a column with fewer is cheaper through the A^T stream than as
+    // G partial slots)
+    std::vector<uint32_t> rp(size_t(n) + 1);
+    CK(cudaMemcpyAsync(rp.data(), D.AT.rp, sizeof(uint32_t) * (size_t(n) + 1),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    uint32_t maxcnt = 0;
+    for (uint32_t c = 0; c < n; ++c) maxcnt = std::max(maxcnt, rp[c + 1] - rp[c]);
+    const uint32_t thr = std::min(512u, std::max(2u, maxcnt / 4));
+    uint32_t a = n, b = 0;
+    for (uint32_t c = 0; c < n; ++c)
+      if (rp[c + 1] - rp[c] >= thr) {
+        a = std::min(a, c);
+        b = c;
+      }
+    if (a == n) return;
+    const uint32_t W = b - a + 1;
+    // shared memory: p's window and the accumulator (W each) + the ring
+    const size_t acc_bytes = 2 * size_t((W + 15u) & ~15u) * sizeof(T);
+    if (W > 65536u || acc_bytes > kGramSmemBudget * 3 / 4) return;
+    if (!force && double(rp[b + 1] - rp[a]) < 0.75 * double(nnz)) return;
+    // per row: entries inside / outside the window
+    uint32_t *cin, *cout, *rp_out, *isg, *pos;
+    unsigned int* mx;
+    CK(dmalloc(&cin, sizeof(uint32_t) * (size_t(m) + 1)));
+    CK(dmalloc(&cout, sizeof(uint32_t) * (size_t(m) + 1)));
+    CK(dmalloc(&isg, sizeof(uint32_t) * (size_t(m) + 1)));
+    CK(dmalloc(&pos, sizeof(uint32_t) * (size_t(m) + 1)));
+    CK(dmalloc(&mx, sizeof(unsigned int)));
+    auto release = [&] {
+      for (void* q : {(void*)cin, (void*)cout, (void*)isg, (void*)pos, (void*)mx}) CK(dfree(q));
+    };
+    rp_out = alloc<uint32_t>(size_t(m) + 1);
+    CK(cudaMemsetAsync(cout + m, 0, sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(mx, 0, sizeof(unsigned int), s));
+    gram_count_kernel<<<grid_for(uint64_t(m) * 32), kThreads, 0, s>>>(D.A.rp, D.A.ci, m, a, W, cin,
+                                                                      cout, mx);
+    CK_LAUNCH();
+    exclusive_scan_u32(cout, rp_out, m + 1, tmp, s);
+    // the row-pass rows (>= kGramThin in-window entries) and the thin rows
+    gram_isg_kernel<<<grid_for(uint64_t(m) + 1), kThreads, 0, s>>>(cin, m, isg);
+    CK_LAUNCH();
+    exclusive_scan_u32(isg, pos, m + 1, tmp, s);
+    uint32_t h[3];
+    CK(cudaMemcpyAsync(h, pos + m, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h + 1, rp_out + m, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h + 2, mx, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint32_t ng = h[0];
+    gram_nnz_out = h[1];
+    const uint32_t slot_len = (h[2] + 7u) & ~7u;  // the longest row, padded
+    if (ng == 0 || h[2] > kGramMaxRowLen) {
+      release();
+      return;
+    }
+    // shared memory: the window accumulator + NS ring slots; NS - 2 consumers
+    const size_t slot_bytes = size_t(slot_len) * (sizeof(T) + sizeof(uint16_t));
+    const uint32_t NS = uint32_t(
+        std::min<size_t>(16, (kGramSmemBudget - acc_bytes - 256) / slot_bytes));
+    if (NS < 3) {
+      release();
+      return;
+    }
+    gram.NS = NS;
+    gram.slot_len = slot_len;
+    gram.C = std::min<uint32_t>(8, NS - 1);
+    gram_threads = 32 * (1 + gram.C);
+    gram_smem = acc_bytes + size_t(NS) * slot_bytes + 2 * NS * sizeof(uint64_t);
+    uint32_t* grows = alloc<uint32_t>(size_t(ng) + 1);
+    uint32_t* trows = alloc<uint32_t>(size_t(m - ng) + 1);
+    uint8_t* thin = alloc<uint8_t>(size_t(m) + 1);
+    gram_split_kernel<<<grid_for(m), kThreads, 0, s>>>(cin, pos, m, grows, trows, thin);
+    CK_LAUNCH();
+    // padded storage of the row-pass rows' in-window entries
+    uint32_t* glen = alloc<uint32_t>(size_t(ng) + 1);
+    uint32_t* gstart = alloc<uint32_t>(size_t(ng) + 1);
+    gram_plen_kernel<<<grid_for(uint64_t(ng) + 1), kThreads, 0, s>>>(grows, ng, cin, isg, glen);
+    CK_LAUNCH();
+    exclusive_scan_u32(isg, gstart, ng + 1, tmp, s);
+    uint32_t tot_g = 0;
+    CK(cudaMemcpyAsync(&tot_g, gstart + ng, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    gram_nnz_g = tot_g;
+    uint32_t* din = pos;  // (pos is no longer needed)
+    CK(cudaMemsetAsync(din, 0xff, sizeof(uint32_t) * m, s));
+    gram_din_kernel<<<grid_for(ng), kThreads, 0, s>>>(grows, ng, gstart, din);
+    CK_LAUNCH();
+    uint16_t* off_g = alloc<uint16_t>(size_t(tot_g) + 8);
+    T* val_g = alloc<T>(size_t(tot_g) + 8);
+    CK(cudaMemsetAsync(off_g, 0, sizeof(uint16_t) * (size_t(tot_g) + 8), s));
+    CK(cudaMemsetAsync(val_g, 0, sizeof(T) * (size_t(tot_g) + 8), s));
+    uint32_t* col_out = alloc<uint32_t>(size_t(gram_nnz_out) + 1);
+    T* val_out = alloc<T>(size_t(gram_nnz_out) + 1);
+    gram_fill_kernel<T><<<grid_for(uint64_t(m) * 32), kThreads, 0, s>>>(
+        D.A.rp, D.A.ci, D.A.val, m, a, W, din, rp_out, off_g, val_g, col_out, val_out);
+    CK_LAUNCH();
+    // cost-balanced CTA ranges over the row-pass rows
+    gram_weight_kernel<<<grid_for(uint64_t(ng) + 1), kThreads, 0, s>>>(grows, ng, cin, cout, isg);
+    CK_LAUNCH();
+    uint32_t* wpre = alloc<uint32_t>(size_t(ng) + 1);
+    exclusive_scan_u32(isg, wpre, ng + 1, tmp, s);
+    // A_thin^T over the window columns
+    uint32_t* tcnt = cin;  // (cin is no longer needed: W + 1 <= m + 1 is not guaranteed)
+    if (W + 1 > m + 1) CK(dmalloc(&tcnt, sizeof(uint32_t) * (size_t(W) + 1)));
+    CK(cudaMemsetAsync(tcnt + W, 0, 4, s));
+    gram_thin_t_kernel<T><<<grid_for(uint64_t(W) * 32), kThreads, 0, s>>>(
+        D.AT.rp, D.AT.ci, D.AT.val, a, W, thin, tcnt, nullptr, nullptr, nullptr, 0);
+    CK_LAUNCH();
+    uint32_t* rp_thin = alloc<uint32_t>(size_t(W) + 1);
+    exclusive_scan_u32(tcnt, rp_thin, W + 1, tmp, s);
+    uint32_t nthin = 0, wtot = 0;
+    CK(cudaMemcpyAsync(&nthin, rp_thin + W, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&wtot, wpre + ng, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (tcnt != cin) CK(dfree(tcnt));
+    gram_nthin = nthin;
+    gram_thin_nnz = nnz - (wtot - kGramRowCost * ng);  // entries of the thin rows
+    uint32_t* col_thin = alloc<uint32_t>(size_t(nthin) + 1);
+    T* val_thin = alloc<T>(size_t(nthin) + 1);
+    gram_thin_t_kernel<T><<<grid_for(uint64_t(W) * 32), kThreads, 0, s>>>(
+        D.AT.rp, D.AT.ci, D.AT.val, a, W, thin, nullptr, rp_thin, col_thin, val_thin, 1);
+    CK_LAUNCH();
+    release();
+    // grid: as many CTAs as fit
+    int sms = 0, nb = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaFuncSetAttribute(k_gram<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gram_smem)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_gram<T>, int(gram_threads), gram_smem));
+    if (nb <= 0) return;
+    gram.G = std::min<uint32_t>(uint32_t(sms) * uint32_t(nb), ng);
+    uint32_t* cut = alloc<uint32_t>(size_t(gram.G) + 1);
+    gram_cut_kernel<<<ceil_div(gram.G + 1, 256u), 256, 0, s>>>(wpre, ng, gram.G, cut);
+    CK_LAUNCH();
+    gram.w0 = a;
+    gram.W = W;
+    gram.cut = cut;
+    gram.rows = grows;
+    gram.gstart = gstart;
+    gram.glen = glen;
+    gram.off_g = off_g;
+    gram.val_g = val_g;
+    gram.trows = trows;
+    gram.n_trows = m - ng;
+    gram.rp_thin = rp_thin;
+    gram.col_thin = col_thin;
+    gram.val_thin = val_thin;
+    gram.rp_out = rp_out;
+    gram.col_out = col_out;
+    gram.val_out = val_out;
+    gram.part = alloc<T>(size_t(gram.G) * W);
+    gram_ng = ng;
+    if (const char* dg = std::getenv("QPCG_GRAM_DEBUG")) gram.dbg = uint32_t(std::atoi(dg));
+    // A^T rows outside the window: [0, a) and [b + 1, n)
+    if (a > 0) {
+      atLo = D.AT;
+      atLo.rows = a;
+      gLo = plan_build<T>(atLo.rp, a, rp[a], tmp, s);
+    }
+    if (b + 1 < n) {
+      atHi = D.AT;
+      atHi.rp = D.AT.rp + (b + 1);
+      atHi.rows = n - (b + 1);
+      gram_hi0 = b + 1;
+      gHi = plan_build<T>(atHi.rp, n - (b + 1), rp[n] - rp[b + 1], tmp, s);
+    }
+    gram_on = true;
+    if (const char* tr = std::getenv("QPCG_GRAM_TRACE"); tr && tr[0] == '1')
+      std::fprintf(stderr,
+                   "[gram] window [%u, %u) W=%u, row-pass rows %u (max %u entries, slot %u), thin "
+                   "rows %u (A_thin^T %u), out-of-window entries %u; ring %u slots, %u consumer "
+                   "warps, smem %zu B, G=%u (%d per SM)\n",
+                   a, b + 1, W, ng, h[2], slot_len, m - ng, nthin, gram_nnz_out, NS, gram.C,
+                   gram_smem, gram.G, nb);
+  }
+  // bytes one operator apply streams on the one-pass path (k_gram + reduce +
+  // the out-of-window A^T rows; P, p and the vectors as in §8(d))
+  double gram_stream_bytes() const {
+    const double S = sizeof(T), m = D.m;
+    // row pass (padded in-window entries, out-of-window entries, the row
+    // descriptors), t, the partial windows written and read, the thin rows'
+    // entries (k_gram_thin) and A_thin^T
+    double b = double(gram_nnz_g) * (S + 2) + double(gram_nnz_out) * (S + 4) +
+               8.0 * (double(gram_ng) + 1) + 8.0 * (m + 1) + S * m +
+               2.0 * S * double(gram.G) * gram.W + double(gram_thin_nnz) * (S + 4) +
+               double(gram_nthin) * (S + 4);
+    if (gLo.grid()) b += plan_stream_bytes(atLo, gLo);
+    if (gHi.grid()) b += plan_stream_bytes(atHi, gHi);
+    return b;
+  }
+
   // ------------------------------------------------------ enqueue helpers
   void enq_rhs(const Handles&) {
     k_pack_rhs<T><<<grid_for(D.m), kThreads, 0, s>>>(D);
@@ -776,8 +1011,12 @@ class Workspace : public IEngine<T> {
     CK_LAUNCH();
   }
   void enq_pcg_iter(const Handles& H) {
-    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
-    launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
+    if (gram_on) {
+      enq_gram();
+    } else {
+      launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
+      launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
+    }
     k_pcg_dot<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D);
     CK_LAUNCH();
     k_pcg_update<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D, H);
@@ -1105,6 +1344,8 @@ class Workspace : public IEngine<T> {
     info->certificate_valid = has_cert;
     info->n = n;
     info->m = m;
+    info->engine_flags = (gram_on ? QPCG_ENGINE_ONE_PASS_OPERATOR : 0u) |
+                         (ran_persistent ? QPCG_ENGINE_PERSISTENT : 0u);
     info->setup_seconds = setup_seconds;
     info->solve_seconds = solve_s;
     info->h2d_seconds = h2d_seconds;
@@ -1129,6 +1370,7 @@ class Workspace : public IEngine<T> {
     if (opt.mode == QPCG_MODE_EAGER || opt.on_iteration) {
       run_eager();
     } else if (use_persistent()) {
+      ran_persistent = true;
       run_persistent();
     } else {
       if (!exec) {
@@ -1297,8 +1539,9 @@ class Workspace : public IEngine<T> {
     fill(D.r, D.n, T(1));
     std::vector<cudaEvent_t> ev(2 * reps);
     for (auto& e : ev) CK(cudaEventCreate(&e));
-    double acc[3] = {0, 0, 0};
-    for (int which = 0; which < 3; ++which) {
+    double acc[4] = {0, 0, 0, 0};
+    for (int which = 0; which < 4; ++which) {
+      if (which == 3 && !gram_on) break;
       for (uint32_t i = 0; i < reps; ++i) {
         hc = run;
         push_ctl();
@@ -1307,8 +1550,10 @@ class Workspace : public IEngine<T> {
           launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
         else if (which == 1)
           launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
-        else
+        else if (which == 2)
           enq_pcg_iter(Handles{});
+        else
+          enq_gram_kernel_only();
         CK(cudaEventRecord(ev[2 * i + 1], s));
       }
       CK(cudaStreamSynchronize(s));
@@ -1339,6 +1584,15 @@ class Workspace : public IEngine<T> {
     out[6] = fa + S * n + S * m;
     out[7] = fat + mb(D.P) + S * m + 2 * S * n;
     out[8] = fa + fat + mb(D.P) + S * (2 * m + 11 * n);
+    // one-pass operator apply (gram.cuh): k_gram alone, its bytes (A's
+    // in-window + out-of-window entries, row pointers, t, the partial windows
+    // written), the whole PCG iteration's bytes on that path
+    out[9] = acc[3];
+    out[10] = gram_on ? double(gram_nnz_g) * (S + 2) + double(gram_nnz_out) * (S + 4) +
+                            8.0 * (double(gram_ng) + 1) + 8.0 * (m + 1) + S * m + S * n +
+                            S * double(gram.G) * gram.W
+                      : 0.0;
+    out[11] = gram_on ? gram_stream_bytes() + mb(D.P) + S * (11 * n) : 0.0;
   }
 
   // ------------------------------------- operator-level PCG (ops C-ABI)

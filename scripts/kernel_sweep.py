@@ -16,7 +16,7 @@ lib.qpcg_bench_kernels.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
 for cfg in cfgs:
     p = G.config(cfg)
     with solver.Workspace(p, Settings(lambda_pcg=1e-3), device=0) as ws:
-        out = np.zeros(9)
+        out = np.zeros(12)
         lib.qpcg_bench_kernels(ws.ws, reps, out.ctypes.data)
         lib.qpcg_bench_kernels(ws.ws, reps, out.ctypes.data)
     print(f"[{cfg}] A {out[0]*1e3:7.1f} us {out[3]/out[0]/1e6:6.0f} GB/s | A^T {out[1]*1e3:7.1f} us "

@@ -13,7 +13,7 @@ lib.qpcg_bench_kernels.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
 for cfg in sys.argv[1].split(","):
     p = G.config(cfg).astype(np.float32)
     with solver.Workspace(p, Settings(lambda_pcg=1e-3), device=0) as ws:
-        out = np.zeros(9)
+        out = np.zeros(12)
         lib.qpcg_bench_kernels(ws.ws, 20, out.ctypes.data)
         lib.qpcg_bench_kernels(ws.ws, 20, out.ctypes.data)
     print(f"[{cfg} f32] A {out[0]*1e3:7.1f} us | A^T {out[1]*1e3:7.1f} us | PCG iter {out[2]*1e3:7.1f} us "

@@ -34,7 +34,9 @@ unit_row = rows[1]
 per = {}
 for r in rows[2:]:
     kn = r[hdr.index("Kernel Name")]
-    name = next((e for e in ("EpiKp", "EpiAp", "EpiRhs", "EpiAdmm", "EpiDual") if e in kn), "other")
+    name = next((e for e in ("k_gram_reduce", "k_gram", "EpiKpOff", "EpiKp", "EpiAp", "EpiRhs",
+                             "EpiAdmm", "EpiDual", "k_pcg_dot", "k_pcg_update", "k_pcg_pupdate",
+                             "k_pcg_init", "k_pcg_fin") if e in kn), "other")
     rec = {}
     for k, short in keys.items():
         if k not in hdr:
@@ -53,6 +55,8 @@ for name, recs in per.items():
     avg["launches_captured"] = len(recs)
     avg["dram_bytes"] = avg["dram_read"] + avg["dram_write"]
     summary["kernels"][name] = avg
+if "k_gram" in summary["kernels"]:
+    summary["k_gram_dram_bytes"] = summary["kernels"]["k_gram"]["dram_bytes"]
 if "EpiKp" in summary["kernels"]:
     summary["at_pass_dram_bytes"] = summary["kernels"]["EpiKp"]["dram_bytes"]
 if "EpiAp" in summary["kernels"]:
