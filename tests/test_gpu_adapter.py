@@ -15,7 +15,8 @@ def test_adapter_runs_against_reference_types():
     out = subprocess.run([EXE, "3"], capture_output=True, text=True, timeout=600)
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.count(" OK") == 7
+    assert out.stdout.count(" OK") == 8  # 7 classes + the on_iteration check
+    assert "MISMATCH" not in out.stdout
     assert "invalid_argument" in out.stdout
 
 
