@@ -397,6 +397,34 @@ def ncu_traffic(config: str, dtype: str = "f64", kernel: str = "EpiKp"):
         return None
 
 
+def config_dict(args, problem, world: int, sharded: bool) -> dict:
+    """The workload description both arms print (identical dicts)."""
+    S = 8 if args.dtype == "f64" else 4
+    a_bytes = problem.a.nnz * (S + 4) * 2
+    return {"workload": WORKLOADS[args.config], "config_id": args.config,
+            "n": problem.n, "m": problem.m, "nnz_P_upper": problem.p_upper.nnz,
+            "nnz_A": problem.a.nnz, "settings": {"lambda_pcg": args.lambda_pcg},
+            "parallelism": (f"rowshard{world}-{args.transport}" if sharded else f"replicas{world}")
+                           if world > 1 else
+                           ("single" if args.shards <= 1 else f"virtual-rowshard{args.shards}"),
+            "l2": ("inputs larger than L2 (A and A^T streams ~%.1f GB per PCG iteration)"
+                   % (a_bytes / 1e9)) if a_bytes >= (256 << 20) else
+                  "matrices fit in L2: a 512 MB buffer is overwritten before every timed step",
+            "mode": args.mode}
+
+
+def reference_problem(config: str):
+    """The instance generated by the REFERENCE's own generators (oracle/_ref:
+    bench::detail recipes / bench::generate, generators.hpp) — bit-identical to
+    the engine arm's native generator (tests/test_generators.py)."""
+    from oracle import oracle as O  # reference arm only
+    from paper_1912_04263_b200.generators import CONFIGS
+    spec = CONFIGS[config]
+    if spec[0] == "class":
+        return O.ref_generate(spec[1], spec[2], 0)
+    return O.ref_generate_explicit(*spec, seed=0)
+
+
 # --------------------------------------------------------------- arms
 def run_reference(args, rank: int, world: int) -> None:
     """The reference's own CPU implementation of the path: ONE complete

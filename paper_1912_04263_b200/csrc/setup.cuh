@@ -17,6 +17,9 @@
 //     extract_diagonal (sparse.hpp:382-397) = first diagonal match per row.
 #pragma once
 
+#include <algorithm>
+#include <vector>
+
 #include "spmv.cuh"
 
 namespace qpcg_b200 {
@@ -215,6 +218,129 @@ inline void transpose_structure(const uint32_t* ci, const uint32_t* row_of, uint
 template <typename T>
 void gather_values(const T* src, const uint32_t* perm, uint32_t nnz, T* dst, cudaStream_t s) {
   for_n(nnz, [=] __device__(uint32_t i) { dst[i] = src[perm[i]]; }, s);
+}
+
+// The same gather, dst[i] = src[perm[i]] for the transpose (dst in A^T order,
+// src in A order), in L2-sized WINDOWS of source rows.  A^T row c lists its
+// source rows in increasing order, so the entries of c whose source row lies
+// in window [R_w, R_w+1) are one contiguous segment: window by window, a warp
+// per long A^T row copies its next segment (a cursor per row), the window's
+// source values stay L2-resident while every column gathers from them, and the
+// destination is written in contiguous runs.  The plain gather touches a new
+// 32-byte sector for nearly every 8-byte value (lasso: 17.5 GB of DRAM traffic
+// for 3 GB of data, profiles/r01_ncu_kernels_config2.md).  A^T rows shorter than
+// kWinLongRow are gathered directly (one thread each).
+constexpr uint32_t kWinLongRow = 64;
+template <typename T>
+__global__ void win_gather_kernel(const T* __restrict__ src, const uint32_t* __restrict__ perm,
+                                  const uint32_t* __restrict__ at_rp,
+                                  const uint32_t* __restrict__ at_ci, const uint32_t* rows,
+                                  uint32_t nrows, uint32_t* cur, uint32_t r_end, T* dst) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nrows; t += nw) {
+    const uint32_t c = rows[t];
+    uint32_t k = cur[t];
+    const uint32_t e = at_rp[c + 1];
+    for (;;) {
+      const uint32_t kk = k + lane;
+      const bool in = kk < e && at_ci[kk] < r_end;
+      const unsigned bal = __ballot_sync(0xffffffffu, in);
+      if (in) dst[kk] = src[perm[kk]];
+      const uint32_t cnt = __popc(bal);  // a prefix: the source rows increase
+      k += cnt;
+      if (cnt < 32u) break;
+    }
+    if (lane == 0) cur[t] = k;
+  }
+}
+template <typename T>
+__global__ void short_gather_kernel(const T* __restrict__ src, const uint32_t* __restrict__ perm,
+                                    const uint32_t* __restrict__ at_rp, const uint32_t* rows,
+                                    uint32_t nrows, T* dst) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nrows; t += gridDim.x * blockDim.x) {
+    const uint32_t c = rows[t];
+    for (uint32_t k = at_rp[c]; k < at_rp[c + 1]; ++k) dst[k] = src[perm[k]];
+  }
+}
+static __global__ void win_split_kernel(const uint32_t* at_rp, uint32_t n, const uint32_t* pos,
+                                        uint32_t* longr, uint32_t* shortr, uint32_t* cur) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    const bool lg = at_rp[c + 1] - at_rp[c] >= kWinLongRow;
+    if (lg) {
+      longr[pos[c]] = c;
+      cur[pos[c]] = at_rp[c];
+    } else {
+      shortr[c - pos[c]] = c;
+    }
+  }
+}
+static __global__ void win_flag_kernel(const uint32_t* at_rp, uint32_t n, uint32_t* f) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= n; c += gridDim.x * blockDim.x)
+    f[c] = c < n && at_rp[c + 1] - at_rp[c] >= kWinLongRow;
+}
+// first row r with a_rp[r] >= w * per (window boundaries by source position)
+static __global__ void win_bounds_kernel(const uint32_t* a_rp, uint32_t m, uint64_t per,
+                                         uint32_t nwin, uint32_t* bnd) {
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w > nwin) return;
+  if (w == nwin) {
+    bnd[w] = m;
+    return;
+  }
+  const uint64_t target = per * w;
+  uint32_t lo = 0, hi = m;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a_rp[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  bnd[w] = lo;
+}
+template <typename T>
+void gather_values_windowed(const T* src, const uint32_t* perm, const uint32_t* at_rp,
+                            const uint32_t* at_ci, uint32_t n, const uint32_t* a_rp, uint32_t m,
+                            uint32_t nnz, T* dst, CubTemp& tmp, cudaStream_t s) {
+  constexpr uint64_t kWindowBytes = 32ull << 20;
+  const uint64_t per = std::max<uint64_t>(1, kWindowBytes / sizeof(T));
+  const uint32_t nwin = uint32_t((uint64_t(nnz) + per - 1) / per);
+  if (nwin <= 1 || n == 0) {  // one window: the plain gather is already L2-resident
+    gather_values(src, perm, nnz, dst, s);
+    return;
+  }
+  uint32_t *f, *pos, *longr, *shortr, *cur, *bnd;
+  CK(dmalloc(&f, sizeof(uint32_t) * (size_t(n) + 1)));
+  CK(dmalloc(&pos, sizeof(uint32_t) * (size_t(n) + 1)));
+  CK(dmalloc(&longr, sizeof(uint32_t) * (size_t(n) + 1)));
+  CK(dmalloc(&shortr, sizeof(uint32_t) * (size_t(n) + 1)));
+  CK(dmalloc(&cur, sizeof(uint32_t) * (size_t(n) + 1)));
+  CK(dmalloc(&bnd, sizeof(uint32_t) * (size_t(nwin) + 1)));
+  win_flag_kernel<<<grid_for(uint64_t(n) + 1), kThreads, 0, s>>>(at_rp, n, f);
+  CK_LAUNCH();
+  exclusive_scan_u32(f, pos, n + 1, tmp, s);
+  win_split_kernel<<<grid_for(n), kThreads, 0, s>>>(at_rp, n, pos, longr, shortr, cur);
+  CK_LAUNCH();
+  win_bounds_kernel<<<ceil_div(nwin + 1, 256u), 256, 0, s>>>(a_rp, m, per, nwin, bnd);
+  CK_LAUNCH();
+  uint32_t nl = 0;
+  std::vector<uint32_t> hb(size_t(nwin) + 1);
+  CK(cudaMemcpyAsync(&nl, pos + n, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hb.data(), bnd, 4 * (size_t(nwin) + 1), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (n - nl) {
+    short_gather_kernel<T><<<grid_for(n - nl), kThreads, 0, s>>>(src, perm, at_rp, shortr, n - nl,
+                                                                 dst);
+    CK_LAUNCH();
+  }
+  if (nl) {
+    for (uint32_t w = 0; w < nwin; ++w) {
+      win_gather_kernel<T><<<grid_for(uint64_t(nl) * 32), kThreads, 0, s>>>(
+          src, perm, at_rp, at_ci, longr, nl, cur, hb[w + 1], dst);
+      CK_LAUNCH();
+    }
+  }
+  for (void* p : {(void*)f, (void*)pos, (void*)longr, (void*)shortr, (void*)cur, (void*)bnd})
+    CK(dfree(p));
 }
 
 // ---------------------------------------------------- symmetrize_upper

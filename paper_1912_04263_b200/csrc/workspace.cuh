@@ -552,7 +552,7 @@ class Workspace : public IEngine<T> {
     // ---- from here on A's values are needed
     check_values_late();
     T* ato_v = alloc<T>(annz);
-    gather_values(a_v, permA, annz, ato_v, s);
+    gather_values_windowed(a_v, permA, at_rp, at_ci, n, a_rp, m, annz, ato_v, tmp, s);
     D.Ao = DevCsr<T>{m, n, annz, a_v, a_rp, a_ci};
     D.ATo = DevCsr<T>{n, m, annz, ato_v, at_rp, at_ci};
     D.pPo = D.pP;
@@ -669,7 +669,9 @@ class Workspace : public IEngine<T> {
     const uint32_t n = D.n, m = D.m;
     equil_passes = passes;
     equil_residual = deviation;
-    if (set.scaling_enabled) gather_values(D.A.val, permA, D.A.nnz, D.AT.val, s);
+    if (set.scaling_enabled)
+      gather_values_windowed(D.A.val, permA, D.AT.rp, D.AT.ci, n, D.A.rp, m, D.A.nnz, D.AT.val,
+                             tmp, s);
     {
       T *d = D.d, *e = D.e, *di = D.d_inv, *ei = D.e_inv, *lo = D.l_o, *uo = D.u_o, *ls = D.l,
         *us = D.u;
