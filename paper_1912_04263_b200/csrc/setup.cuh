@@ -425,6 +425,66 @@ void row_inf_norms(const DevCsr<T>& M, const SpmvPlan<T>& P, T* out, cudaStream_
   launch_spmv<T, 1, MaxAbsOp>(M, P, GatherNone<T, 1>{}, StoreEpi<T>{out}, s);
 }
 
+// One Ruiz scaling visit, v = (v * dr[row]) * dc[col] (scale_rows then
+// scale_columns, scaling.hpp:362-380, :333-341), fused with the row
+// inf-norms of the scaled values (row_inf_norms, :324-330) that the NEXT
+// pass needs: a max is order-free, so the norms are bit-identical to a
+// separate pass, which saves one read of the matrix per pass.  Loads are
+// issued U strides at a time (the generic plan_visit keeps one in flight).
+template <typename T, int U>
+__global__ void __launch_bounds__(kThreads) scale_norm_kernel(DevCsr<T> M, SpmvPlan<T> P,
+                                                              const T* __restrict__ dr,
+                                                              const T* __restrict__ dc, T* norm) {
+  if (blockIdx.x < P.nb_items) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t it = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (it >= P.n_items) return;
+    const WorkItem item = P.items[it];
+    const T r = dr[item.row];
+    T acc[1] = {T(0)};
+    for (uint32_t k0 = item.beg; k0 < item.end; k0 += 32u * U) {
+      T v[U];
+      uint32_t c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t k = k0 + 32u * u + lane;
+        const bool ok = k < item.end;
+        v[u] = ok ? M.val[k] : T(0);
+        c[u] = ok ? M.ci[k] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t k = k0 + 32u * u + lane;
+        if (k < item.end) {
+          const T x = (v[u] * r) * dc[c[u]];
+          M.val[k] = x;
+          MaxAbsOp::acc(acc[0], x, T(0));
+        }
+      }
+    }
+    item_finish<T, 1, MaxAbsOp, StoreEpi<T>>(M, P, StoreEpi<T>{norm}, item, lane, acc);
+  } else {
+    const uint32_t idx = (blockIdx.x - P.nb_items) * kThreads + threadIdx.x;
+    if (idx >= P.n_short) return;
+    const uint32_t row = P.short_rows[idx];
+    const T r = dr[row];
+    T a = T(0);
+    for (uint32_t k = M.rp[row]; k < M.rp[row + 1]; ++k) {
+      const T x = (M.val[k] * r) * dc[M.ci[k]];
+      M.val[k] = x;
+      MaxAbsOp::acc(a, x, T(0));
+    }
+    norm[row] = a;
+  }
+}
+template <typename T>
+void scale_and_norms(const DevCsr<T>& M, const SpmvPlan<T>& P, const T* dr, const T* dc, T* norm,
+                     cudaStream_t s) {
+  if (P.grid() == 0) return;
+  scale_norm_kernel<T, 4><<<P.grid(), kThreads, 0, s>>>(M, P, dr, dc, norm);
+  CK_LAUNCH();
+}
+
 // diag_ata: warp per A^T row, sequential sum of squares in stored order.
 // init (nullable): running sums carried in from the row blocks above (the
 // sharded chain); out may alias init.

@@ -59,6 +59,11 @@ struct SpmvPlan {
   uint32_t* wide = nullptr;
   uint32_t n_chunks = 0, n_wide = 0;
   uint32_t chunk_log2 = 12;  // work items hold <= 2^chunk_log2 nnz (plan_chunk_log2)
+  // uncompressed plans whose items average 97..255 entries (svm's A: 151)
+  // run the U = 8 build: one predicated round of 8 strides covers an item,
+  // where U = 4 needs a full round plus a dependent tail round (same
+  // arithmetic, same results)
+  uint32_t u8 = 0;
   uint32_t grid() const { return nb_items + nb_short; }
 };
 
@@ -348,6 +353,9 @@ void launch_spmv_select(const DevCsr<T>& M, const SpmvPlan<T>& P, const G1& g1, 
   if (P.off16 != nullptr)
     spmv_select_kernel<T, N1, G1, E1, N2, G2, E2, 8, true><<<P.grid(), kThreads, 0, s>>>(M, P, g1, e1,
                                                                                          g2, e2);
+  else if (P.u8)
+    spmv_select_kernel<T, N1, G1, E1, N2, G2, E2, 8, false><<<P.grid(), kThreads, 0, s>>>(M, P, g1,
+                                                                                          e1, g2, e2);
   else
     spmv_select_kernel<T, N1, G1, E1, N2, G2, E2, 4, false><<<P.grid(), kThreads, 0, s>>>(M, P, g1, e1,
                                                                                           g2, e2);
@@ -360,6 +368,8 @@ void launch_spmv(const DevCsr<T>& M, const SpmvPlan<T>& P, const Gather& g, cons
   if (P.grid() == 0) return;
   if (P.off16 != nullptr)
     spmv_kernel<T, NCOL, Op, Gather, Epi, 8, true><<<P.grid(), kThreads, 0, s>>>(M, P, g, e);
+  else if (P.u8)
+    spmv_kernel<T, NCOL, Op, Gather, Epi, 8, false><<<P.grid(), kThreads, 0, s>>>(M, P, g, e);
   else
     spmv_kernel<T, NCOL, Op, Gather, Epi, 4, false><<<P.grid(), kThreads, 0, s>>>(M, P, g, e);
   CK_LAUNCH();
@@ -653,6 +663,12 @@ SpmvPlan<T> plan_build(const uint32_t* d_rp, uint32_t rows, uint64_t nnz, CubTem
   }
   P.nb_items = ceil_div(P.n_items, kWarpsPerBlock);
   P.nb_short = ceil_div(P.n_short, kThreads);
+  {  // mean W-bin item length from the totals (row_ptr[rows] - short entries is not
+     // known here; the item count and nnz bound it well enough for the choice)
+    const char* e = std::getenv("QPCG_U8");
+    const uint64_t mean = P.n_items ? nnz / P.n_items : 0;
+    P.u8 = e ? (e[0] == '1') : (mean > 96 && mean < kLongItemMean);
+  }
   CK(cudaStreamSynchronize(s));
   for (void* p : {(void*)is_short, (void*)nch, (void*)is_multi, (void*)multi_nch, (void*)short_pos,
                   (void*)item_off, (void*)lr_idx, (void*)pbase, (void*)items_tmp, (void*)keys,

@@ -595,6 +595,7 @@ class Workspace : public IEngine<T> {
   // maxima are order-free, so the sharded scaling is bit-identical too.
   void ruiz_prepare() {
     const uint32_t n = D.n, m = D.m;
+    rz_norms_fresh = false;
     rz_dx = vec(n, false);
     rz_dz = vec(m, false);
     rz_pn = vec(n, false);
@@ -611,13 +612,16 @@ class Workspace : public IEngine<T> {
     compact_kernel<<<grid_for(n), kThreads, 0, s>>>(flags, pos, n, p_rows);
     CK_LAUNCH();
   }
+  // the A / A^T row norms of the current values: computed here in the first
+  // pass, afterwards by the previous pass's fused scaling visit
+  bool rz_norms_fresh = false;
   void ruiz_norms() {
     row_inf_norms(D.P, D.pP, rz_pn, s);
     if (D.m == 0 || D.AT.nnz == 0)  // empty block: no column contributes
       CK(cudaMemsetAsync(rz_atn, 0, sizeof(T) * D.n, s));
-    else
+    else if (!rz_norms_fresh)
       row_inf_norms(D.AT, D.pAT, rz_atn, s);
-    row_inf_norms(D.A, D.pA, rz_an, s);
+    if (!rz_norms_fresh) row_inf_norms(D.A, D.pA, rz_an, s);
   }
   void ruiz_delta() {
     const uint32_t n = D.n, m = D.m;
@@ -658,8 +662,10 @@ class Workspace : public IEngine<T> {
     CK_LAUNCH();
     CK(cudaEventRecord(ev_join, s_side));
     // main stream meanwhile: A rows (dz) then cols (dx); A^T rows (dx) then cols (dz)
-    plan_visit(D.A, D.pA, ScaleRowColFn<T>{D.A.val, D.A.ci, rz_dz, rz_dx}, s);
-    plan_visit(D.AT, D.pAT, ScaleRowColFn<T>{D.AT.val, D.AT.ci, rz_dx, rz_dz}, s);
+    // (+ the row norms of the scaled values for the next pass)
+    scale_and_norms(D.A, D.pA, rz_dz, rz_dx, rz_an, s);
+    scale_and_norms(D.AT, D.pAT, rz_dx, rz_dz, rz_atn, s);
+    rz_norms_fresh = true;
     CK(cudaStreamWaitEvent(s, ev_join, 0));
   }
 
