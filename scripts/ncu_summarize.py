@@ -12,16 +12,17 @@ import subprocess
 import sys
 
 rep, cfg, note = sys.argv[1], sys.argv[2], " ".join(sys.argv[3:])
+tables = []  # (header, unit row, data rows) per export: the metric sets may differ
 if rep.endswith(".csv"):
-    rows = []
-    for i, f in enumerate(rep.split(",")):
+    for f in rep.split(","):
         part = list(csv.reader(open(f)))
-        rows += part if i == 0 else part[2:]  # one header + unit row (same metric set)
+        if len(part) >= 3:
+            tables.append((part[0], part[1], part[2:]))
 else:
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
-hdr = rows[0]
+    part = list(csv.reader(io.StringIO(raw)))
+    tables.append((part[0], part[1], part[2:]))
 keys = {"gpu__time_duration.sum": "ncu_us", "dram__bytes_read.sum": "dram_read",
         "dram__bytes_write.sum": "dram_write",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct_of_ncu_peak",
@@ -30,25 +31,25 @@ keys = {"gpu__time_duration.sum": "ncu_us", "dram__bytes_read.sum": "dram_read",
         "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
         "launch__registers_per_thread": "registers",
         "lts__t_sectors_srcunit_tex_op_read.sum": "l2_tex_read_sectors"}
-unit_row = rows[1]
 per = {}
-for r in rows[2:]:
-    kn = r[hdr.index("Kernel Name")]
-    name = next((e for e in ("k_gram_reduce", "k_gram", "EpiKpOff", "EpiKp", "EpiAp", "EpiRhs",
-                             "EpiAdmm", "EpiDual", "k_pcg_dot", "k_pcg_update", "k_pcg_pupdate",
-                             "k_pcg_init", "k_pcg_fin") if e in kn), "other")
-    rec = {}
-    for k, short in keys.items():
-        if k not in hdr:
-            continue
-        v = float(r[hdr.index(k)].replace(",", ""))
-        u = unit_row[hdr.index(k)]
-        if short in ("dram_read", "dram_write"):
-            v *= {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(u, 1.0)
-        if short == "ncu_us":
-            v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
-        rec[short] = v
-    per.setdefault(name, []).append(rec)
+for hdr, unit_row, data in tables:
+    for r in data:
+        kn = r[hdr.index("Kernel Name")]
+        name = next((e for e in ("k_gram_reduce", "k_gram", "EpiKpOff", "EpiKp", "EpiAp", "EpiRhs",
+                                 "EpiAdmm", "EpiDual", "k_pcg_dot", "k_pcg_update",
+                                 "k_pcg_pupdate", "k_pcg_init", "k_pcg_fin") if e in kn), "other")
+        rec = {}
+        for k, short in keys.items():
+            if k not in hdr:
+                continue
+            v = float(r[hdr.index(k)].replace(",", ""))
+            u = unit_row[hdr.index(k)]
+            if short in ("dram_read", "dram_write"):
+                v *= {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(u, 1.0)
+            if short == "ncu_us":
+                v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
+            rec[short] = v
+        per.setdefault(name, []).append(rec)
 summary = {"source": note, "kernels": {}}
 for name, recs in per.items():
     avg = {k: sum(r[k] for r in recs) / len(recs) for k in recs[0]}
