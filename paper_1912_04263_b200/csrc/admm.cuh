@@ -299,6 +299,11 @@ struct EpiRhs {
     sigma = D.ctl->sigma;
     return D.ctl->error == 0;
   }
+  __device__ __forceinline__ void prefetch(uint32_t r) const {
+    prefetch_l1(D.x + r);
+    prefetch_l1(D.q + r);
+    prefetch_l1(D.xt + r);
+  }
   __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[2]) const {
     rhs_row(D, sigma, r, s[0], s[1]);
   }
@@ -363,6 +368,12 @@ struct EpiAdmm {
     rho = D.ctl->rho;
     two = ((D.ctl->iter + 1) % D.ctl->check_interval) == 0;
     return D.ctl->error == 0 && two == (NCOL == 2);
+  }
+  __device__ __forceinline__ void prefetch(uint32_t r) const {
+    prefetch_l1(D.z + r);
+    prefetch_l1(D.y + r);
+    prefetch_l1(D.l + r);
+    prefetch_l1(D.u + r);
   }
   __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[NCOL]) const {
     const T zt = s[0];

@@ -28,6 +28,7 @@
 
 #include <cstdlib>
 #include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 
@@ -254,14 +255,33 @@ __device__ __forceinline__ void item_finish(const DevCsr<T>& M, const SpmvPlan<T
   epi(item.row, tot);
 }
 
+// Epilogues that read per-row operands (the m-side ADMM update, the rhs and
+// K p rows) expose prefetch(row): lane 0 of a single-item row issues it at
+// the start of the item, so those loads travel while the row streams instead
+// of after the warp reduction (svm: 1e6 rows of 151 entries, 4 operand loads
+// each).
+template <class E, class = void>
+struct HasPrefetch : std::false_type {};
+template <class E>
+struct HasPrefetch<E, std::void_t<decltype(std::declval<const E&>().prefetch(0u))>>
+    : std::true_type {};
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // One work item (one warp; lane 0 runs the epilogue).  Multi-item rows
 // publish a partial; the last item to arrive combines them in item order
 // (deterministic).
 template <typename T, int NCOL, class Op, class Gather, class Epi, int U, bool CMP,
-          bool L1 = false>
+          bool L1 = false, bool PF = false>
 __device__ __forceinline__ void spmv_item_run(const DevCsr<T>& M, const SpmvPlan<T>& P,
                                               const Gather& gather, const Epi& epi,
                                               const WorkItem& item, uint32_t c0, uint32_t lane) {
+  // (PF: stand-alone kernels only; the persistent loop rewrites these vectors
+  // between grid barriers and keeps to plain loads)
+  if constexpr (PF && HasPrefetch<Epi>::value) {
+    if (lane == 0 && item.lr == 0xffffffffu) epi.prefetch(item.row);
+  }
   T acc[NCOL];
 #pragma unroll
   for (int j = 0; j < NCOL; ++j) acc[j] = T(0);
@@ -269,12 +289,12 @@ __device__ __forceinline__ void spmv_item_run(const DevCsr<T>& M, const SpmvPlan
   item_finish<T, NCOL, Op, Epi>(M, P, epi, item, lane, acc);
 }
 template <typename T, int NCOL, class Op, class Gather, class Epi, int U, bool CMP,
-          bool L1 = false>
+          bool L1 = false, bool PF = false>
 __device__ __forceinline__ void spmv_item(const DevCsr<T>& M, const SpmvPlan<T>& P,
                                           const Gather& gather, const Epi& epi, uint32_t it,
                                           uint32_t lane) {
-  spmv_item_run<T, NCOL, Op, Gather, Epi, U, CMP, L1>(M, P, gather, epi, P.items[it],
-                                                      CMP ? P.c0[it] : 0u, lane);
+  spmv_item_run<T, NCOL, Op, Gather, Epi, U, CMP, L1, PF>(M, P, gather, epi, P.items[it],
+                                                          CMP ? P.c0[it] : 0u, lane);
 }
 
 // One short row (<= kShortRowMax nnz), one thread, left to right: bit-exact.
@@ -313,7 +333,8 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(DevCsr<T> M, SpmvPlan<T>
   gather.init();
   if (blockIdx.x < P.nb_items) {
     const uint32_t it = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-    if (it < P.n_items) spmv_item<T, NCOL, Op, Gather, Epi, U, CMP>(M, P, gather, epi, it, threadIdx.x & 31);
+    if (it < P.n_items)
+      spmv_item<T, NCOL, Op, Gather, Epi, U, CMP, false, true>(M, P, gather, epi, it, threadIdx.x & 31);
   } else {
     const uint32_t idx = (blockIdx.x - P.nb_items) * kThreads + threadIdx.x;
     if (idx < P.n_short) spmv_short<T, NCOL, Op, Gather, Epi>(M, P, gather, epi, idx);
@@ -336,7 +357,8 @@ __global__ void __launch_bounds__(kThreads) spmv_select_kernel(DevCsr<T> M, Spmv
     if (blockIdx.x < P.nb_items) {
       const uint32_t it = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
       if (it < P.n_items)
-        spmv_item<T, NCOL, SumOp, Gather, Epi, U, CMP>(M, P, gather, epi, it, threadIdx.x & 31);
+        spmv_item<T, NCOL, SumOp, Gather, Epi, U, CMP, false, true>(M, P, gather, epi, it,
+                                                                    threadIdx.x & 31);
     } else {
       const uint32_t idx = (blockIdx.x - P.nb_items) * kThreads + threadIdx.x;
       if (idx < P.n_short) spmv_short<T, NCOL, SumOp, Gather, Epi>(M, P, gather, epi, idx);
