@@ -64,6 +64,15 @@ WORKLOADS = {
 }
 
 
+def _json_default(o):
+    """numpy scalars / arrays in the bench line -> plain JSON values."""
+    if isinstance(o, np.generic):
+        return o.item()
+    if isinstance(o, np.ndarray):
+        return o.tolist()
+    raise TypeError(f"not JSON serializable: {type(o).__name__}")
+
+
 def log(*a):
     print("[bench]", *a, file=sys.stderr, flush=True)
 
@@ -467,7 +476,7 @@ def run_reference(args, rank: int, world: int) -> None:
                       "r_dual_inf": float(r.r_dual_inf), "equil_passes": int(r.equil_passes)},
             "generation_s": gen_s, "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, default=_json_default), flush=True)
 
 
 def run_sweep(args) -> None:
@@ -613,7 +622,7 @@ def main():
     pk = peaks()
     S = 8 if dtype == np.float64 else 4
     at_ms, pcg_ms = kt[1], kt[2]
-    gram = kt[9] > 0  # the one-pass operator apply (csrc/gram.cuh) runs the PCG iterations
+    gram = bool(kt[9] > 0)  # the one-pass operator apply (csrc/gram.cuh) runs the PCG iterations
     hbm = pk["hbm_gbs"]
     rate = lambda b, t_ms: b / (t_ms * 1e-3) / 1e9  # noqa: E731
     if gram:
@@ -691,7 +700,7 @@ def main():
                                                 lam=args.lambda_pcg)
         except Exception as e:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "error": repr(e)}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, default=_json_default), flush=True)
     if dist is not None:
         dist.destroy_process_group()
 
