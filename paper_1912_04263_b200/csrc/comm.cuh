@@ -17,6 +17,7 @@
 
 #include <dlfcn.h>
 #include <sys/stat.h>
+#include <cstdlib>
 #include <nccl.h>  // types and enums only: every symbol is resolved through dlopen
 
 #include <chrono>
@@ -57,9 +58,17 @@ inline NcclApi& nccl_api() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
-    // the soname torch (or the system) already mapped wins; fall back to the
-    // unversioned development link
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // 1. a copy already mapped into the process (torch's) wins;
+    // 2. QPCG_NCCL_LIB (the Python layer points it at the pip NCCL that torch
+    //    itself loads, so a later `import torch` finds the same library
+    //    instead of clashing with an older system soname);
+    // 3. the system soname, then the unversioned development link
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) {
+      const char* lib = std::getenv("QPCG_NCCL_LIB");
+      if (lib && lib[0]) h = dlopen(lib, RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) return;
     auto sym = [&](auto& fn, const char* name) { fn = reinterpret_cast<std::decay_t<decltype(fn)>>(dlsym(h, name)); };

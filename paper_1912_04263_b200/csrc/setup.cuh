@@ -433,6 +433,7 @@ void row_inf_norms(const DevCsr<T>& M, const SpmvPlan<T>& P, T* out, cudaStream_
 // issued U strides at a time (the generic plan_visit keeps one in flight).
 template <typename T, int U>
 __global__ void __launch_bounds__(kThreads) scale_norm_kernel(DevCsr<T> M, SpmvPlan<T> P,
+                                                              const T* src,
                                                               const T* __restrict__ dr,
                                                               const T* __restrict__ dc, T* norm) {
   if (blockIdx.x < P.nb_items) {
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(kThreads) scale_norm_kernel(DevCsr<T> M, SpmvP
       for (int u = 0; u < U; ++u) {
         const uint32_t k = k0 + 32u * u + lane;
         const bool ok = k < item.end;
-        v[u] = ok ? M.val[k] : T(0);
+        v[u] = ok ? src[k] : T(0);
         c[u] = ok ? M.ci[k] : 0u;
       }
 #pragma unroll
@@ -470,18 +471,20 @@ __global__ void __launch_bounds__(kThreads) scale_norm_kernel(DevCsr<T> M, SpmvP
     const T r = dr[row];
     T a = T(0);
     for (uint32_t k = M.rp[row]; k < M.rp[row + 1]; ++k) {
-      const T x = (M.val[k] * r) * dc[M.ci[k]];
+      const T x = (src[k] * r) * dc[M.ci[k]];
       M.val[k] = x;
       MaxAbsOp::acc(a, x, T(0));
     }
     norm[row] = a;
   }
 }
+// src: the values to scale (M.val in place, or the originals on the first
+// pass, which then also initialises M.val)
 template <typename T>
-void scale_and_norms(const DevCsr<T>& M, const SpmvPlan<T>& P, const T* dr, const T* dc, T* norm,
-                     cudaStream_t s) {
+void scale_and_norms(const DevCsr<T>& M, const SpmvPlan<T>& P, const T* src, const T* dr,
+                     const T* dc, T* norm, cudaStream_t s) {
   if (P.grid() == 0) return;
-  scale_norm_kernel<T, 4><<<P.grid(), kThreads, 0, s>>>(M, P, dr, dc, norm);
+  scale_norm_kernel<T, 4><<<P.grid(), kThreads, 0, s>>>(M, P, src, dr, dc, norm);
   CK_LAUNCH();
 }
 

@@ -572,8 +572,12 @@ class Workspace : public IEngine<T> {
     D.A = DevCsr<T>{m, n, annz, alloc<T>(annz), a_rp, a_ci};
     D.AT = DevCsr<T>{n, m, annz, alloc<T>(annz), at_rp, at_ci};
     CK(cudaMemcpyAsync(D.P.val, Pfull.val, sizeof(T) * Pfull.nnz, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(D.A.val, a_v, sizeof(T) * annz, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(D.AT.val, ato_v, sizeof(T) * annz, cudaMemcpyDeviceToDevice, s));
+    // with scaling, the first Ruiz pass writes the scaled A and A^T straight
+    // from the originals (ruiz_scale), so they are not copied here
+    if (!set.scaling_enabled) {
+      CK(cudaMemcpyAsync(D.A.val, a_v, sizeof(T) * annz, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(D.AT.val, ato_v, sizeof(T) * annz, cudaMemcpyDeviceToDevice, s));
+    }
     D.q = vec(n, false);
     CK(cudaMemcpyAsync(D.q, D.q_o, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
     D.d = vec(n, false);
@@ -619,9 +623,9 @@ class Workspace : public IEngine<T> {
     row_inf_norms(D.P, D.pP, rz_pn, s);
     if (D.m == 0 || D.AT.nnz == 0)  // empty block: no column contributes
       CK(cudaMemsetAsync(rz_atn, 0, sizeof(T) * D.n, s));
-    else if (!rz_norms_fresh)
-      row_inf_norms(D.AT, D.pAT, rz_atn, s);
-    if (!rz_norms_fresh) row_inf_norms(D.A, D.pA, rz_an, s);
+    else if (!rz_norms_fresh)  // (first pass: the scaled copies are not written yet)
+      row_inf_norms(D.ATo, D.pAT, rz_atn, s);
+    if (!rz_norms_fresh) row_inf_norms(D.Ao, D.pA, rz_an, s);
   }
   void ruiz_delta() {
     const uint32_t n = D.n, m = D.m;
@@ -663,8 +667,9 @@ class Workspace : public IEngine<T> {
     CK(cudaEventRecord(ev_join, s_side));
     // main stream meanwhile: A rows (dz) then cols (dx); A^T rows (dx) then cols (dz)
     // (+ the row norms of the scaled values for the next pass)
-    scale_and_norms(D.A, D.pA, rz_dz, rz_dx, rz_an, s);
-    scale_and_norms(D.AT, D.pAT, rz_dx, rz_dz, rz_atn, s);
+    // first pass: read the originals, write the scaled copies
+    scale_and_norms(D.A, D.pA, rz_norms_fresh ? D.A.val : D.Ao.val, rz_dz, rz_dx, rz_an, s);
+    scale_and_norms(D.AT, D.pAT, rz_norms_fresh ? D.AT.val : D.ATo.val, rz_dx, rz_dz, rz_atn, s);
     rz_norms_fresh = true;
     CK(cudaStreamWaitEvent(s, ev_join, 0));
   }

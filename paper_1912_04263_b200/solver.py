@@ -26,6 +26,25 @@ LIB_PATH = os.environ.get("QPCG_LIB") or os.path.join(os.path.dirname(os.path.ab
 _lib = None
 
 
+def _point_at_pip_nccl() -> None:
+    """QPCG_NCCL_LIB -> the pip NCCL (nvidia-nccl) that torch loads, when it is
+    installed and the variable is unset: the engine dlopens NCCL lazily, and
+    a system libnccl.so.2 of another version mapped first would clash with a
+    later `import torch` (csrc/comm.cuh nccl_api)."""
+    if os.environ.get("QPCG_NCCL_LIB"):
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia")
+        for base in (spec.submodule_search_locations or []) if spec else []:
+            cand = os.path.join(base, "nccl", "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["QPCG_NCCL_LIB"] = cand
+                return
+    except Exception:
+        pass
+
+
 def load_library() -> C.CDLL:
     """Load the engine's C-ABI library (never falls back to anything else)."""
     global _lib
@@ -34,6 +53,7 @@ def load_library() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"qpcg-b200: CUDA engine not built ({LIB_PATH} missing); "
                           "run __graft_entry__.build() / python -m paper_1912_04263_b200.build")
+    _point_at_pip_nccl()
     lib = C.CDLL(LIB_PATH)
     vp = C.c_void_p
     for pre in ("f64", "f32"):

@@ -156,6 +156,8 @@ def test_release_cached_memory_returns_device_memory():
     free1, _ = torch.cuda.mem_get_info(0)
     solver.release_cached_memory()
     free2, _ = torch.cuda.mem_get_info(0)
+    print(f"free: after a release {free0 >> 20} MiB, after two solves {free1 >> 20} MiB, "
+          f"after a release {free2 >> 20} MiB")
     assert free2 >= free1
     assert free2 >= free0 - (64 << 20)  # nothing of the finished solves is kept
 
@@ -176,3 +178,19 @@ def test_on_iteration_observer():
     assert last.x.shape == (p.n,) and last.z.shape == (p.m,) and last.l.shape == (p.m,)
     assert np.all(last.l <= last.z) and np.all(last.z <= last.u)  # z = proj_[l,u](w), scaled
     assert len(d.pcg_calls) == g.iterations
+
+
+def test_nccl_before_torch_import():
+    """The engine loads NCCL lazily; when that happens before `import torch` it
+    must map the same NCCL torch will (the pip copy, QPCG_NCCL_LIB), or the
+    later import clashes with an older system libnccl.so.2."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_1912_04263_b200 import solver\n"
+            "solver.nccl_unique_id()\n"
+            "import torch\n"
+            "print('ok', torch.cuda.mem_get_info(0)[0] > 0)\n") % (
+        __import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok True" in r.stdout, r.stderr[-2000:]

@@ -204,3 +204,23 @@ def test_full_size_defaults_against_reference(cfg):
     assert [c["iterations"] for c in d.pcg_calls[:k]] == [c["iterations"] for c in rc[:k]]
     for a, b in zip(d.pcg_calls[:3], rc[:3]):
         assert a["eps"] == pytest.approx(b["eps"], rel=1e-6)
+
+
+def test_portfolio_scale8_eps1e5():
+    """SURVEY.md §8(c) step 4 at a larger portfolio: at eps = 1e-5 the
+    chaotic class is held to the 1e-3 objective and x criteria against the oracle
+    (tests/golden/portfolio8_eps1e-5.json, tests/golden/make_portfolio8.py), widened
+    only to 2x the oracle's own reorder noise at that tolerance."""
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                       "portfolio8_eps1e-5.json")))
+    p = G.generate("portfolio", 8, 0)
+    s = Settings(lambda_pcg=0.01, eps_abs=1e-5, eps_rel=1e-5, max_admm_iter=20000)
+    g = solver.solve(p, s, device=0)
+    assert g.status == gold["status"] == "solved"
+    ro = rel(g.objective, gold["objective"])
+    rx = xrel(g.x, np.array(gold["x"]))
+    print(f"portfolio 8 @1e-5: iterations {g.iterations} vs {gold['iterations']}, objective {ro:.2e}, "
+          f"x {rx:.2e} (oracle twin noise {gold['noise_rel_obj']:.2e}, {gold['noise_x']:.2e})")
+    assert ro <= max(1e-3, 2 * gold["noise_rel_obj"])
+    assert rx <= max(1e-3, 2 * gold["noise_x"])
+    assert kkt_ok(p, g, s)
