@@ -270,6 +270,7 @@ class Workspace : public IEngine<T> {
       std::fprintf(stderr, "[setup] %-16s %8.3f ms  launches %llu\n", what, (now_s() - w0) * 1e3,
                    (unsigned long long)(g_launches - l0));
     };
+    trace_t0 = trace ? w0 : 0.0;
     load(Pu, q, A, l, u, 0, A.rows, false);
     mark("load");
     ValKeys k = validate_keys();
@@ -519,6 +520,13 @@ class Workspace : public IEngine<T> {
   }
 
   // symmetrize_upper, transpose_csr, plans, the original and scaled copies
+  // QPCG_SETUP_TRACE=1: finer marks inside build_structures (stream synced)
+  double trace_t0 = 0.0;
+  void tmark(const char* what) {
+    if (trace_t0 == 0.0) return;
+    CK(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "[setup]   %-20s %8.3f ms\n", what, (now_s() - trace_t0) * 1e3);
+  }
   void build_structures() {
     // this workspace's stream and arena for the transient buffers too (the
     // helpers free them stream-ordered, without a synchronisation)
@@ -538,21 +546,27 @@ class Workspace : public IEngine<T> {
     plan_free(pPu);
     D.pP = plan_build<T>(Pfull.rp, n, Pfull.nnz, tmp, s);
     D.Po = Pfull;
+    tmark("plans A, P + symm.");
     // transpose_csr (solver.hpp:398)
     plan_visit(D.A, D.pA, RowOfFn{row_of}, s);
     uint32_t* at_rp = alloc<uint32_t>(n + 1);
     uint32_t* at_ci = alloc<uint32_t>(annz);
     permA = alloc<uint32_t>(annz);
     transpose_structure(a_ci, row_of, n, annz, at_rp, at_ci, permA, tmp, s);
+    tmark("transpose struct");
     D.pAT = plan_build<T>(at_rp, n, annz, tmp, s);
+    tmark("plan A^T");
     if (compress_indices()) {  // 16-bit column offsets for the A / A^T streams
       plan_compress(D.pA, a_ci, annz, n, tmp, s);
       plan_compress(D.pAT, at_ci, annz, m, tmp, s);
     }
+    tmark("compress");
     // ---- from here on A's values are needed
     check_values_late();
+    tmark("values");
     T* ato_v = alloc<T>(annz);
     gather_values_windowed(a_v, permA, at_rp, at_ci, n, a_rp, m, annz, ato_v, tmp, s);
+    tmark("A_orig^T gather");
     D.Ao = DevCsr<T>{m, n, annz, a_v, a_rp, a_ci};
     D.ATo = DevCsr<T>{n, m, annz, ato_v, at_rp, at_ci};
     D.pPo = D.pP;
