@@ -183,7 +183,20 @@ static __global__ void k_p2p_barrier(PeerPtrs area, int R, int rank) {
   *ep = e;
   const volatile unsigned long long* mine =
       reinterpret_cast<const volatile unsigned long long*>(area.p[rank]);
-  while (*mine < e * (unsigned long long)R) __nanosleep(200);
+  // a rank that never arrives (crashed, or a peer mapping that does not
+  // reach this GPU) must not hang the device: after 300 s the kernel traps,
+  // which fails this process's context instead of spinning forever
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*mine < e * (unsigned long long)R) {
+    __nanosleep(200);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 300ull * 1000000000ull) {
+      printf("qpcg peer barrier: rank %d waited 300 s for %d ranks (epoch %llu): trap\n", rank,
+             R, e);
+      __trap();
+    }
+  }
   __threadfence_system();
 }
 
