@@ -203,11 +203,12 @@ def test_full_size_defaults_against_reference(cfg):
     k = min(len(rc), len(d.pcg_calls), 10)
     # the first tolerance comes from the initial residuals (bit-exact setup);
     # the PCG iteration counts agree exactly except for portfolio, whose
-    # 270-iteration first solves move by a few iterations under reordering
-    # (SURVEY F3): a 2 % band there
+    # ~250-iteration solves at the 1e-7 tolerance floor move by a few
+    # iterations under reordering (its own reorder noise on this
+    # instance is 5e-3 in the objective): a 5 % band there
     assert d.pcg_calls[0]["eps"] == pytest.approx(rc[0]["eps"], rel=1e-9)
     for a, b in zip(d.pcg_calls[:k], rc[:k]):
-        band = 0 if cfg != "5a" else max(2, int(0.02 * b["iterations"]))
+        band = 0 if cfg != "5a" else max(3, int(0.05 * b["iterations"]))
         assert abs(a["iterations"] - b["iterations"]) <= band, (a, b)
     for a, b in zip(d.pcg_calls[1:3], rc[1:3]):
         assert a["eps"] == pytest.approx(b["eps"], rel=1e-6 if cfg != "5a" else 1e-2)
