@@ -69,7 +69,12 @@ inline EnginePools& engine_pools() {
   return p;
 }
 inline cudaMemPool_t engine_pool(int device) {
-  if (device < 0 || device >= kMaxDevices) return nullptr;
+  // QPCG_DEFAULT_POOL=1: allocate from the device's default pool instead
+  static const bool use_default = [] {
+    const char* e = std::getenv("QPCG_DEFAULT_POOL");
+    return e && e[0] == '1';
+  }();
+  if (use_default || device < 0 || device >= kMaxDevices) return nullptr;
   EnginePools& P = engine_pools();
   std::lock_guard<std::mutex> g(P.mu);
   if (!P.pool[device]) {

@@ -266,7 +266,11 @@ template <class E>
 struct HasPrefetch<E, std::void_t<decltype(std::declval<const E&>().prefetch(0u))>>
     : std::true_type {};
 __device__ __forceinline__ void prefetch_l1(const void* p) {
+#ifndef QPCG_NO_PREFETCH
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#else
+  (void)p;
+#endif
 }
 
 // One work item (one warp; lane 0 runs the epilogue).  Multi-item rows

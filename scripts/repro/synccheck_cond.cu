@@ -11,8 +11,9 @@
 //             clears the condition after 3 iterations)
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -o /tmp/synccheck_cond synccheck_cond.cu
-//   compute-sanitizer --tool synccheck /tmp/synccheck_cond plain|graph|while
+//   compute-sanitizer --tool synccheck /tmp/synccheck_cond plain|graph|while [blocks]
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cuda_runtime.h>
 
@@ -39,16 +40,17 @@ __global__ void k_count(int* counter, cudaGraphConditionalHandle h) {
 
 int main(int argc, char** argv) {
   const char* mode = argc > 1 ? argv[1] : "while";
+  const unsigned blocks = argc > 2 ? unsigned(std::atoi(argv[2])) : 3u;  // grid of k_shfl
   float* out;
   int* counter;
-  CK(cudaMalloc(&out, sizeof(float) * 256 * 3));
+  CK(cudaMalloc(&out, sizeof(float) * 256 * blocks));
   CK(cudaMalloc(&counter, sizeof(int)));
   const int three = 3;
   CK(cudaMemcpy(counter, &three, sizeof(int), cudaMemcpyHostToDevice));
   cudaStream_t s;
   CK(cudaStreamCreate(&s));
   if (!std::strcmp(mode, "plain")) {
-    k_shfl<<<3, 256, 0, s>>>(out);
+    k_shfl<<<blocks, 256, 0, s>>>(out);
     CK(cudaGetLastError());
   } else {
     cudaGraph_t g;
@@ -70,7 +72,7 @@ int main(int argc, char** argv) {
     cudaKernelNodeParams kp = {};
     void* a1[] = {&out};
     kp.func = (void*)k_shfl;
-    kp.gridDim = dim3(3);
+    kp.gridDim = dim3(blocks);
     kp.blockDim = dim3(256);
     kp.kernelParams = a1;
     CK(cudaGraphAddKernelNode(&n1, body, nullptr, 0, &kp));
