@@ -7,6 +7,8 @@
 // mode the same kernels also drive CUDA-graph conditional nodes.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "spmv.cuh"
 #include "comm.cuh"
 
@@ -721,15 +723,64 @@ __device__ __forceinline__ void pcg_pupdate_elems(const Dev<T>& D, uint32_t t0, 
   if (C->error || C->k == 0) return;  // nothing to do before the first update
   const T beta = C->beta;
   const bool imp = C->improved;
-  for (uint32_t i = t0; i < D.n; i += stride) {
-    const T yi = D.dinv[i] * D.r[i];
-    D.p[i] = -yi + beta * D.p[i];
-    if (imp) D.best[i] = D.xt[i];
+  if (imp) {
+    strided(t0, stride, D.n,
+            [&](uint32_t i) { return V4<T>{D.dinv[i], D.r[i], D.p[i], D.xt[i]}; },
+            [&](uint32_t i, const V4<T>& e) {
+              const T yi = e.a * e.b;
+              D.p[i] = -yi + beta * e.c;
+              D.best[i] = e.d;
+            });
+  } else {
+    strided(t0, stride, D.n, [&](uint32_t i) { return V3<T>{D.dinv[i], D.r[i], D.p[i]}; },
+            [&](uint32_t i, const V3<T>& e) {
+              const T yi = e.a * e.b;
+              D.p[i] = -yi + beta * e.c;
+            });
   }
 }
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_pcg_pupdate(Dev<T> D) {
   pcg_pupdate_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
+// The three vector kernels of a PCG iteration (k_pcg_dot, k_pcg_update,
+// k_pcg_pupdate) as ONE cooperative kernel on the same fixed reduction grid,
+// separated by grid barriers: the same per-thread elements, block trees and
+// block-ordered partial sums, so every bit is unchanged (the persistent driver
+// and the separate kernels agree with it), minus two launches and two
+// last-block round trips per iteration.  Launched cooperatively (all blocks
+// co-resident: red_grid() <= 2 per SM), also inside the CUDA graph.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_pcg_step(Dev<T> D, Handles H) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  Ctl<T>* C = D.ctl;
+  const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  if (!C->pcg_active || C->error) {  // (uniform: written by earlier kernels)
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.pcg, 0);
+    return;
+  }
+  {  // p . Kp, alpha (k_pcg_dot)
+    T v[1] = {T(0)};
+    pcg_dot_elems(D, t0, stride, v);
+    T tot[1];
+    if (grid_reduce<T, 1>(v, 0x0u, D.red, &C->red_counter, tot) && threadIdx.x == 0)
+      pcg_dot_decide(C, tot);
+  }
+  grid.sync();
+  if (C->error) {  // NotPositiveDefinite (k_pcg_update's exit)
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(H.pcg, 0);
+    return;
+  }
+  {  // x, r, r.y, |r| (k_pcg_update)
+    T v[2] = {T(0), T(0)};
+    pcg_update_elems(D, t0, stride, v);
+    T tot[2];
+    if (grid_reduce<T, 2>(v, 0x2u, D.red, &C->red_counter, tot) && threadIdx.x == 0)
+      pcg_update_decide(C, tot, H);
+  }
+  grid.sync();
+  pcg_pupdate_elems(D, t0, stride);  // p, best (k_pcg_pupdate)
 }
 
 // PCG exit: x~ = 0 (b == 0) or best iterate (cap); PcgCall record.

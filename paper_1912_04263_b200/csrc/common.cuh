@@ -191,6 +191,43 @@ inline bool cache_owned(void* p, size_t* bytes) {
   return true;
 }
 
+// Can a cooperative launch be captured into a CUDA graph and replayed on this
+// driver / device?  Probed once per process on a private stream.
+static __global__ void coop_probe_kernel(int* out) {
+  if (threadIdx.x == 0) atomicAdd(out, 1);
+}
+inline bool coop_capture_probe() {
+  static std::once_flag once;
+  static bool ok = false;
+  std::call_once(once, [] {
+    cudaStream_t st = nullptr;
+    int* d = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    int h = 0;
+    bool good = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaMalloc(&d, sizeof(int)) == cudaSuccess &&
+                cudaMemset(d, 0, sizeof(int)) == cudaSuccess &&
+                cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (good) {
+      void* args[] = {&d};
+      const bool launched = cudaLaunchCooperativeKernel((const void*)coop_probe_kernel, dim3(2),
+                                                        dim3(32), args, 0, st) == cudaSuccess;
+      good = (cudaStreamEndCapture(st, &g) == cudaSuccess) && launched && g != nullptr;
+    }
+    good = good && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess &&
+           cudaGraphLaunch(ge, st) == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess &&
+           cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess && h == 2;
+    cudaGetLastError();  // a failed probe leaves no sticky error behind
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    if (d) cudaFree(d);
+    if (st) cudaStreamDestroy(st);
+    ok = good;
+  });
+  return ok;
+}
+
 // qpcg_release_cached_memory(): the idle cached blocks are freed, then every
 // engine pool is trimmed to what live workspaces still hold.
 inline void release_cached_memory() {

@@ -1044,6 +1044,15 @@ class Workspace : public IEngine<T> {
       launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
       launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
     }
+    if (coop_pcg_ok()) {
+      Dev<T> d = D;
+      Handles h = H;
+      void* args[] = {&d, &h};
+      CK(cudaLaunchCooperativeKernel((const void*)k_pcg_step<T>, dim3(red_grid<T>(D.n)),
+                                     dim3(kThreads), args, 0, s));
+      CK_LAUNCH();
+      return;
+    }
     k_pcg_dot<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D);
     CK_LAUNCH();
     k_pcg_update<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D, H);
@@ -1051,6 +1060,28 @@ class Workspace : public IEngine<T> {
     k_pcg_pupdate<T><<<grid_for(D.n), kThreads, 0, s>>>(D);
     CK_LAUNCH();
   }
+  // k_pcg_step (opt-in, QPCG_COOP_PCG=1): needs cooperative launches to
+  // capture into CUDA graphs on this driver (probed once per process) and a
+  // co-resident grid.  Measured at config 2: 378.3 / 378.6 ms per solve with
+  // the three kernels vs 379.6 / 380.2 ms fused (inside the graph the two
+  // launches it saves cost ~1 us each; svm's PCG iteration 750 vs 749 us), so
+  // the separate kernels stay the default; the results are identical.
+  bool coop_pcg_ok() {
+    static const bool env_on = [] {
+      const char* e = std::getenv("QPCG_COOP_PCG");
+      return e && e[0] == '1';
+    }();
+    if (!env_on) return false;
+    if (coop_state == 0) {
+      int nb = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pcg_step<T>, kThreads, 0);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      const bool fits = uint64_t(nb) * uint64_t(sms) >= red_grid<T>(D.n);
+      coop_state = (fits && coop_capture_probe()) ? 1 : 2;
+    }
+    return coop_state == 1;
+  }
+  int coop_state = 0;  // 0 unknown, 1 on, 2 off
   void enq_post_pcg(const Handles& H) {
     k_pcg_fin<T><<<grid_for(D.n), kThreads, 0, s>>>(D);
     CK_LAUNCH();
