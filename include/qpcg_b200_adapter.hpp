@@ -107,14 +107,36 @@ struct Api<float> {
   }
 };
 
-// qpcg_iteration_cb -> std::function<void(const IterationView<T>&)>
+// appends this solve's PCG records not yet in diag (base: the size diag had
+// when the solve started; the reference only ever appends to it)
+template <typename T>
+void append_pcg_calls(qpcg_workspace* w, qpcg::SolveDiagnostics<T>* diag, size_t base) {
+  const uint32_t k = qpcg_get_pcg_calls(w, nullptr, 0);
+  const size_t have = diag->pcg_calls.size() - base;
+  if (k <= have) return;
+  std::vector<qpcg_pcg_call> calls(k);
+  qpcg_get_pcg_calls(w, calls.data(), k);
+  for (size_t i = have; i < calls.size(); ++i) {
+    const auto& c = calls[i];
+    diag->pcg_calls.push_back({c.admm_iter, T(c.eps), T(c.r_prim_scaled_inf),
+                               T(c.r_dual_scaled_inf), c.iterations, c.converged != 0});
+  }
+}
+
+// qpcg_iteration_cb -> std::function<void(const IterationView<T>&)>; like the
+// reference (solver.hpp:446-454) the iteration's PcgCall is appended to
+// diag->pcg_calls before the callback runs
 template <typename T>
 struct IterTrampoline {
   const std::function<void(const qpcg::IterationView<T>&)>* fn;
   std::vector<T> x, z, y, l, u;
+  qpcg_workspace* w = nullptr;
+  qpcg::SolveDiagnostics<T>* diag = nullptr;
+  size_t base = 0;
   static void call(void* user, uint32_t iter, const void* xp, const void* zp, const void* yp,
                    const void* lp, const void* up, uint32_t n, uint32_t m) {
     auto* t = static_cast<IterTrampoline*>(user);
+    if (t->w && t->diag) append_pcg_calls(t->w, t->diag, t->base);
     auto fill = [](std::vector<T>& v, const void* p, uint32_t k) {
       const T* a = static_cast<const T*>(p);
       v.assign(a, a + k);
@@ -150,7 +172,8 @@ qpcg::SolveOutcome<T> solve(const qpcg::QpProblem<T>& p, const qpcg::Settings<T>
   qpcg_options opt;
   qpcg_default_options(&opt);
   opt.record_diagnostics = diag != nullptr ? 1 : 0;
-  IterTrampoline<T> tramp{diag != nullptr ? &diag->on_iteration : nullptr, {}, {}, {}, {}, {}};
+  IterTrampoline<T> tramp{diag != nullptr ? &diag->on_iteration : nullptr, {}, {}, {}, {}, {},
+                          nullptr, diag, diag != nullptr ? diag->pcg_calls.size() : 0};
   if (diag != nullptr && diag->on_iteration) {
     opt.on_iteration = &IterTrampoline<T>::call;
     opt.on_iteration_user = &tramp;
@@ -162,6 +185,7 @@ qpcg::SolveOutcome<T> solve(const qpcg::QpProblem<T>& p, const qpcg::Settings<T>
   WsGuard g;
   int rc = Api<T>::setup(&g.w, &pv, p.q.data(), &av, p.l.data(), p.u.data(), &cs, &opt);
   if (rc != QPCG_OK) rethrow(rc, qpcg_last_error(nullptr));
+  tramp.w = g.w;
   const size_t n = p.p_upper.rows, m = p.a.rows;
   if (initial != nullptr) {
     if (initial->x.size() != n || initial->z.size() != m || initial->y.size() != m)
@@ -193,11 +217,7 @@ qpcg::SolveOutcome<T> solve(const qpcg::QpProblem<T>& p, const qpcg::Settings<T>
   out.rho_final = T(info.rho_final);
   out.rho_update_count = info.rho_update_count;
   if (diag != nullptr) {
-    std::vector<qpcg_pcg_call> calls(qpcg_get_pcg_calls(g.w, nullptr, 0));
-    qpcg_get_pcg_calls(g.w, calls.data(), uint32_t(calls.size()));
-    for (const auto& c : calls)
-      diag->pcg_calls.push_back({c.admm_iter, T(c.eps), T(c.r_prim_scaled_inf),
-                                 T(c.r_dual_scaled_inf), c.iterations, c.converged != 0});
+    append_pcg_calls(g.w, diag, tramp.base);  // (on_iteration may have appended some)
     std::vector<uint32_t> checks(qpcg_get_check_iterations(g.w, nullptr, 0));
     qpcg_get_check_iterations(g.w, checks.data(), uint32_t(checks.size()));
     for (auto it : checks) diag->check_iterations.push_back(it);

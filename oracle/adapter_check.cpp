@@ -61,8 +61,14 @@ int main(int argc, char** argv) {
     const auto p = qpcg::bench::generate<double>(spec);
     qpcg::Settings<double> s;
     s.lambda_pcg = 0.01;
-    auto observe = [](std::vector<unsigned>& its, std::vector<double>& xn) {
-      return [&its, &xn](const qpcg::IterationView<double>& v) {
+    // the callback also sees this iteration's PcgCall already appended
+    // (solver.hpp:446-454 appends it before calling on_iteration)
+    bool calls_in_step = true;
+    qpcg::SolveDiagnostics<double>* watched = nullptr;
+    auto observe = [&calls_in_step, &watched](std::vector<unsigned>& its, std::vector<double>& xn) {
+      return [&its, &xn, &calls_in_step, &watched](const qpcg::IterationView<double>& v) {
+        if (watched && (watched->pcg_calls.empty() || watched->pcg_calls.back().admm_iter != v.iter))
+          calls_in_step = false;
         its.push_back(v.iter);
         double m = 0;
         for (double e : v.x) m = std::max(m, std::abs(e));
@@ -74,14 +80,18 @@ int main(int argc, char** argv) {
     qpcg::SolveDiagnostics<double> dr, dg;
     dr.on_iteration = observe(ri, rx);
     dg.on_iteration = observe(gi, gx);
+    watched = &dr;
     const auto r = qpcg::solve(p, s, nullptr, &dr);
+    const bool ref_in_step = calls_in_step;
+    watched = &dg;
     const auto g = qpcg::b200::solve(p, s, nullptr, &dg);
+    const bool b200_in_step = calls_in_step && ref_in_step;
     bool ok = gi.size() == g.iterations && ri.size() == r.iterations && !gi.empty();
     for (size_t i = 0; ok && i < gi.size(); ++i) ok = gi[i] == i + 1;
     double d = 0;
     for (size_t i = 0; ok && i < std::min<size_t>(3, gx.size()); ++i)
       d = std::max(d, std::abs(gx[i] - rx[i]) / std::max(1.0, rx[i]));
-    ok = ok && d < 1e-6;
+    ok = ok && d < 1e-6 && b200_in_step && dg.pcg_calls.size() == g.iterations;
     bad += !ok;
     std::printf("on_iteration: reference %zu calls, b200 %zu calls, first |x|inf rel diff %.1e %s\n",
                 ri.size(), gi.size(), d, ok ? "OK" : "MISMATCH");

@@ -282,8 +282,15 @@ def solve(p: QpProblem, settings: Settings | None = None, initial: WarmStart | N
     shards > 1 / nccl / peer: the row-sharded engine (SURVEY.md §8(e));
     sm_budget: cap on the SMs of the persistent driver (see solve_batch)."""
     if diag is not None:
+        fn, holder = diag.on_iteration, {}
+
+        def observed(view):  # solver.hpp:446-454: the PcgCall is recorded first
+            if "ws" in holder:
+                fetch_diagnostics(holder["ws"].lib, holder["ws"].ws, diag)
+            fn(view)
         with Workspace(p, settings, device, mode, record_diagnostics=True, shards=shards,
-                       nccl=nccl, peer=peer, on_iteration=diag.on_iteration) as ws:
+                       nccl=nccl, peer=peer, on_iteration=observed if fn else None) as ws:
+            holder["ws"] = ws
             if initial is not None:
                 ws.warm_start(initial.x, initial.z, initial.y)
             return ws.solve(diag)

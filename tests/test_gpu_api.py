@@ -168,8 +168,10 @@ def test_on_iteration_observer():
     loop gives bitwise the same solve as the graph driver."""
     from paper_1912_04263_b200.problem import SolveDiagnostics
     p = G.generate("huber", 4, 1)
-    views = []
-    d = SolveDiagnostics(on_iteration=views.append)
+    views, seen = [], []
+    d = SolveDiagnostics()
+    d.on_iteration = lambda v: (views.append(v), seen.append(
+        bool(d.pcg_calls) and d.pcg_calls[-1]["admm_iter"] == v.iter))
     g = solver.solve(p, S, diag=d, device=0)
     ref = solver.solve(p, S, device=0)
     assert [v.iter for v in views] == list(range(1, g.iterations + 1))
@@ -178,6 +180,7 @@ def test_on_iteration_observer():
     assert last.x.shape == (p.n,) and last.z.shape == (p.m,) and last.l.shape == (p.m,)
     assert np.all(last.l <= last.z) and np.all(last.z <= last.u)  # z = proj_[l,u](w), scaled
     assert len(d.pcg_calls) == g.iterations
+    assert all(seen)  # each iteration's PcgCall is recorded before the callback
 
 
 def test_nccl_before_torch_import():
