@@ -378,7 +378,12 @@ struct EpiAdmm {
     prefetch_l1(D.u + r);
   }
   __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[NCOL]) const {
-    const T zt = s[0];
+    mside(D, alpha, one_m_alpha, rho, r, s[0]);
+    if constexpr (NCOL == 2) D.ax[r] = s[1];
+  }
+  // the m-side update of row r (solver.hpp:369-376) from its z~
+  static __device__ __forceinline__ void mside(const Dev<T>& D, T alpha, T one_m_alpha, T rho,
+                                               uint32_t r, T zt) {
     const T zp = D.z[r], yp = D.y[r];
     const T w = alpha * zt + one_m_alpha * zp + yp / rho;
     const T zn = smin(smax(w, D.l[r]), D.u[r]);
@@ -387,9 +392,35 @@ struct EpiAdmm {
     D.z[r] = zn;
     D.y[r] = yn;
     D.dy[r] = yn - yp;
+  }
+};
+
+// Plans of short rows (svm's A: 1e6 rows of ~151 entries) run the m-side
+// update as a separate row-parallel pass instead of in the SpMV epilogue: the
+// epilogue of a warp-per-row item executes on one lane, so 1e6 of them (with
+// their IEEE division and 8 scattered accesses) cost ~200 us of issue slots,
+// while a thread per row does the same arithmetic coalesced.  The z~ pass
+// then only stores z~ (and A x on check iterations); same values, same bits.
+template <typename T, int NCOL = 2>
+struct EpiAdmmStore {
+  Dev<T> D;
+  __device__ __forceinline__ bool init() {
+    const bool two = ((D.ctl->iter + 1) % D.ctl->check_interval) == 0;
+    return D.ctl->error == 0 && two == (NCOL == 2);
+  }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[NCOL]) const {
+    D.zt[r] = s[0];
     if constexpr (NCOL == 2) D.ax[r] = s[1];
   }
 };
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_admm_mside(Dev<T> D) {
+  const Ctl<T>* C = D.ctl;
+  if (C->error) return;
+  const T alpha = C->alpha, oma = T(1) - alpha, rho = C->rho;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < D.m; j += gridDim.x * blockDim.x)
+    EpiAdmm<T, 1>::mside(D, alpha, oma, rho, j, D.zt[j]);
+}
 
 // plain store (A x for the initial / final residuals)
 template <typename T>

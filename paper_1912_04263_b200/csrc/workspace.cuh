@@ -1087,9 +1087,17 @@ class Workspace : public IEngine<T> {
     CK_LAUNCH();
     // z~ = A x~ with the m-side update: the 2-column build on check
     // iterations (col 1 = A x_new), else the 1-column one; one launch
-    launch_spmv_select<T, 1, GatherVec<T>, EpiAdmm<T, 1>, 2, GatherAdmm<T>, EpiAdmm<T, 2>>(
-        D.A, D.pA, GatherVec<T>{D.xt}, EpiAdmm<T, 1>{D, T(0), T(0), T(0), false},
-        GatherAdmm<T>{D.g2n}, EpiAdmm<T, 2>{D, T(0), T(0), T(0), false}, s);
+    if (D.pA.u8) {  // short rows: the m-side update as a row-parallel pass (EpiAdmmStore)
+      launch_spmv_select<T, 1, GatherVec<T>, EpiAdmmStore<T, 1>, 2, GatherAdmm<T>,
+                         EpiAdmmStore<T, 2>>(D.A, D.pA, GatherVec<T>{D.xt}, EpiAdmmStore<T, 1>{D},
+                                             GatherAdmm<T>{D.g2n}, EpiAdmmStore<T, 2>{D}, s);
+      k_admm_mside<T><<<grid_for(D.m), kThreads, 0, s>>>(D);
+      CK_LAUNCH();
+    } else {
+      launch_spmv_select<T, 1, GatherVec<T>, EpiAdmm<T, 1>, 2, GatherAdmm<T>, EpiAdmm<T, 2>>(
+          D.A, D.pA, GatherVec<T>{D.xt}, EpiAdmm<T, 1>{D, T(0), T(0), T(0), false},
+          GatherAdmm<T>{D.g2n}, EpiAdmm<T, 2>{D, T(0), T(0), T(0), false}, s);
+    }
     k_xupdate<T><<<grid_for(D.n), kThreads, 0, s>>>(D, H);
     CK_LAUNCH();
   }
