@@ -187,33 +187,10 @@ inline int bits_for(uint32_t n) {
 
 // Structure of the transpose of (rows x cols, row_of[], ci[]):
 // out_rp [cols+1], out_ci [nnz] (= source rows), perm [nnz].
+struct WinPlan;
 inline void transpose_structure(const uint32_t* ci, const uint32_t* row_of, uint32_t cols,
                                 uint32_t nnz, uint32_t* out_rp, uint32_t* out_ci, uint32_t* perm,
-                                CubTemp& tmp, cudaStream_t s) {
-  CK(cudaMemsetAsync(out_rp, 0, sizeof(uint32_t) * (cols + 1), s));
-  if (nnz == 0) return;
-  uint32_t *cnt, *keys_out, *idx;
-  CK(dmalloc(&cnt, sizeof(uint32_t) * (cols + 1)));
-  CK(dmalloc(&keys_out, sizeof(uint32_t) * nnz));
-  CK(dmalloc(&idx, sizeof(uint32_t) * nnz));
-  CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (cols + 1), s));
-  count_cols_kernel<<<grid_for(nnz), kThreads, 0, s>>>(ci, nnz, cnt);
-  CK_LAUNCH();
-  exclusive_scan_u32(cnt, out_rp, cols + 1, tmp, s);  // cnt[cols] == 0 -> out_rp[cols] = nnz
-  iota_kernel<<<grid_for(nnz), kThreads, 0, s>>>(idx, nnz);
-  CK_LAUNCH();
-  size_t b = 0;
-  const int nb = bits_for(cols);
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, b, ci, keys_out, idx, perm, nnz, 0, nb, s));
-  tmp.ensure(b);
-  CK(cub::DeviceRadixSort::SortPairs(tmp.ptr, b, ci, keys_out, idx, perm, nnz, 0, nb, s));
-  const uint32_t* perm_c = perm;
-  for_n(nnz, [=] __device__(uint32_t i) { out_ci[i] = row_of[perm_c[i]]; }, s);
-  // (frees are ordered on s: dmalloc / dfree follow the caller's AllocScope(s))
-  CK(dfree(cnt));
-  CK(dfree(keys_out));
-  CK(dfree(idx));
-}
+                                CubTemp& tmp, cudaStream_t s, WinPlan* wp = nullptr);
 
 template <typename T>
 void gather_values(const T* src, const uint32_t* perm, uint32_t nnz, T* dst, cudaStream_t s) {
@@ -221,21 +198,22 @@ void gather_values(const T* src, const uint32_t* perm, uint32_t nnz, T* dst, cud
 }
 
 // The same gather, dst[i] = src[perm[i]] for the transpose (dst in A^T order,
-// src in A order), in L2-sized WINDOWS of source rows.  A^T row c lists its
-// source rows in increasing order, so the entries of c whose source row lies
-// in window [R_w, R_w+1) are one contiguous segment: window by window, a warp
-// per long A^T row copies its next segment (a cursor per row), the window's
-// source values stay L2-resident while every column gathers from them, and the
-// destination is written in contiguous runs.  The plain gather touches a new
-// 32-byte sector for nearly every 8-byte value (lasso: 17.5 GB of DRAM traffic
-// for 3 GB of data, profiles/r01_ncu_kernels_config2.md).  A^T rows shorter than
-// kWinLongRow are gathered directly (one thread each).
+// src in A order), in L2-sized WINDOWS of source positions.  A^T row c lists
+// its source entries in increasing position (rows increase), so the entries
+// of c whose source position lies in window [P_w, P_w+1) are one contiguous
+// segment: window by window, a warp per long A^T row copies its next segment
+// (a cursor per row), the window's source stays L2-resident while every
+// column gathers from it, and the destination is written in contiguous runs.
+// The plain gather touches a new 32-byte sector for nearly every 8-byte value
+// (lasso: 17.5 GB of DRAM traffic for 3 GB of data,
+// profiles/r01_ncu_kernels_config2.md).  A^T rows shorter than kWinLongRow
+// are gathered directly (one thread each).  Used for A's values and for the
+// source-row array that becomes A^T's column indices.
 constexpr uint32_t kWinLongRow = 64;
 template <typename T>
 __global__ void win_gather_kernel(const T* __restrict__ src, const uint32_t* __restrict__ perm,
-                                  const uint32_t* __restrict__ at_rp,
-                                  const uint32_t* __restrict__ at_ci, const uint32_t* rows,
-                                  uint32_t nrows, uint32_t* cur, uint32_t r_end, T* dst) {
+                                  const uint32_t* __restrict__ at_rp, const uint32_t* rows,
+                                  uint32_t nrows, uint32_t* cur, uint32_t p_end, T* dst) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nrows; t += nw) {
@@ -244,10 +222,12 @@ __global__ void win_gather_kernel(const T* __restrict__ src, const uint32_t* __r
     const uint32_t e = at_rp[c + 1];
     for (;;) {
       const uint32_t kk = k + lane;
-      const bool in = kk < e && at_ci[kk] < r_end;
+      uint32_t sp = 0xffffffffu;
+      if (kk < e) sp = perm[kk];
+      const bool in = sp < p_end;
       const unsigned bal = __ballot_sync(0xffffffffu, in);
-      if (in) dst[kk] = src[perm[kk]];
-      const uint32_t cnt = __popc(bal);  // a prefix: the source rows increase
+      if (in) dst[kk] = src[sp];
+      const uint32_t cnt = __popc(bal);  // a prefix: the source positions increase
       k += cnt;
       if (cnt < 32u) break;
     }
@@ -279,68 +259,93 @@ static __global__ void win_flag_kernel(const uint32_t* at_rp, uint32_t n, uint32
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= n; c += gridDim.x * blockDim.x)
     f[c] = c < n && at_rp[c + 1] - at_rp[c] >= kWinLongRow;
 }
-// first row r with a_rp[r] >= w * per (window boundaries by source position)
-static __global__ void win_bounds_kernel(const uint32_t* a_rp, uint32_t m, uint64_t per,
-                                         uint32_t nwin, uint32_t* bnd) {
-  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w > nwin) return;
-  if (w == nwin) {
-    bnd[w] = m;
-    return;
+// the long / short A^T rows and the per-row cursors, shared by every gather
+// through one permutation (reset() rewinds the cursors)
+struct WinPlan {
+  uint32_t n = 0, nl = 0;
+  uint32_t *longr = nullptr, *shortr = nullptr, *cur = nullptr, *cur0 = nullptr;
+  void build(const uint32_t* at_rp, uint32_t rows, CubTemp& tmp, cudaStream_t s) {
+    n = rows;
+    uint32_t *f, *pos;
+    CK(dmalloc(&f, sizeof(uint32_t) * (size_t(n) + 1)));
+    CK(dmalloc(&pos, sizeof(uint32_t) * (size_t(n) + 1)));
+    CK(dmalloc(&longr, sizeof(uint32_t) * (size_t(n) + 1)));
+    CK(dmalloc(&shortr, sizeof(uint32_t) * (size_t(n) + 1)));
+    CK(dmalloc(&cur, sizeof(uint32_t) * (size_t(n) + 1)));
+    CK(dmalloc(&cur0, sizeof(uint32_t) * (size_t(n) + 1)));
+    win_flag_kernel<<<grid_for(uint64_t(n) + 1), kThreads, 0, s>>>(at_rp, n, f);
+    CK_LAUNCH();
+    exclusive_scan_u32(f, pos, n + 1, tmp, s);
+    win_split_kernel<<<grid_for(n), kThreads, 0, s>>>(at_rp, n, pos, longr, shortr, cur0);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(&nl, pos + n, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(dfree(f));
+    CK(dfree(pos));
   }
-  const uint64_t target = per * w;
-  uint32_t lo = 0, hi = m;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (a_rp[mid] < target) lo = mid + 1;
-    else hi = mid;
+  void release() {
+    for (void* p : {(void*)longr, (void*)shortr, (void*)cur, (void*)cur0}) CK(dfree(p));
+    longr = shortr = cur = cur0 = nullptr;
   }
-  bnd[w] = lo;
-}
+};
 template <typename T>
-void gather_values_windowed(const T* src, const uint32_t* perm, const uint32_t* at_rp,
-                            const uint32_t* at_ci, uint32_t n, const uint32_t* a_rp, uint32_t m,
-                            uint32_t nnz, T* dst, CubTemp& tmp, cudaStream_t s) {
+void gather_windowed(const T* src, const uint32_t* perm, const uint32_t* at_rp, uint32_t nnz,
+                     const WinPlan& wp, T* dst, cudaStream_t s) {
   constexpr uint64_t kWindowBytes = 32ull << 20;
   const uint64_t per = std::max<uint64_t>(1, kWindowBytes / sizeof(T));
   const uint32_t nwin = uint32_t((uint64_t(nnz) + per - 1) / per);
-  if (nwin <= 1 || n == 0) {  // one window: the plain gather is already L2-resident
-    gather_values(src, perm, nnz, dst, s);
+  if (nwin <= 1 || wp.n == 0) {  // one window: the plain gather is already L2-resident
+    for_n(nnz, [=] __device__(uint32_t i) { dst[i] = src[perm[i]]; }, s);
     return;
   }
-  uint32_t *f, *pos, *longr, *shortr, *cur, *bnd;
-  CK(dmalloc(&f, sizeof(uint32_t) * (size_t(n) + 1)));
-  CK(dmalloc(&pos, sizeof(uint32_t) * (size_t(n) + 1)));
-  CK(dmalloc(&longr, sizeof(uint32_t) * (size_t(n) + 1)));
-  CK(dmalloc(&shortr, sizeof(uint32_t) * (size_t(n) + 1)));
-  CK(dmalloc(&cur, sizeof(uint32_t) * (size_t(n) + 1)));
-  CK(dmalloc(&bnd, sizeof(uint32_t) * (size_t(nwin) + 1)));
-  win_flag_kernel<<<grid_for(uint64_t(n) + 1), kThreads, 0, s>>>(at_rp, n, f);
-  CK_LAUNCH();
-  exclusive_scan_u32(f, pos, n + 1, tmp, s);
-  win_split_kernel<<<grid_for(n), kThreads, 0, s>>>(at_rp, n, pos, longr, shortr, cur);
-  CK_LAUNCH();
-  win_bounds_kernel<<<ceil_div(nwin + 1, 256u), 256, 0, s>>>(a_rp, m, per, nwin, bnd);
-  CK_LAUNCH();
-  uint32_t nl = 0;
-  std::vector<uint32_t> hb(size_t(nwin) + 1);
-  CK(cudaMemcpyAsync(&nl, pos + n, 4, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(hb.data(), bnd, 4 * (size_t(nwin) + 1), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  if (n - nl) {
-    short_gather_kernel<T><<<grid_for(n - nl), kThreads, 0, s>>>(src, perm, at_rp, shortr, n - nl,
-                                                                 dst);
+  if (wp.n - wp.nl) {
+    short_gather_kernel<T><<<grid_for(wp.n - wp.nl), kThreads, 0, s>>>(src, perm, at_rp, wp.shortr,
+                                                                        wp.n - wp.nl, dst);
     CK_LAUNCH();
   }
-  if (nl) {
+  if (wp.nl) {
+    CK(cudaMemcpyAsync(wp.cur, wp.cur0, sizeof(uint32_t) * wp.nl, cudaMemcpyDeviceToDevice, s));
     for (uint32_t w = 0; w < nwin; ++w) {
-      win_gather_kernel<T><<<grid_for(uint64_t(nl) * 32), kThreads, 0, s>>>(
-          src, perm, at_rp, at_ci, longr, nl, cur, hb[w + 1], dst);
+      const uint32_t p_end = uint32_t(std::min<uint64_t>(nnz, per * (w + 1)));
+      win_gather_kernel<T><<<grid_for(uint64_t(wp.nl) * 32), kThreads, 0, s>>>(
+          src, perm, at_rp, wp.longr, wp.nl, wp.cur, p_end, dst);
       CK_LAUNCH();
     }
   }
-  for (void* p : {(void*)f, (void*)pos, (void*)longr, (void*)shortr, (void*)cur, (void*)bnd})
-    CK(dfree(p));
+}
+
+inline void transpose_structure(const uint32_t* ci, const uint32_t* row_of, uint32_t cols,
+                                uint32_t nnz, uint32_t* out_rp, uint32_t* out_ci, uint32_t* perm,
+                                CubTemp& tmp, cudaStream_t s, WinPlan* wp) {
+  CK(cudaMemsetAsync(out_rp, 0, sizeof(uint32_t) * (cols + 1), s));
+  if (nnz == 0) return;
+  uint32_t *cnt, *keys_out, *idx;
+  CK(dmalloc(&cnt, sizeof(uint32_t) * (cols + 1)));
+  CK(dmalloc(&keys_out, sizeof(uint32_t) * nnz));
+  CK(dmalloc(&idx, sizeof(uint32_t) * nnz));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (cols + 1), s));
+  count_cols_kernel<<<grid_for(nnz), kThreads, 0, s>>>(ci, nnz, cnt);
+  CK_LAUNCH();
+  exclusive_scan_u32(cnt, out_rp, cols + 1, tmp, s);  // cnt[cols] == 0 -> out_rp[cols] = nnz
+  iota_kernel<<<grid_for(nnz), kThreads, 0, s>>>(idx, nnz);
+  CK_LAUNCH();
+  size_t b = 0;
+  const int nb = bits_for(cols);
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, b, ci, keys_out, idx, perm, nnz, 0, nb, s));
+  tmp.ensure(b);
+  CK(cub::DeviceRadixSort::SortPairs(tmp.ptr, b, ci, keys_out, idx, perm, nnz, 0, nb, s));
+  // out_ci[i] = row_of[perm[i]], windowed like the value gathers
+  if (wp) {
+    wp->build(out_rp, cols, tmp, s);
+    gather_windowed(row_of, perm, out_rp, nnz, *wp, out_ci, s);
+  } else {
+    const uint32_t* perm_c = perm;
+    for_n(nnz, [=] __device__(uint32_t i) { out_ci[i] = row_of[perm_c[i]]; }, s);
+  }
+  // (frees are ordered on s: dmalloc / dfree follow the caller's AllocScope(s))
+  CK(dfree(cnt));
+  CK(dfree(keys_out));
+  CK(dfree(idx));
 }
 
 // ---------------------------------------------------- symmetrize_upper

@@ -153,6 +153,7 @@ class Workspace : public IEngine<T> {
   qpcg_options opt{};
   std::vector<void*> allocs;
   uint32_t* permA = nullptr;  // transpose permutation of A
+  WinPlan winA;               // its windowed-gather plan (setup only)
   uint32_t* p_rows = nullptr;  // rows of P_full with entries (ordered mean)
   uint32_t n_prows = 0;
   T* ruiz_scal = nullptr;      // [mean, qinf, gamma, c, dev]
@@ -552,7 +553,7 @@ class Workspace : public IEngine<T> {
     uint32_t* at_rp = alloc<uint32_t>(n + 1);
     uint32_t* at_ci = alloc<uint32_t>(annz);
     permA = alloc<uint32_t>(annz);
-    transpose_structure(a_ci, row_of, n, annz, at_rp, at_ci, permA, tmp, s);
+    transpose_structure(a_ci, row_of, n, annz, at_rp, at_ci, permA, tmp, s, &winA);
     tmark("transpose struct");
     D.pAT = plan_build<T>(at_rp, n, annz, tmp, s);
     tmark("plan A^T");
@@ -565,7 +566,7 @@ class Workspace : public IEngine<T> {
     check_values_late();
     tmark("values");
     T* ato_v = alloc<T>(annz);
-    gather_values_windowed(a_v, permA, at_rp, at_ci, n, a_rp, m, annz, ato_v, tmp, s);
+    gather_windowed(a_v, permA, at_rp, annz, winA, ato_v, s);
     tmark("A_orig^T gather");
     D.Ao = DevCsr<T>{m, n, annz, a_v, a_rp, a_ci};
     D.ATo = DevCsr<T>{n, m, annz, ato_v, at_rp, at_ci};
@@ -694,9 +695,8 @@ class Workspace : public IEngine<T> {
     const uint32_t n = D.n, m = D.m;
     equil_passes = passes;
     equil_residual = deviation;
-    if (set.scaling_enabled)
-      gather_values_windowed(D.A.val, permA, D.AT.rp, D.AT.ci, n, D.A.rp, m, D.A.nnz, D.AT.val,
-                             tmp, s);
+    if (set.scaling_enabled) gather_windowed(D.A.val, permA, D.AT.rp, D.A.nnz, winA, D.AT.val, s);
+    winA.release();  // (the transpose permutation's last use)
     {
       T *d = D.d, *e = D.e, *di = D.d_inv, *ei = D.e_inv, *lo = D.l_o, *uo = D.u_o, *ls = D.l,
         *us = D.u;
