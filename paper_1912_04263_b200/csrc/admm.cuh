@@ -1264,7 +1264,9 @@ __global__ void __launch_bounds__(kThreads) k_objective(Dev<T> D) {
 // max-norm helper (q_inf etc.)
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_infnorm(const T* v, uint32_t n, T* part,
-                                                     uint32_t* counter, T* out) {
+                                                     uint32_t* counter, T* out,
+                                                     const uint32_t* act = nullptr) {
+  if (act && !*act) return;  // (an inactive Ruiz pass)
   T a[1] = {T(0)};
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     a[0] = smax(a[0], tabs(v[i]));

@@ -27,7 +27,9 @@ namespace qpcg_b200 {
 // -------------------------------------------------------- visitor kernels
 // Calls f(row, k) for every stored entry, driven by a plan (load balanced).
 template <typename T, class F>
-__global__ void __launch_bounds__(kThreads) plan_visit_kernel(DevCsr<T> M, SpmvPlan<T> P, F f) {
+__global__ void __launch_bounds__(kThreads) plan_visit_kernel(DevCsr<T> M, SpmvPlan<T> P, F f,
+                                                             const uint32_t* act) {
+  if (act && !*act) return;  // (an inactive Ruiz pass)
   if (blockIdx.x < P.nb_items) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t it = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -42,9 +44,10 @@ __global__ void __launch_bounds__(kThreads) plan_visit_kernel(DevCsr<T> M, SpmvP
   }
 }
 template <typename T, class F>
-void plan_visit(const DevCsr<T>& M, const SpmvPlan<T>& P, F f, cudaStream_t s) {
+void plan_visit(const DevCsr<T>& M, const SpmvPlan<T>& P, F f, cudaStream_t s,
+                const uint32_t* act = nullptr) {
   if (P.grid() == 0) return;
-  plan_visit_kernel<T, F><<<P.grid(), kThreads, 0, s>>>(M, P, f);
+  plan_visit_kernel<T, F><<<P.grid(), kThreads, 0, s>>>(M, P, f, act);
   CK_LAUNCH();
 }
 
@@ -428,14 +431,16 @@ uint32_t symmetrize_upper_dev(const DevCsr<T>& up, const uint32_t* up_row_of, De
 template <typename T>
 struct StoreEpi {
   T* out;
-  __device__ bool init() { return true; }
+  const uint32_t* act = nullptr;  // an inactive Ruiz pass: no-op
+  __device__ bool init() { return act == nullptr || *act != 0u; }
   __device__ void operator()(uint32_t r, const T (&s)[1]) const { out[r] = s[0]; }
 };
 
 template <typename T>
-void row_inf_norms(const DevCsr<T>& M, const SpmvPlan<T>& P, T* out, cudaStream_t s) {
+void row_inf_norms(const DevCsr<T>& M, const SpmvPlan<T>& P, T* out, cudaStream_t s,
+                   const uint32_t* act = nullptr) {
   if (M.rows == 0) return;
-  launch_spmv<T, 1, MaxAbsOp>(M, P, GatherNone<T, 1>{}, StoreEpi<T>{out}, s);
+  launch_spmv<T, 1, MaxAbsOp>(M, P, GatherNone<T, 1>{}, StoreEpi<T>{out, act}, s);
 }
 
 // One Ruiz scaling visit, v = (v * dr[row]) * dc[col] (scale_rows then
@@ -448,7 +453,9 @@ template <typename T, int U>
 __global__ void __launch_bounds__(kThreads) scale_norm_kernel(DevCsr<T> M, SpmvPlan<T> P,
                                                               const T* src,
                                                               const T* __restrict__ dr,
-                                                              const T* __restrict__ dc, T* norm) {
+                                                              const T* __restrict__ dc, T* norm,
+                                                              const uint32_t* act) {
+  if (act && !*act) return;
   if (blockIdx.x < P.nb_items) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t it = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -495,9 +502,9 @@ __global__ void __launch_bounds__(kThreads) scale_norm_kernel(DevCsr<T> M, SpmvP
 // pass, which then also initialises M.val)
 template <typename T>
 void scale_and_norms(const DevCsr<T>& M, const SpmvPlan<T>& P, const T* src, const T* dr,
-                     const T* dc, T* norm, cudaStream_t s) {
+                     const T* dc, T* norm, cudaStream_t s, const uint32_t* act = nullptr) {
   if (P.grid() == 0) return;
-  scale_norm_kernel<T, 4><<<P.grid(), kThreads, 0, s>>>(M, P, src, dr, dc, norm);
+  scale_norm_kernel<T, 4><<<P.grid(), kThreads, 0, s>>>(M, P, src, dr, dc, norm, act);
   CK_LAUNCH();
 }
 
@@ -549,10 +556,15 @@ constexpr int kMeanTile = 2048;
 template <typename T>
 __global__ void __launch_bounds__(256) ordered_mean_kernel(const T* __restrict__ v,
                                                           const uint32_t* __restrict__ list,
-                                                          uint32_t cnt, uint32_t n, T* out) {
+                                                          uint32_t cnt, uint32_t n, T* out,
+                                                          const uint32_t* act = nullptr) {
+  if (act && !*act) return;
   __shared__ T buf[2][kMeanTile];
   const uint32_t tid = threadIdx.x;
-  for (uint32_t i = tid; i < kMeanTile && i < cnt; i += blockDim.x) buf[0][i] = v[list[i]];
+  // list == nullptr: v is already packed (pack_list_kernel), the tile loads
+  // are then coalesced and quick even while the main stream saturates HBM
+  for (uint32_t i = tid; i < kMeanTile && i < cnt; i += blockDim.x)
+    buf[0][i] = list ? v[list[i]] : v[i];
   __syncthreads();
   T s = T(0);
   for (uint32_t t = 0; uint64_t(t) * kMeanTile < cnt; ++t) {
@@ -560,7 +572,7 @@ __global__ void __launch_bounds__(256) ordered_mean_kernel(const T* __restrict__
     const uint64_t base_next = uint64_t(t + 1) * kMeanTile;
     if (tid >= 32) {
       for (uint32_t i = tid - 32; i < kMeanTile && base_next + i < cnt; i += blockDim.x - 32)
-        buf[nxt][i] = v[list[base_next + i]];
+        buf[nxt][i] = list ? v[list[base_next + i]] : v[base_next + i];
     } else if (tid == 0) {
       const uint32_t m = uint32_t(min(uint64_t(kMeanTile), uint64_t(cnt) - uint64_t(t) * kMeanTile));
       const T* b = buf[cur];
@@ -577,6 +589,15 @@ __global__ void __launch_bounds__(256) ordered_mean_kernel(const T* __restrict__
     __syncthreads();
   }
   if (tid == 0) *out = s / T(n);
+}
+
+// packed[i] = v[list[i]] (the ordered mean's operands, gathered in parallel)
+template <typename T>
+__global__ void pack_list_kernel(const T* __restrict__ v, const uint32_t* __restrict__ list,
+                                 uint32_t cnt, T* packed, const uint32_t* act) {
+  if (act && !*act) return;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+    packed[i] = v[list[i]];
 }
 
 // rows of a CSR structure with at least one stored entry, in increasing order

@@ -58,13 +58,19 @@ inline double now_s() {
 }
 
 // ------------------------------------------------------------ setup kernels
+// act: this pass runs (device flag); act_next (nullable): written with
+// whether the next pass runs, (more && deviation > eps) — the loop test of
+// scaling.hpp:116 decided on the device, so the passes need no host sync
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_ruiz_delta(const T* pn, const T* atn, uint32_t n,
                                                         const T* an, uint32_t m, T* dx, T* dz,
                                                         T* d, T* e, T* q, T* part,
-                                                        uint32_t* counter, T* dev_out) {
+                                                        uint32_t* counter, T* dev_out,
+                                                        const uint32_t* act, uint32_t* act_next,
+                                                        uint32_t more, T eps) {
   // scaling.hpp:125-138: delta = 1/sqrt(col norm) (1 for empty), D *= dx, E *= dz,
   // q *= dx; deviation = |1 - delta|_inf (:163-165)
+  if (act && !*act) return;
   T v[1] = {T(0)};
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -84,12 +90,16 @@ __global__ void __launch_bounds__(kThreads) k_ruiz_delta(const T* pn, const T* a
   }
   T tot[1];
   if (!grid_reduce<T, 1>(v, 0x1u, part, counter, tot)) return;
-  if (threadIdx.x == 0) *dev_out = tot[0];
+  if (threadIdx.x == 0) {
+    *dev_out = tot[0];
+    if (act_next) *act_next = (more && tot[0] > eps) ? 1u : 0u;
+  }
 }
 
 // gamma = 1/max(mean, |q|_inf) (1 if 0); c *= gamma  (scaling.hpp:159-162)
 template <typename T>
-__global__ void k_ruiz_gamma(const T* mean, const T* qinf, T* gamma, T* c) {
+__global__ void k_ruiz_gamma(const T* mean, const T* qinf, T* gamma, T* c, const uint32_t* act) {
+  if (act && !*act) return;
   const T denom = smax(*mean, *qinf);
   const T g = denom > T(0) ? T(1) / denom : T(1);
   *gamma = g;
@@ -97,7 +107,8 @@ __global__ void k_ruiz_gamma(const T* mean, const T* qinf, T* gamma, T* c) {
 }
 
 template <typename T>
-__global__ void k_scale_by(T* v, uint32_t n, const T* g) {
+__global__ void k_scale_by(T* v, uint32_t n, const T* g, const uint32_t* act) {
+  if (act && !*act) return;
   const T s = *g;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     v[i] *= s;
@@ -282,15 +293,31 @@ class Workspace : public IEngine<T> {
     uint32_t passes = 0;
     T deviation = T(0);
     if (set.scaling_enabled) {
+      // every pass enqueued at once: pass p's kernels run iff rz_act[p]
+      // (k_ruiz_delta of pass p - 1 decides), one synchronisation at the end
       ruiz_prepare();
-      deviation = T(1);
-      while (passes < set.equil_max_passes && deviation > T(set.eps_equil)) {
-        ++passes;
-        ruiz_norms();
-        ruiz_delta();
-        ruiz_scale();
-        deviation = read_scalar(ruiz_scal + 4);
+      tmark("ruiz prepare");
+      const uint32_t P = set.equil_max_passes;
+      rz_act = alloc<uint32_t>(size_t(P) + 1);
+      rz_dev = vec(size_t(P) + 1, true);
+      CK(cudaMemsetAsync(rz_act, 0, sizeof(uint32_t) * (size_t(P) + 1), s));
+      const uint32_t one = 1u;
+      CK(cudaMemcpyAsync(rz_act, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+      for (uint32_t p = 0; p < P; ++p) {
+        ruiz_norms(int(p));
+        ruiz_delta(int(p));
+        ruiz_scale(int(p));
+        if (p < 2) tmark(p == 0 ? "ruiz pass 0" : "ruiz pass 1");
       }
+      std::vector<uint32_t> act(size_t(P) + 1);
+      std::vector<T> dev(size_t(P) + 1);
+      CK(cudaMemcpyAsync(act.data(), rz_act, sizeof(uint32_t) * (size_t(P) + 1),
+                         cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(dev.data(), rz_dev, sizeof(T) * (size_t(P) + 1), cudaMemcpyDeviceToHost,
+                         s));
+      CK(cudaStreamSynchronize(s));
+      while (passes < P && act[passes]) ++passes;
+      deviation = passes ? dev[passes - 1] : T(1);
     }
     mark("ruiz");
     finish_scaling(passes, deviation);
@@ -630,23 +657,35 @@ class Workspace : public IEngine<T> {
     n_prows = scan_total(flags, pos, n, s);
     compact_kernel<<<grid_for(n), kThreads, 0, s>>>(flags, pos, n, p_rows);
     CK_LAUNCH();
+    rz_packed = vec(size_t(n_prows) + 1, false);
   }
+  T* rz_packed = nullptr;  // P's row norms of the nonempty rows, packed for the ordered mean
   // the A / A^T row norms of the current values: computed here in the first
   // pass, afterwards by the previous pass's fused scaling visit
   bool rz_norms_fresh = false;
-  void ruiz_norms() {
-    row_inf_norms(D.P, D.pP, rz_pn, s);
+  // rz_act[p]: pass p runs (device flags; the unsharded setup enqueues every
+  // pass without a host synchronisation and k_ruiz_delta decides the next);
+  // rz_dev[p]: pass p's deviation
+  uint32_t* rz_act = nullptr;
+  T* rz_dev = nullptr;
+  const uint32_t* act_of(int pass) const { return pass < 0 ? nullptr : rz_act + pass; }
+  void ruiz_norms(int pass = -1) {
+    const uint32_t* act = act_of(pass);
+    row_inf_norms(D.P, D.pP, rz_pn, s, act);
     if (D.m == 0 || D.AT.nnz == 0)  // empty block: no column contributes
       CK(cudaMemsetAsync(rz_atn, 0, sizeof(T) * D.n, s));
     else if (!rz_norms_fresh)  // (first pass: the scaled copies are not written yet)
-      row_inf_norms(D.ATo, D.pAT, rz_atn, s);
-    if (!rz_norms_fresh) row_inf_norms(D.Ao, D.pA, rz_an, s);
+      row_inf_norms(D.ATo, D.pAT, rz_atn, s, act);
+    if (!rz_norms_fresh) row_inf_norms(D.Ao, D.pA, rz_an, s, act);
   }
-  void ruiz_delta() {
+  void ruiz_delta(int pass = -1) {
     const uint32_t n = D.n, m = D.m;
+    const bool dev_loop = pass >= 0;
     k_ruiz_delta<T><<<red_grid<T>(std::max(n, m)), kThreads, 0, s>>>(
         rz_pn, rz_atn, n, rz_an, m, rz_dx, rz_dz, D.d, D.e, D.q, D.red, &D.ctl->red_counter,
-        ruiz_scal + 4);
+        dev_loop ? rz_dev + pass : ruiz_scal + 4, act_of(pass),
+        dev_loop ? rz_act + pass + 1 : nullptr,
+        dev_loop && uint32_t(pass + 1) < set.equil_max_passes ? 1u : 0u, T(set.eps_equil));
     CK_LAUNCH();
   }
   // The cost scaling (the sequential mean of P's row norms, |q|, gamma, P and
@@ -654,15 +693,26 @@ class Workspace : public IEngine<T> {
   // main stream scales A and A^T (the mean is a latency-bound dependent chain).
   cudaStream_t s_side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  void ruiz_scale() {
+  void ruiz_scale(int pass = -1) {
     const uint32_t n = D.n;
+    const uint32_t* act = act_of(pass);
     if (!s_side) {
-      CK(cudaStreamCreateWithFlags(&s_side, cudaStreamNonBlocking));
+      // high priority: the side stream's one-block sequential mean must get an
+      // SM as soon as one frees up, not after the main stream's full-grid
+      // scaling visits (it is a ~0.5 ms dependent chain at config 2)
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&s_side, cudaStreamNonBlocking, hi));
       CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
-    plan_visit(D.P, D.pP, ScaleRowColFn<T>{D.P.val, D.P.ci, rz_dx, rz_dx}, s);
-    row_inf_norms(D.P, D.pP, rz_pn, s);
+    plan_visit(D.P, D.pP, ScaleRowColFn<T>{D.P.val, D.P.ci, rz_dx, rz_dx}, s, act);
+    row_inf_norms(D.P, D.pP, rz_pn, s, act);
+    static const bool serial = [] {
+      const char* e = std::getenv("QPCG_RUIZ_SERIAL");
+      return e && e[0] == '1';
+    }();
+    cudaStream_t s_side = serial ? s : this->s_side;
     CK(cudaEventRecord(ev_fork, s));
     CK(cudaStreamWaitEvent(s_side, ev_fork, 0));
     // cost scaling (scaling.hpp:156-162), side stream
@@ -670,21 +720,28 @@ class Workspace : public IEngine<T> {
     T* qinf = ruiz_scal + 1;
     T* gamma = ruiz_scal + 2;
     T* cc = ruiz_scal + 3;
-    ordered_mean_kernel<T><<<1, 256, 0, s_side>>>(rz_pn, p_rows, n_prows, n, mean);
+    if (n_prows) {
+      pack_list_kernel<T><<<grid_for(n_prows), kThreads, 0, s_side>>>(rz_pn, p_rows, n_prows,
+                                                                      rz_packed, act);
+      CK_LAUNCH();
+    }
+    ordered_mean_kernel<T><<<1, 256, 0, s_side>>>(rz_packed, nullptr, n_prows, n, mean, act);
     CK_LAUNCH();
-    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s_side>>>(D.q, n, D.red, &D.ctl->red_counter, qinf);
+    k_infnorm<T><<<red_grid<T>(n), kThreads, 0, s_side>>>(D.q, n, D.red, &D.ctl->red_counter, qinf,
+                                                          act);
     CK_LAUNCH();
-    k_ruiz_gamma<T><<<1, 1, 0, s_side>>>(mean, qinf, gamma, cc);
+    k_ruiz_gamma<T><<<1, 1, 0, s_side>>>(mean, qinf, gamma, cc, act);
     CK_LAUNCH();
-    k_scale_by<T><<<grid_for(D.P.nnz), kThreads, 0, s_side>>>(D.P.val, D.P.nnz, gamma);
-    k_scale_by<T><<<grid_for(n), kThreads, 0, s_side>>>(D.q, n, gamma);
+    k_scale_by<T><<<grid_for(D.P.nnz), kThreads, 0, s_side>>>(D.P.val, D.P.nnz, gamma, act);
+    k_scale_by<T><<<grid_for(n), kThreads, 0, s_side>>>(D.q, n, gamma, act);
     CK_LAUNCH();
     CK(cudaEventRecord(ev_join, s_side));
     // main stream meanwhile: A rows (dz) then cols (dx); A^T rows (dx) then cols (dz)
     // (+ the row norms of the scaled values for the next pass)
     // first pass: read the originals, write the scaled copies
-    scale_and_norms(D.A, D.pA, rz_norms_fresh ? D.A.val : D.Ao.val, rz_dz, rz_dx, rz_an, s);
-    scale_and_norms(D.AT, D.pAT, rz_norms_fresh ? D.AT.val : D.ATo.val, rz_dx, rz_dz, rz_atn, s);
+    scale_and_norms(D.A, D.pA, rz_norms_fresh ? D.A.val : D.Ao.val, rz_dz, rz_dx, rz_an, s, act);
+    scale_and_norms(D.AT, D.pAT, rz_norms_fresh ? D.AT.val : D.ATo.val, rz_dx, rz_dz, rz_atn, s,
+                    act);
     rz_norms_fresh = true;
     CK(cudaStreamWaitEvent(s, ev_join, 0));
   }
