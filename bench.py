@@ -254,8 +254,8 @@ class Engine:
             raise RuntimeError(self.lib.qpcg_last_error(None).decode())
         try:
             out = np.zeros(12)
-            self.lib.qpcg_bench_kernels.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
-            rc = self.lib.qpcg_bench_kernels(ws, reps, out.ctypes.data)
+            self.lib.qpcg_bench_kernels_n.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32]
+            rc = self.lib.qpcg_bench_kernels_n(ws, reps, out.ctypes.data, 12)
             if rc != 0:
                 raise RuntimeError(self.lib.qpcg_last_error(ws).decode())
         finally:

@@ -56,15 +56,16 @@ int qpcg_debug_operator(qpcg_workspace* ws, const void* x, void* kx, void* diag_
 /* Times `reps` launches each of the PCG-iteration kernels on the workspace's
  * stream with CUDA events.  out[0] ms per A pass (t = rho A p), out[1] ms per
  * A^T pass (Kp = P p + sigma p + A^T t), out[2] ms per whole PCG iteration
- * (5 kernels), out[3..5] algorithmic bytes of each (4-byte
- * column indices), out[6..8] the same with the bytes of the matrix formats
- * actually streamed (16-bit compressed column offsets where used).
- * out[9] ms per one-pass kernel k_gram (the operator apply with A streamed
- * once, csrc/gram.cuh; 0 when the workspace runs the two-pass path),
- * out[10] its bytes, out[11] the bytes of a whole PCG iteration on that path.
- * The A / A^T pass timings are taken either way; out[2] times the path the
- * solve uses.  out must hold 12 doubles. */
+ * (the path the solve uses), out[3..5] algorithmic bytes of each (SURVEY
+ * §8(d): 4-byte column indices), out[6..8] the same with the bytes of the
+ * matrix formats actually streamed (16-bit compressed column offsets where
+ * used).  qpcg_bench_kernels writes these 9 doubles; qpcg_bench_kernels_n
+ * writes min(cap, QPCG_BENCH_KERNELS_MAX) and adds out[9] ms per one-pass
+ * kernel k_gram (csrc/gram.cuh, opt-in; 0 when off), out[10] its bytes,
+ * out[11] the bytes of a whole PCG iteration on that path. */
+#define QPCG_BENCH_KERNELS_MAX 12
 int qpcg_bench_kernels(qpcg_workspace* ws, uint32_t reps, double* out);
+int qpcg_bench_kernels_n(qpcg_workspace* ws, uint32_t reps, double* out, uint32_t cap);
 
 #ifdef __cplusplus
 }

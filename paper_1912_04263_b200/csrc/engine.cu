@@ -290,8 +290,14 @@ int qpcg_debug_operator(qpcg_workspace* ws, const void* x, void* kx, void* dinv)
 }
 
 int qpcg_bench_kernels(qpcg_workspace* ws, uint32_t reps, double* out) {
-  // (sharded workspaces: the kernels of this process's first row block)
-  return either(ws, [&](auto& e) { e.bench_kernels(reps, out); });
+  return qpcg_bench_kernels_n(ws, reps, out, 9);  // the round-1 layout: 9 doubles
+}
+int qpcg_bench_kernels_n(qpcg_workspace* ws, uint32_t reps, double* out, uint32_t cap) {
+  double full[QPCG_BENCH_KERNELS_MAX] = {};
+  const int rc = either(ws, [&](auto& e) { e.bench_kernels(reps, full); });
+  if (rc == QPCG_OK && out != nullptr)
+    for (uint32_t i = 0; i < cap && i < QPCG_BENCH_KERNELS_MAX; ++i) out[i] = full[i];
+  return rc;
 }
 
 }  // extern "C"

@@ -15,7 +15,7 @@ from paper_1912_04263_b200.problem import Settings
 
 S = Settings(lambda_pcg=1e-3)
 lib = solver.load_library()
-lib.qpcg_bench_kernels.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
+lib.qpcg_bench_kernels_n.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32]
 for cfg in sys.argv[1:] or ["2", "3", "4"]:
     p = G.config(cfg)
     if cfg == "4":
@@ -25,7 +25,7 @@ for cfg in sys.argv[1:] or ["2", "3", "4"]:
         with solver.Workspace(p, S, device=0) as ws:
             r = ws.solve()
             out = np.zeros(12)
-            lib.qpcg_bench_kernels(ws.ws, 20, out.ctypes.data)
+            lib.qpcg_bench_kernels_n(ws.ws, 20, out.ctypes.data, 12)
         t = time.time()
         r2 = solver.solve(p, S, device=0)
         print(json.dumps({"config": cfg, "gram": gram, "status": r.status,
