@@ -197,3 +197,23 @@ def test_nccl_before_torch_import():
         __import__("os").path.dirname(__import__("os").path.dirname(__file__)))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok True" in r.stdout, r.stderr[-2000:]
+
+
+def test_bench_kernels_output_sizes():
+    """qpcg_bench_kernels writes exactly its documented 9 doubles (callers size
+    their buffers for it); qpcg_bench_kernels_n writes at most `cap`."""
+    import ctypes as C
+    lib = solver.load_library()
+    lib.qpcg_bench_kernels.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
+    lib.qpcg_bench_kernels_n.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32]
+    p = G.generate("lasso", 4, 0)
+    with solver.Workspace(p, S, device=0) as ws:
+        out = np.full(16, -7.0)
+        assert lib.qpcg_bench_kernels(ws.ws, 2, out.ctypes.data) == 0
+        assert np.all(out[9:] == -7.0) and np.all(out[:3] > 0)
+        out = np.full(16, -7.0)
+        assert lib.qpcg_bench_kernels_n(ws.ws, 2, out.ctypes.data, 5) == 0
+        assert np.all(out[5:] == -7.0)
+        out = np.full(16, -7.0)
+        assert lib.qpcg_bench_kernels_n(ws.ws, 2, out.ctypes.data, 16) == 0
+        assert np.all(out[12:] == -7.0)
