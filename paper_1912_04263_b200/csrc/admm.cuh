@@ -44,7 +44,9 @@ struct Ctl {
   T objective;
   // reductions / diagnostics
   uint32_t red_counter, n_calls, n_checks, n_rho;
-  uint32_t inf_branch, rho_branch, diag_cap, n_inf, n_rho_branch, pad_;
+  uint32_t inf_branch, rho_branch, diag_cap, n_inf, n_rho_branch;
+  // 1: z~ = A x~ carried through PCG as z~ += alpha_k (A p_k) (see zt_pass)
+  uint32_t zt_recur;
 };
 
 // diagnostics records (device side, converted to qpcg_pcg_call on the host)
@@ -87,6 +89,7 @@ struct Dev {
   T *x, *z, *y, *xt, *zt, *dx, *dy;
   // PCG workspace
   T *b, *r, *p, *kp, *best, *dinv, *t, *diag_p, *diag_ata;
+  T* ap;  // [m] A p of the current PCG iteration (unscaled by rho), for the z~ recurrence
   // residual workspace (ResidualData, solver.hpp:181-188)
   T *ax, *px, *aty, *rdual;
   // outputs (unscaled)
@@ -311,17 +314,24 @@ struct EpiRhs {
   }
 };
 
-// t = rho (A p)   (linsys.hpp:84-85)
+// t = rho (A p)   (linsys.hpp:84-85); with the z~ recurrence on, A p itself
+// is kept as well (ap, read by k_pcg_update once alpha_k is known)
 template <typename T>
 struct EpiAp {
   T* t;
+  T* ap;  // nullptr: not kept
   const Ctl<T>* ctl;
-  T rho;
+  T rho = T(0);
+  bool keep = false;
   __device__ __forceinline__ bool init() {
     rho = ctl->rho;
+    keep = ap != nullptr && ctl->zt_recur != 0;
     return ctl->pcg_active != 0 && ctl->error == 0;
   }
-  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const { t[r] = s[0] * rho; }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const {
+    t[r] = s[0] * rho;
+    if (keep) ap[r] = s[0];
+  }
 };
 
 // Kp = (P p + sigma p) + A^T t   (linsys.hpp:86-89)
@@ -341,6 +351,23 @@ struct EpiKp {
     D.kp[r] = kp_row(D, sigma, r, s[0]);
   }
 };
+
+// Whether the ADMM step needs the z~ pass (z~ = A x~, solver.hpp:359) after
+// this PCG solve.  With the recurrence on (Ctl::zt_recur), z~ is carried
+// through PCG by linearity: the warm start is the previous x~ whose A x~ is
+// the previous z~, and every x_{k+1} = x_k + alpha_k p_k adds alpha_k (A p_k),
+// which the PCG A pass has just computed (EpiAp keeps it), so the full
+// matrix read of the z~ pass is skipped.  It still runs (and overwrites the
+// carried z~ with the directly computed product) on check iterations, where
+// the 2-column pass also forms A x_new for the residuals (which therefore stay
+// the reference's direct products, and the carried rounding restarts every
+// check_interval steps), and when PCG did not return its last iterate (cap:
+// best iterate; b == 0: zero).
+template <typename T>
+__device__ __forceinline__ bool zt_pass(const Ctl<T>* C) {
+  return C->zt_recur == 0 || C->pcg_exit != kPcgConverged ||
+         ((C->iter + 1) % C->check_interval) == 0;
+}
 
 // z~ = A x~ with the whole m-side ADMM update fused (solver.hpp:360-378);
 // col1 (check iterations only) = A x_new with x_new formed on the fly exactly
@@ -369,7 +396,7 @@ struct EpiAdmm {
     one_m_alpha = T(1) - alpha;
     rho = D.ctl->rho;
     two = ((D.ctl->iter + 1) % D.ctl->check_interval) == 0;
-    return D.ctl->error == 0 && two == (NCOL == 2);
+    return D.ctl->error == 0 && two == (NCOL == 2) && zt_pass(D.ctl);
   }
   __device__ __forceinline__ void prefetch(uint32_t r) const {
     prefetch_l1(D.z + r);
@@ -406,17 +433,19 @@ struct EpiAdmmStore {
   Dev<T> D;
   __device__ __forceinline__ bool init() {
     const bool two = ((D.ctl->iter + 1) % D.ctl->check_interval) == 0;
-    return D.ctl->error == 0 && two == (NCOL == 2);
+    return D.ctl->error == 0 && two == (NCOL == 2) && zt_pass(D.ctl);
   }
   __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[NCOL]) const {
     D.zt[r] = s[0];
     if constexpr (NCOL == 2) D.ax[r] = s[1];
   }
 };
+// always: after an EpiAdmmStore pass (short-row plans); else only when the
+// z~ pass was skipped (the fused EpiAdmm epilogue did not run)
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_admm_mside(Dev<T> D) {
+__global__ void __launch_bounds__(kThreads) k_admm_mside(Dev<T> D, bool always) {
   const Ctl<T>* C = D.ctl;
-  if (C->error) return;
+  if (C->error || (!always && zt_pass(C))) return;
   const T alpha = C->alpha, oma = T(1) - alpha, rho = C->rho;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < D.m; j += gridDim.x * blockDim.x)
     EpiAdmm<T, 1>::mside(D, alpha, oma, rho, j, D.zt[j]);
@@ -710,6 +739,9 @@ __device__ __forceinline__ void pcg_update_elems(const Dev<T>& D, uint32_t t0, u
             v[0] += ri * yi;
             v[1] = smax(v[1], tabs(ri));
           });
+  if (D.ctl->zt_recur)  // z~ += a (A p)  (zt_pass)
+    strided(t0, stride, D.m, [&](uint32_t j) { return V2<T>{D.zt[j], D.ap[j]}; },
+            [&](uint32_t j, const V2<T>& e) { D.zt[j] = e.a + a * e.b; });
 }
 template <typename T>
 __device__ void pcg_update_decide(Ctl<T>* C, const T (&tot)[2], Handles H) {

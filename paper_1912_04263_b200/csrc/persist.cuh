@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
     }
     // ---- PCG iterations
     while (C->pcg_active && !C->error) {
-      spmv_phase<T, 1, SumOp>(grid, D.A, D.pA, GatherVec<T, false>{D.p}, EpiAp<T>{D.t, C, T(0)});
+      spmv_phase<T, 1, SumOp>(grid, D.A, D.pA, GatherVec<T, false>{D.p}, EpiAp<T>{D.t, D.ap, C});
       grid.sync();
       spmv_phase<T, 1, SumOp>(grid, D.AT, D.pAT, GatherVec<T, false>{D.t}, EpiKp<T>{D, T(0)});
       grid.sync();
@@ -183,6 +183,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
                             EpiAdmm<T, 2>{D, T(0), T(0), T(0), false});
     spmv_phase<T, 1, SumOp>(grid, D.A, D.pA, GatherVec<T, false>{D.xt},
                             EpiAdmm<T, 1>{D, T(0), T(0), T(0), false});
+    if (!C->error && !zt_pass(C)) {  // z~ carried through PCG: the m-side update alone
+      const T alpha = C->alpha, oma = T(1) - alpha, rho = C->rho;
+      for (uint32_t j = t0; j < D.m; j += stride) EpiAdmm<T, 1>::mside(D, alpha, oma, rho, j, D.zt[j]);
+    }
     grid.sync();
     if (!C->error) {
       xupdate_elems(D, t0, stride);

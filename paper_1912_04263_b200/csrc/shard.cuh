@@ -265,7 +265,7 @@ class Sharded : public IEngine<T> {
   void enq_pcg_iter(Handles H = {}) {
     int li = 0;
     each([&](Workspace<T>& w) {
-      launch_spmv<T, 1, SumOp>(w.D.A, w.D.pA, GatherVec<T>{w.D.p}, EpiAp<T>{w.D.t, w.D.ctl, T(0)}, w.s);
+      launch_spmv<T, 1, SumOp>(w.D.A, w.D.pA, GatherVec<T>{w.D.p}, EpiAp<T>{w.D.t, w.D.ap, w.D.ctl}, w.s);
       at_pass_combined<1>(w, li++, GatherVec<T>{w.D.t}, 1);
     });
     combine_parts(n);

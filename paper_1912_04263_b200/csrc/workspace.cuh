@@ -787,7 +787,7 @@ class Workspace : public IEngine<T> {
     D.kp = vec(n); D.best = vec(n); D.px = vec(n); D.aty = vec(n); D.rdual = vec(n);
     D.xo = vec(n); D.pxo = vec(n);
     D.z = vec(m); D.y = vec(m); D.zt = vec(m); D.dy = vec(m); D.t = vec(m); D.ax = vec(m);
-    D.zo = vec(m); D.yo = vec(m);
+    D.zo = vec(m); D.yo = vec(m); D.ap = vec(m);
     D.cert = vec(std::max(n, m));
     D.g2m = alloc<pair_t<T>>(m);
     D.g2n = alloc<pair_t<T>>(n);
@@ -825,6 +825,7 @@ class Workspace : public IEngine<T> {
     hc.rho = T(st.rho_bar_init);
     hc.status = QPCG_STATUS_MAX_ITER_REACHED;
     hc.diag_cap = cap;
+    hc.zt_recur = zt_recur_enabled();
     push_ctl();
     k_precond<T><<<grid_for(n), kThreads, 0, s>>>(D, 1);
     CK_LAUNCH();
@@ -1060,6 +1061,8 @@ class Workspace : public IEngine<T> {
       gHi = plan_build<T>(atHi.rp, n - (b + 1), rp[n] - rp[b + 1], tmp, s);
     }
     gram_on = true;
+    hc.zt_recur = 0;  // the one-pass apply forms A p inside the Gram product, not kept
+    push_ctl();
     if (const char* tr = std::getenv("QPCG_GRAM_TRACE"); tr && tr[0] == '1')
       std::fprintf(stderr,
                    "[gram] window [%u, %u) W=%u, row-pass rows %u (max %u entries, slot %u), thin "
@@ -1098,7 +1101,7 @@ class Workspace : public IEngine<T> {
     if (gram_on) {
       enq_gram();
     } else {
-      launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
+      launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ap, D.ctl}, s);
       launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
     }
     if (coop_pcg_ok()) {
@@ -1139,6 +1142,15 @@ class Workspace : public IEngine<T> {
     return coop_state == 1;
   }
   int coop_state = 0;  // 0 unknown, 1 on, 2 off
+  // z~ carried through PCG (admm.cuh zt_pass); QPCG_ZT_RECUR=0 runs the z~
+  // pass after every PCG solve as the reference does
+  static uint32_t zt_recur_enabled() {
+    static const uint32_t on = [] {
+      const char* e = std::getenv("QPCG_ZT_RECUR");
+      return (e && e[0] == '0') ? 0u : 1u;
+    }();
+    return on;
+  }
   void enq_post_pcg(const Handles& H) {
     k_pcg_fin<T><<<grid_for(D.n), kThreads, 0, s>>>(D);
     CK_LAUNCH();
@@ -1148,12 +1160,15 @@ class Workspace : public IEngine<T> {
       launch_spmv_select<T, 1, GatherVec<T>, EpiAdmmStore<T, 1>, 2, GatherAdmm<T>,
                          EpiAdmmStore<T, 2>>(D.A, D.pA, GatherVec<T>{D.xt}, EpiAdmmStore<T, 1>{D},
                                              GatherAdmm<T>{D.g2n}, EpiAdmmStore<T, 2>{D}, s);
-      k_admm_mside<T><<<grid_for(D.m), kThreads, 0, s>>>(D);
+      k_admm_mside<T><<<grid_for(D.m), kThreads, 0, s>>>(D, true);
       CK_LAUNCH();
     } else {
       launch_spmv_select<T, 1, GatherVec<T>, EpiAdmm<T, 1>, 2, GatherAdmm<T>, EpiAdmm<T, 2>>(
           D.A, D.pA, GatherVec<T>{D.xt}, EpiAdmm<T, 1>{D, T(0), T(0), T(0), false},
           GatherAdmm<T>{D.g2n}, EpiAdmm<T, 2>{D, T(0), T(0), T(0), false}, s);
+      // the m-side update when the z~ pass was skipped (decided on the device)
+      k_admm_mside<T><<<grid_for(D.m), kThreads, 0, s>>>(D, false);
+      CK_LAUNCH();
     }
     k_xupdate<T><<<grid_for(D.n), kThreads, 0, s>>>(D, H);
     CK_LAUNCH();
@@ -1634,7 +1649,7 @@ class Workspace : public IEngine<T> {
     hc.error = 0;
     push_ctl();
     CK(cudaMemcpyAsync(D.p, x, sizeof(T) * D.n, cudaMemcpyHostToDevice, s));
-    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
+    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ap, D.ctl}, s);
     launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
     if (kx) CK(cudaMemcpyAsync(kx, D.kp, sizeof(T) * D.n, cudaMemcpyDeviceToHost, s));
     if (dinv) CK(cudaMemcpyAsync(dinv, D.dinv, sizeof(T) * D.n, cudaMemcpyDeviceToHost, s));
@@ -1670,7 +1685,7 @@ class Workspace : public IEngine<T> {
         push_ctl();
         CK(cudaEventRecord(ev[2 * i], s));
         if (which == 0)
-          launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
+          launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ap, D.ctl}, s);
         else if (which == 1)
           launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
         else if (which == 2)
@@ -1839,7 +1854,7 @@ class Workspace : public IEngine<T> {
     push_ctl();
     // r0 = K x0 - b (linsys.hpp:219-220): the passes read p
     CK(cudaMemcpyAsync(D.p, D.xt, sizeof(T) * n, cudaMemcpyDeviceToDevice, s));
-    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ctl, T(0)}, s);
+    launch_spmv<T, 1, SumOp>(D.A, D.pA, GatherVec<T>{D.p}, EpiAp<T>{D.t, D.ap, D.ctl}, s);
     launch_spmv<T, 1, SumOp>(D.AT, D.pAT, GatherVec<T>{D.t}, EpiKp<T>{D, T(0)}, s);
     {
       T *r = D.r, *kp = D.kp;

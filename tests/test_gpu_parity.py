@@ -77,7 +77,11 @@ def test_classes_f32(cls, scale):
 @pytest.mark.parametrize("cls", ["lasso", "svm", "random", "control"])
 def test_default_settings_status_match(cls):
     p = G.generate(cls, 4, 0)
-    s = Settings(max_admm_iter=2000)
+    # random converges near 2000 iterations, and its count moves by ~25 % under
+    # a mere reordering of the same instance (oracle: 1825, reversed twin 1635;
+    # seed 1: 2340 vs 1775), so a 2000 cap sits inside its own noise band: it
+    # runs to the reference's default cap (settings.hpp:33)
+    s = Settings(max_admm_iter=50000 if cls == "random" else 2000)
     g = solver.solve(p, s, device=0)
     o = O.oracle_solve(p, s)
     assert g.status == o.status
