@@ -45,8 +45,10 @@ struct Ctl {
   // reductions / diagnostics
   uint32_t red_counter, n_calls, n_checks, n_rho;
   uint32_t inf_branch, rho_branch, diag_cap, n_inf, n_rho_branch;
-  // 1: z~ = A x~ carried through PCG as z~ += alpha_k (A p_k) (see zt_pass)
-  uint32_t zt_recur;
+  // z~ = A x~ carried through PCG as z~ += alpha_k (A p_k) (see zt_pass):
+  // zt_recur enables it; zt_acc: this PCG solve carries it (decided at its
+  // start: the previous solve took <= zt_kmax iterations); k_last: that count
+  uint32_t zt_recur, zt_acc, zt_kmax, k_last;
 };
 
 // diagnostics records (device side, converted to qpcg_pcg_call on the host)
@@ -325,7 +327,7 @@ struct EpiAp {
   bool keep = false;
   __device__ __forceinline__ bool init() {
     rho = ctl->rho;
-    keep = ap != nullptr && ctl->zt_recur != 0;
+    keep = ap != nullptr && ctl->zt_acc != 0;
     return ctl->pcg_active != 0 && ctl->error == 0;
   }
   __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const {
@@ -362,10 +364,14 @@ struct EpiKp {
 // the 2-column pass also forms A x_new for the residuals (which therefore stay
 // the reference's direct products, and the carried rounding restarts every
 // check_interval steps), and when PCG did not return its last iterate (cap:
-// best iterate; b == 0: zero).
+// best iterate; b == 0: zero).  Carrying costs three m-vector accesses per
+// PCG iteration against one A pass per ADMM step, so a solve carries it only
+// when the previous solve took at most zt_kmax iterations (the break-even
+// count from the sizes, set on the host): the PCG-heavy portfolio steps
+// (~120 iterations each) run the pass instead.
 template <typename T>
 __device__ __forceinline__ bool zt_pass(const Ctl<T>* C) {
-  return C->zt_recur == 0 || C->pcg_exit != kPcgConverged ||
+  return C->zt_acc == 0 || C->pcg_exit != kPcgConverged ||
          ((C->iter + 1) % C->check_interval) == 0;
 }
 
@@ -653,6 +659,7 @@ __device__ void pcg_init_decide(Ctl<T>* C, const T (&tot)[4], Handles H) {
   C->k = 0;
   C->improved = 0;
   C->pcg_exit = kPcgConverged;
+  C->zt_acc = C->zt_recur != 0 && C->k_last <= C->zt_kmax;
   uint32_t active = 0;
   if (tot[3] != T(0)) {
     C->error = kErrInvalid;  // pcg: warm start must be finite (linsys.hpp:203-205)
@@ -739,7 +746,7 @@ __device__ __forceinline__ void pcg_update_elems(const Dev<T>& D, uint32_t t0, u
             v[0] += ri * yi;
             v[1] = smax(v[1], tabs(ri));
           });
-  if (D.ctl->zt_recur)  // z~ += a (A p)  (zt_pass)
+  if (D.ctl->zt_acc)  // z~ += a (A p)  (zt_pass)
     strided(t0, stride, D.m, [&](uint32_t j) { return V2<T>{D.zt[j], D.ap[j]}; },
             [&](uint32_t j, const V2<T>& e) { D.zt[j] = e.a + a * e.b; });
 }
@@ -871,6 +878,7 @@ template <typename T>
 __device__ void pcg_fin_book(const Dev<T>& D, bool record) {
   Ctl<T>* C = D.ctl;
   C->pcg_total += C->k;
+  C->k_last = C->k;
   if (record && C->n_calls < C->diag_cap) {
     DiagRec<T> rec;
     rec.admm_iter = C->iter + 1;

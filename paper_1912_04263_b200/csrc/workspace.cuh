@@ -826,6 +826,12 @@ class Workspace : public IEngine<T> {
     hc.status = QPCG_STATUS_MAX_ITER_REACHED;
     hc.diag_cap = cap;
     hc.zt_recur = zt_recur_enabled();
+    {  // break-even PCG count: one A pass vs (3 m-vector accesses + ~8 MB of
+       // tail latency at the HBM rate) per carried iteration
+      const double pass = plan_stream_bytes(D.A, D.pA) + double(n) * sizeof(T);
+      const double per_it = 3.0 * double(m) * sizeof(T) + 8e6;
+      hc.zt_kmax = uint32_t(std::min(pass / per_it, 1e9));
+    }
     push_ctl();
     k_precond<T><<<grid_for(n), kThreads, 0, s>>>(D, 1);
     CK_LAUNCH();
