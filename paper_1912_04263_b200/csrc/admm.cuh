@@ -49,6 +49,7 @@ struct Ctl {
   // zt_recur enables it; zt_acc: this PCG solve carries it (decided at its
   // start: the previous solve took <= zt_kmax iterations); k_last: that count
   uint32_t zt_recur, zt_acc, zt_kmax, k_last;
+  uint32_t n_zt;  // z~ passes run (graph launch accounting)
 };
 
 // diagnostics records (device side, converted to qpcg_pcg_call on the host)
@@ -66,7 +67,7 @@ struct RhoRec {
 
 // Handles of the CUDA-graph conditional nodes (0 in eager mode).
 struct Handles {
-  unsigned long long admm = 0, pcg = 0, chk = 0, inf = 0, rho = 0;
+  unsigned long long admm = 0, pcg = 0, chk = 0, inf = 0, rho = 0, zt = 0;
 };
 
 __device__ __forceinline__ void set_cond(unsigned long long h, unsigned int v) {
@@ -879,6 +880,7 @@ __device__ void pcg_fin_book(const Dev<T>& D, bool record) {
   Ctl<T>* C = D.ctl;
   C->pcg_total += C->k;
   C->k_last = C->k;
+  if (zt_pass(C)) C->n_zt += 1;
   if (record && C->n_calls < C->diag_cap) {
     DiagRec<T> rec;
     rec.admm_iter = C->iter + 1;
@@ -893,7 +895,9 @@ __device__ void pcg_fin_book(const Dev<T>& D, bool record) {
   C->n_calls += 1;
 }
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_pcg_fin(Dev<T> D) {
+__global__ void __launch_bounds__(kThreads) k_pcg_fin(Dev<T> D, Handles H) {
+  if (blockIdx.x == 0 && threadIdx.x == 0)  // the graph's IF node around the z~ pass
+    set_cond(H.zt, D.ctl->error == 0 && zt_pass(D.ctl));
   if (D.ctl->error) return;
   pcg_fin_elems(D, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
   if (blockIdx.x == 0 && threadIdx.x == 0) pcg_fin_book(D, true);

@@ -1157,25 +1157,35 @@ class Workspace : public IEngine<T> {
     }();
     return on;
   }
+  // After PCG: k_pcg_fin, the z~ pass (skipped on the device when z~ was
+  // carried, admm.cuh zt_pass; in the graph it sits in an IF node, so a
+  // skipped pass launches nothing), the m-side update, the n-side update.
   void enq_post_pcg(const Handles& H) {
-    k_pcg_fin<T><<<grid_for(D.n), kThreads, 0, s>>>(D);
+    enq_pcg_fin(H);
+    enq_zt_pass();
+    enq_post_zt(H);
+  }
+  void enq_pcg_fin(const Handles& H) {
+    k_pcg_fin<T><<<grid_for(D.n), kThreads, 0, s>>>(D, H);
     CK_LAUNCH();
-    // z~ = A x~ with the m-side update: the 2-column build on check
-    // iterations (col 1 = A x_new), else the 1-column one; one launch
-    if (D.pA.u8) {  // short rows: the m-side update as a row-parallel pass (EpiAdmmStore)
+  }
+  // z~ = A x~ with the m-side update: the 2-column build on check iterations
+  // (col 1 = A x_new), else the 1-column one; one launch
+  void enq_zt_pass() {
+    if (D.pA.u8)  // short rows: the m-side update as a row-parallel pass (EpiAdmmStore)
       launch_spmv_select<T, 1, GatherVec<T>, EpiAdmmStore<T, 1>, 2, GatherAdmm<T>,
                          EpiAdmmStore<T, 2>>(D.A, D.pA, GatherVec<T>{D.xt}, EpiAdmmStore<T, 1>{D},
                                              GatherAdmm<T>{D.g2n}, EpiAdmmStore<T, 2>{D}, s);
-      k_admm_mside<T><<<grid_for(D.m), kThreads, 0, s>>>(D, true);
-      CK_LAUNCH();
-    } else {
+    else
       launch_spmv_select<T, 1, GatherVec<T>, EpiAdmm<T, 1>, 2, GatherAdmm<T>, EpiAdmm<T, 2>>(
           D.A, D.pA, GatherVec<T>{D.xt}, EpiAdmm<T, 1>{D, T(0), T(0), T(0), false},
           GatherAdmm<T>{D.g2n}, EpiAdmm<T, 2>{D, T(0), T(0), T(0), false}, s);
-      // the m-side update when the z~ pass was skipped (decided on the device)
-      k_admm_mside<T><<<grid_for(D.m), kThreads, 0, s>>>(D, false);
-      CK_LAUNCH();
-    }
+  }
+  void enq_post_zt(const Handles& H) {
+    // short-row plans: always (EpiAdmmStore only stored z~); else only when
+    // the z~ pass was skipped (its fused epilogue did not run)
+    k_admm_mside<T><<<grid_for(D.m), kThreads, 0, s>>>(D, D.pA.u8 != 0);
+    CK_LAUNCH();
     k_xupdate<T><<<grid_for(D.n), kThreads, 0, s>>>(D, H);
     CK_LAUNCH();
   }
@@ -1238,10 +1248,10 @@ class Workspace : public IEngine<T> {
     return cp.conditional.phGraph_out[0];
   }
 
-  uint64_t body_kernels[5] = {};  // per execution: ADMM step, PCG iteration, check, infeas, rho
+  uint64_t body_kernels[6] = {};  // per execution: ADMM step, PCG iteration, check, infeas, rho, z~ pass
   void build_graph() {
     CK(cudaGraphCreate(&graph, 0));
-    cudaGraphConditionalHandle h_admm, h_pcg, h_chk, h_inf, h_rho;
+    cudaGraphConditionalHandle h_admm, h_pcg, h_chk, h_inf, h_rho, h_zt;
     CK(cudaGraphConditionalHandleCreate(&h_admm, graph, 1, cudaGraphCondAssignDefault));
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
@@ -1254,12 +1264,14 @@ class Workspace : public IEngine<T> {
     CK(cudaGraphConditionalHandleCreate(&h_pcg, b_admm, 0, cudaGraphCondAssignDefault));
     CK(cudaGraphConditionalHandleCreate(&h_chk, b_admm, 0, cudaGraphCondAssignDefault));
     CK(cudaGraphConditionalHandleCreate(&h_rho, b_admm, 0, cudaGraphCondAssignDefault));
+    CK(cudaGraphConditionalHandleCreate(&h_zt, b_admm, 0, cudaGraphCondAssignDefault));
     Handles H;
+    H.zt = (unsigned long long)h_zt;
     H.admm = (unsigned long long)h_admm;
     H.pcg = (unsigned long long)h_pcg;
     H.chk = (unsigned long long)h_chk;
     H.rho = (unsigned long long)h_rho;
-    cudaGraph_t b_pcg, b_chk, b_rho, b_inf, g_out;
+    cudaGraph_t b_pcg, b_chk, b_rho, b_inf, b_zt, g_out;
     // kernels per execution of each body, counted as they are captured
     // (the solve's launch count multiplies them by the executions)
     uint64_t c0 = g_launches;
@@ -1267,7 +1279,9 @@ class Workspace : public IEngine<T> {
     enq_rhs(H);
     enq_pcg_init(H);
     b_pcg = add_cond_in_capture(h_pcg, cudaGraphCondTypeWhile);
-    enq_post_pcg(H);
+    enq_pcg_fin(H);
+    b_zt = add_cond_in_capture(h_zt, cudaGraphCondTypeIf);
+    enq_post_zt(H);
     b_chk = add_cond_in_capture(h_chk, cudaGraphCondTypeIf);
     enq_rho_flag(H);
     b_rho = add_cond_in_capture(h_rho, cudaGraphCondTypeIf);
@@ -1279,6 +1293,11 @@ class Workspace : public IEngine<T> {
     enq_pcg_iter(H);
     CK(cudaStreamEndCapture(s, &g_out));
     body_kernels[1] = g_launches - c0;
+    c0 = g_launches;
+    CK(cudaStreamBeginCaptureToGraph(s, b_zt, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    enq_zt_pass();
+    CK(cudaStreamEndCapture(s, &g_out));
+    body_kernels[5] = g_launches - c0;
     CK(cudaGraphConditionalHandleCreate(&h_inf, b_chk, 0, cudaGraphCondAssignDefault));
     H.inf = (unsigned long long)h_inf;
     c0 = g_launches;
@@ -1464,6 +1483,8 @@ class Workspace : public IEngine<T> {
     hc.red_counter = 0;
     hc.n_inf = 0;
     hc.n_rho_branch = 0;
+    hc.n_zt = 0;
+    hc.k_last = 0;  // the first PCG solve carries z~ (a fresh workspace's state)
     push_ctl();
   }
   void raise_device_error() {
@@ -1546,7 +1567,7 @@ class Workspace : public IEngine<T> {
     if (opt.mode != QPCG_MODE_EAGER && !use_persistent())  // kernels executed inside the graph
       launches += body_kernels[0] * hc.iter + body_kernels[1] * hc.pcg_total +
                   body_kernels[2] * hc.n_checks + body_kernels[3] * hc.n_inf +
-                  body_kernels[4] * hc.n_rho_branch;
+                  body_kernels[4] * hc.n_rho_branch + body_kernels[5] * hc.n_zt;
     if (has_cert) download(cert, D.cert, sizeof(T) * (hc.status == 1 ? D.m : D.n));
     CK(cudaStreamSynchronize(s));
     const double d2h = now_s() - td;
@@ -1882,7 +1903,7 @@ class Workspace : public IEngine<T> {
       throw NotPositiveDefinite("pcg: encountered direction of nonpositive curvature");
     if (hc.error == kErrRho) throw InvalidArgument("kkt operator: rho must be positive");
     if (hc.error == kErrInvalid) throw InvalidArgument("pcg: warm start must be finite");
-    k_pcg_fin<T><<<grid_for(n), kThreads, 0, s>>>(D);
+    k_pcg_fin<T><<<grid_for(n), kThreads, 0, s>>>(D, Handles{});
     CK_LAUNCH();
     download(x, D.xt, sizeof(T) * n);
     CK(cudaStreamSynchronize(s));
