@@ -50,6 +50,9 @@ struct Ctl {
   // start: the previous solve took <= zt_kmax iterations); k_last: that count
   uint32_t zt_recur, zt_acc, zt_kmax, k_last;
   uint32_t n_zt;  // z~ passes run (graph launch accounting)
+  // w = A^T (rho z~) carried alongside z~ (w += alpha_k A^T t_k): w_recur
+  // enables it; w_valid: the next rhs pass may take r0's column from w
+  uint32_t w_recur, w_valid;
 };
 
 // diagnostics records (device side, converted to qpcg_pcg_call on the host)
@@ -93,6 +96,8 @@ struct Dev {
   // PCG workspace
   T *b, *r, *p, *kp, *best, *dinv, *t, *diag_p, *diag_ata;
   T* ap;  // [m] A p of the current PCG iteration (unscaled by rho), for the z~ recurrence
+  T *atp, *w;  // [n] A^T t of the current PCG iteration; carried A^T (rho z~)
+  T* g1m;      // [m] rho z - y (the one-column rhs pass's gather)
   // residual workspace (ResidualData, solver.hpp:181-188)
   T *ax, *px, *aty, *rdual;
   // outputs (unscaled)
@@ -276,9 +281,18 @@ struct GatherRhs {
   }
 };
 // {rho z - y, rho z~} (solver.hpp:351; linsys.hpp:84-85 with A x~ = z~)
+// (rhs_one: only rho z - y, the r0 column comes from the carried w)
+template <typename T>
+__device__ __forceinline__ bool rhs_one(const Ctl<T>* C) {
+  return C->w_recur != 0 && C->w_valid != 0;
+}
 template <typename T>
 __device__ __forceinline__ void pack_rhs_elems(const Dev<T>& D, uint32_t t0, uint32_t stride) {
   const T rho = D.ctl->rho;
+  if (rhs_one(D.ctl)) {
+    for (uint32_t i = t0; i < D.m; i += stride) D.g1m[i] = rho * D.z[i] - D.y[i];
+    return;
+  }
   for (uint32_t i = t0; i < D.m; i += stride) {
     pair_t<T> v;
     v.x = rho * D.z[i] - D.y[i];
@@ -299,13 +313,16 @@ __device__ __forceinline__ void rhs_row(const Dev<T>& D, T sigma, uint32_t r, T 
   D.b[r] = rhs;
   D.r[r] = kx - rhs;
 }
+// two columns: rhs and r0's A^T (rho z~), which also (re)starts the carried w
 template <typename T>
 struct EpiRhs {
   Dev<T> D;
   T sigma;
+  bool keep = false;
   __device__ __forceinline__ bool init() {
     sigma = D.ctl->sigma;
-    return D.ctl->error == 0;
+    keep = D.ctl->w_recur != 0;
+    return D.ctl->error == 0 && !rhs_one(D.ctl);
   }
   __device__ __forceinline__ void prefetch(uint32_t r) const {
     prefetch_l1(D.x + r);
@@ -314,6 +331,26 @@ struct EpiRhs {
   }
   __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[2]) const {
     rhs_row(D, sigma, r, s[0], s[1]);
+    if (keep) D.w[r] = s[1];
+  }
+};
+// one column (rho z - y): r0's A^T (rho z~) is the carried w (see zt_pass)
+template <typename T>
+struct EpiRhs1 {
+  Dev<T> D;
+  T sigma;
+  __device__ __forceinline__ bool init() {
+    sigma = D.ctl->sigma;
+    return D.ctl->error == 0 && rhs_one(D.ctl);
+  }
+  __device__ __forceinline__ void prefetch(uint32_t r) const {
+    prefetch_l1(D.x + r);
+    prefetch_l1(D.q + r);
+    prefetch_l1(D.xt + r);
+    prefetch_l1(D.w + r);
+  }
+  __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const {
+    rhs_row(D, sigma, r, s[0], D.w[r]);
   }
 };
 
@@ -346,12 +383,15 @@ template <typename T>
 struct EpiKp {
   Dev<T> D;
   T sigma;
+  bool keep = false;  // A^T t kept for the carried w
   __device__ __forceinline__ bool init() {
     sigma = D.ctl->sigma;
+    keep = D.ctl->w_recur != 0 && D.ctl->zt_acc != 0;
     return D.ctl->pcg_active != 0 && D.ctl->error == 0;
   }
   __device__ __forceinline__ void operator()(uint32_t r, const T (&s)[1]) const {
     D.kp[r] = kp_row(D, sigma, r, s[0]);
+    if (keep) D.atp[r] = s[0];
   }
 };
 
@@ -747,9 +787,13 @@ __device__ __forceinline__ void pcg_update_elems(const Dev<T>& D, uint32_t t0, u
             v[0] += ri * yi;
             v[1] = smax(v[1], tabs(ri));
           });
-  if (D.ctl->zt_acc)  // z~ += a (A p)  (zt_pass)
+  if (D.ctl->zt_acc) {  // z~ += a (A p)  (zt_pass)
     strided(t0, stride, D.m, [&](uint32_t j) { return V2<T>{D.zt[j], D.ap[j]}; },
             [&](uint32_t j, const V2<T>& e) { D.zt[j] = e.a + a * e.b; });
+    if (D.ctl->w_recur)  // w += a (A^T t), i.e. A^T (rho z~) with the same rho
+      strided(t0, stride, D.n, [&](uint32_t i) { return V2<T>{D.w[i], D.atp[i]}; },
+              [&](uint32_t i, const V2<T>& e) { D.w[i] = e.a + a * e.b; });
+  }
 }
 template <typename T>
 __device__ void pcg_update_decide(Ctl<T>* C, const T (&tot)[2], Handles H) {
@@ -880,7 +924,11 @@ __device__ void pcg_fin_book(const Dev<T>& D, bool record) {
   Ctl<T>* C = D.ctl;
   C->pcg_total += C->k;
   C->k_last = C->k;
-  if (zt_pass(C)) C->n_zt += 1;
+  const bool pass = zt_pass(C);
+  if (pass) C->n_zt += 1;
+  // w carried through this whole solve and not restarted by a z~ pass: the
+  // next rhs pass takes r0's column from it (a rho change clears it)
+  C->w_valid = C->w_recur != 0 && C->zt_acc != 0 && !pass;
   if (record && C->n_calls < C->diag_cap) {
     DiagRec<T> rec;
     rec.admm_iter = C->iter + 1;
@@ -1200,6 +1248,7 @@ __device__ void rho_decide(Dev<T> D, T z_inf, bool record = true) {
     D.rhos[C->n_rho] = rr;
   }
   C->n_rho += 1;
+  C->w_valid = 0;  // w = A^T (rho z~) holds the old rho
   if (!(next > T(0))) {
     C->error = kErrRho;  // kkt operator: rho must be positive
     C->done = 1;

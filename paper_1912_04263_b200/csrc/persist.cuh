@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_admm_persistent(Dev<T> Dg, Pers
     if (!C->error) pack_rhs_elems(D, t0, stride);
     grid.sync();
     spmv_phase<T, 2, SumOp>(grid, D.AT, D.pAT, GatherRhs<T, false>{D.g2m}, EpiRhs<T>{D, T(0)});
+    spmv_phase<T, 1, SumOp>(grid, D.AT, D.pAT, GatherVec<T, false>{D.g1m}, EpiRhs1<T>{D, T(0)});
     grid.sync();
     if (!C->error) {  // k_pcg_init
       T tot[4];

@@ -788,6 +788,11 @@ class Workspace : public IEngine<T> {
     D.xo = vec(n); D.pxo = vec(n);
     D.z = vec(m); D.y = vec(m); D.zt = vec(m); D.dy = vec(m); D.t = vec(m); D.ax = vec(m);
     D.zo = vec(m); D.yo = vec(m); D.ap = vec(m);
+    if (!D.split) {  // the carried w (the row-sharded rhs pass keeps its two columns)
+      D.atp = vec(n);
+      D.w = vec(n);
+      D.g1m = vec(m);
+    }
     D.cert = vec(std::max(n, m));
     D.g2m = alloc<pair_t<T>>(m);
     D.g2n = alloc<pair_t<T>>(n);
@@ -826,6 +831,7 @@ class Workspace : public IEngine<T> {
     hc.status = QPCG_STATUS_MAX_ITER_REACHED;
     hc.diag_cap = cap;
     hc.zt_recur = zt_recur_enabled();
+    hc.w_recur = hc.zt_recur && !D.split;
     {  // break-even PCG count: one A pass vs (3 m-vector accesses + ~8 MB of
        // tail latency at the HBM rate) per carried iteration
       const double pass = plan_stream_bytes(D.A, D.pA) + double(n) * sizeof(T);
@@ -1068,6 +1074,7 @@ class Workspace : public IEngine<T> {
     }
     gram_on = true;
     hc.zt_recur = 0;  // the one-pass apply forms A p inside the Gram product, not kept
+    hc.w_recur = 0;
     push_ctl();
     if (const char* tr = std::getenv("QPCG_GRAM_TRACE"); tr && tr[0] == '1')
       std::fprintf(stderr,
@@ -1094,10 +1101,14 @@ class Workspace : public IEngine<T> {
   }
 
   // ------------------------------------------------------ enqueue helpers
+  // rhs + r0: the 2-column pass, or 1 column when r0's A^T (rho z~) is the
+  // carried w (admm.cuh rhs_one; decided on the device, one launch)
   void enq_rhs(const Handles&) {
     k_pack_rhs<T><<<grid_for(D.m), kThreads, 0, s>>>(D);
     CK_LAUNCH();
-    launch_spmv<T, 2, SumOp>(D.AT, D.pAT, GatherRhs<T>{D.g2m}, EpiRhs<T>{D, T(0)}, s);
+    launch_spmv_select<T, 1, GatherVec<T>, EpiRhs1<T>, 2, GatherRhs<T>, EpiRhs<T>>(
+        D.AT, D.pAT, GatherVec<T>{D.g1m}, EpiRhs1<T>{D, T(0)}, GatherRhs<T>{D.g2m},
+        EpiRhs<T>{D, T(0)}, s);
   }
   void enq_pcg_init(const Handles& H) {
     k_pcg_init<T><<<red_grid<T>(D.n), kThreads, 0, s>>>(D, H);
@@ -1485,6 +1496,7 @@ class Workspace : public IEngine<T> {
     hc.n_rho_branch = 0;
     hc.n_zt = 0;
     hc.k_last = 0;  // the first PCG solve carries z~ (a fresh workspace's state)
+    hc.w_valid = 0;  // and the first rhs pass forms both columns
     push_ctl();
   }
   void raise_device_error() {
@@ -1633,6 +1645,7 @@ class Workspace : public IEngine<T> {
     CK(cudaSetDevice(device));
     pull_ctl();
     hc.rho = rho;
+    hc.w_valid = 0;
     push_ctl();
     k_precond<T><<<grid_for(D.n), kThreads, 0, s>>>(D, 1);
     CK_LAUNCH();
