@@ -1,8 +1,10 @@
-"""z~ carried through PCG (csrc/admm.cuh zt_pass) against the reference's
-per-step z~ = A x~ pass (solver.hpp:359), selected per process by
-QPCG_ZT_RECUR: the same solve in two processes must give the same status and
-iteration count and agree to rounding noise (the carried z~ differs from the
-direct product in the last bits only; the pass reruns on every check iteration)."""
+"""z~ and r0's A^T (rho z~) carried through PCG (csrc/admm.cuh zt_pass,
+rhs_one) against the reference's per-step z~ = A x~ pass (solver.hpp:359) and
+two-column rhs/r0 pass (solver.hpp:351-355, linsys.hpp:218-219), selected per
+process by QPCG_ZT_RECUR: the same solve in two processes must give the same
+status and iteration count and agree to rounding noise (the carried products
+differ from the direct ones in the last bits only; both restart from direct
+products after every check iteration)."""
 import json
 import os
 import subprocess
