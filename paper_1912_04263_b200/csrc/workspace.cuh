@@ -837,6 +837,8 @@ class Workspace : public IEngine<T> {
       const double pass = plan_stream_bytes(D.A, D.pA) + double(n) * sizeof(T);
       const double per_it = 3.0 * double(m) * sizeof(T) + 8e6;
       hc.zt_kmax = uint32_t(std::min(pass / per_it, 1e9));
+      if (const char* e = std::getenv("QPCG_ZT_KMAX"))  // (tests: force the carry on small problems)
+        hc.zt_kmax = uint32_t(std::strtoul(e, nullptr, 10));
     }
     push_ctl();
     k_precond<T><<<grid_for(n), kThreads, 0, s>>>(D, 1);

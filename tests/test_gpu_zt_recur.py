@@ -49,3 +49,49 @@ def test_carried_z_tilde_matches_the_per_step_pass():
     # graph and eager stay bitwise identical with the carried z~
     for i in range(0, len(b), 2):
         assert b[i][3:] == b[i + 1][3:]
+
+
+@pytest.fixture
+def carry_always():
+    """The break-even gate keeps the carry off on small problems (one A pass
+    costs less than the per-iteration carry there); force it on so the carried
+    paths of all three drivers run on every PCG solve."""
+    old = os.environ.get("QPCG_ZT_KMAX")
+    os.environ["QPCG_ZT_KMAX"] = "1000000"
+    yield
+    if old is None:
+        del os.environ["QPCG_ZT_KMAX"]
+    else:
+        os.environ["QPCG_ZT_KMAX"] = old
+
+
+@pytest.mark.parametrize("cls", ["control", "equality", "huber", "lasso", "portfolio", "random",
+                                 "svm"])
+def test_carried_paths_bitwise_across_drivers_and_parity(cls, carry_always):
+    from oracle import oracle as O
+    from paper_1912_04263_b200 import generators as G, solver
+    from paper_1912_04263_b200.problem import Settings
+    from test_gpu_parity import check_parity
+    from test_gpu_persistent import graph_only, same
+    s = Settings(lambda_pcg=0.01)
+    p = G.generate(cls, 5, 1)
+    a = solver.solve(p, s, device=0, mode="persistent")
+    b = graph_only(p, s)
+    c = solver.solve(p, s, device=0, mode="eager")
+    same(a, b)
+    same(a, c)
+    check_parity(p, s, a, O.oracle_solve(p, s))
+
+
+def test_forced_carry_skips_z_tilde_passes(carry_always):
+    """With the carry forced on, the graph launches fewer z~ passes (IF node)."""
+    from paper_1912_04263_b200 import generators as G
+    from paper_1912_04263_b200.problem import Settings
+    from test_gpu_persistent import graph_only
+    s = Settings(lambda_pcg=0.01)
+    p = G.generate("lasso", 5, 1)
+    on = graph_only(p, s)
+    os.environ["QPCG_ZT_KMAX"] = "0"  # carry only after PCG solves of 0 iterations
+    off = graph_only(p, s)
+    assert on.iterations == off.iterations
+    assert on.info["kernel_launches"] < off.info["kernel_launches"]
