@@ -151,6 +151,10 @@ typedef struct {
 #define QPCG_ENGINE_ONE_PASS_OPERATOR 1u /* PCG operator apply with A streamed
                                             once (csrc/gram.cuh) */
 #define QPCG_ENGINE_PERSISTENT 2u        /* the whole loop as one kernel */
+#define QPCG_ENGINE_CARRIED_PRODUCTS 4u  /* z~ = A x~ and r0's A^T (rho z~) carried
+                                            through PCG instead of recomputed every
+                                            ADMM step (QPCG_ZT_RECUR=0
+                                            turns it off) */
 
 #define QPCG_MEM_HOST 0   /* caller arrays are host memory (copied in setup) */
 #define QPCG_MEM_DEVICE 1 /* caller arrays are device memory on `device` */

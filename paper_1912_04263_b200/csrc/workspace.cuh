@@ -1524,7 +1524,8 @@ class Workspace : public IEngine<T> {
     info->n = n;
     info->m = m;
     info->engine_flags = (gram_on ? QPCG_ENGINE_ONE_PASS_OPERATOR : 0u) |
-                         (ran_persistent ? QPCG_ENGINE_PERSISTENT : 0u);
+                         (ran_persistent ? QPCG_ENGINE_PERSISTENT : 0u) |
+                         (hc.zt_recur ? QPCG_ENGINE_CARRIED_PRODUCTS : 0u);
     info->setup_seconds = setup_seconds;
     info->solve_seconds = solve_s;
     info->h2d_seconds = h2d_seconds;

@@ -95,3 +95,4 @@ def test_forced_carry_skips_z_tilde_passes(carry_always):
     off = graph_only(p, s)
     assert on.iterations == off.iterations
     assert on.info["kernel_launches"] < off.info["kernel_launches"]
+    assert on.info["engine_flags"] & 4  # QPCG_ENGINE_CARRIED_PRODUCTS
